@@ -1,0 +1,80 @@
+/*
+ * ssjoin_b200.h -- extensions of libssjoin.so beyond the reference ABI.
+ *
+ * Nothing here is needed by a drop-in client; these entry points expose the
+ * multi-GPU row partition, resident device replicas, per-kernel statistics
+ * and the sketch-build kernel for parity tests.  They never change the
+ * behaviour of the ssj_* entry points in ssjoin.h.
+ */
+#ifndef SSJOIN_B200_H
+#define SSJOIN_B200_H
+
+#include "ssjoin.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Canonical collection from token-id records in CSR form: record r owns
+ * tokens[offsets[r] .. offsets[r+1]).  Same canonicalisation as
+ * ssj_collection_load(SSJ_INPUT_TOKEN_IDS) (reference src/collection.cpp:44-54,
+ * 97-137): per-record sort + dedup, records by (size, tokens), ids as-is. */
+ssj_status ssjb_collection_from_csr(const uint32_t* tokens, const uint64_t* offsets, size_t n,
+                                    ssj_collection** out);
+
+/* Borrowed view of the canonical CSR arrays (valid until the handle is freed). */
+ssj_status ssjb_collection_csr(const ssj_collection* coll, const uint32_t** tokens,
+                               const uint64_t** offsets, size_t* n);
+
+/* Keep a replica of the collection resident in HBM of `device` so later joins
+ * skip the host->device upload; unpin releases it. */
+ssj_status ssjb_collection_pin_device(const ssj_collection* coll, int device);
+ssj_status ssjb_collection_unpin_device(const ssj_collection* coll, int device);
+
+/* The part of a PAR_BITMAP / NAIVE self-join whose later record (id_s) lies in
+ * rows [row_begin, row_end), on one GPU (device < 0: the first configured).
+ * Pairs, counters and saturated_records of disjoint row ranges add up exactly
+ * to the full join's (the multi-GPU / multi-rank shard unit). */
+ssj_status ssjb_join_rows(const ssj_collection* coll, const ssj_join_options* opts,
+                          size_t row_begin, size_t row_end, int device, ssj_report** out);
+
+/* parts+1 row boundaries balancing the length-window pair count of each part. */
+ssj_status ssjb_partition_rows(const ssj_collection* coll, const ssj_join_options* opts,
+                               int parts, uint64_t* bounds);
+
+/* GPUs ssj_join spreads one join over (default: env SSJ_GPUS, else 1). */
+int ssjb_device_count(void);
+ssj_status ssjb_set_devices(int count);
+
+typedef struct ssjb_stats {
+    uint64_t window_pairs;   /* pair comparisons = counters.candidates */
+    uint64_t survivors;      /* filter survivors verified on the GPU */
+    uint64_t batches;        /* survivor-buffer batches */
+    uint64_t launches;       /* kernel launches issued */
+    uint64_t h2d_bytes;      /* host->device bytes copied */
+    uint64_t d2h_bytes;      /* device->host bytes copied */
+    double ms_upload;        /* device event times per phase (max over GPUs) */
+    double ms_build;
+    double ms_filter;
+    double ms_rescan;
+    double ms_verify;
+    double ms_sort;
+    double ms_download;
+    int devices;
+    int filter_kernel;       /* 0 = POPC kernel */
+} ssjb_stats;
+
+ssj_status ssjb_report_stats(const ssj_report* report, ssjb_stats* out);
+
+/* Runs the sketch-build kernel for the collection and copies the sketch store
+ * (n * bits/64 words, row-major) into out_host.  method: SSJ_BITMAP_SET/XOR/NEXT. */
+ssj_status ssjb_build_bitmaps(const ssj_collection* coll, int method, int bits, int hash,
+                              int device, uint64_t* out_host);
+
+const char* ssjb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSJOIN_B200_H */

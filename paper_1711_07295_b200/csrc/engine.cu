@@ -1,0 +1,691 @@
+// Device engine: uploads the canonical CSR collection, runs K1-K4 on one GPU
+// for one row shard of the self-join, and returns sorted pairs plus counters
+// identical to the reference's SSJ_ALGO_PAR_BITMAP (src/parallel_join.cpp:40-140)
+// or SSJ_ALGO_NAIVE (src/join.cpp:91-126).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.cuh"
+
+namespace ssjb {
+
+namespace {
+
+#define CK(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw DeviceError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #expr); \
+    } while (0)
+
+constexpr uint32_t kPadRows = 256;  // sketch/size arrays are padded so TMA stages never read past the end
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return std::strtoull(v, nullptr, 10);
+}
+
+void set_device(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw DeviceError(std::string("no CUDA device available for the B200 join (") +
+                          (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) + ")");
+    if (device < 0 || device >= count)
+        throw DeviceError("CUDA device " + std::to_string(device) + " out of range (" + std::to_string(count) +
+                          " visible)");
+    CK(cudaSetDevice(device));
+    static std::once_flag pool_once[16];
+    std::call_once(pool_once[device & 15], [device]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;  // keep freed blocks cached for the next join
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
+// Stream-ordered allocations freed when the scope ends.
+struct Arena {
+    cudaStream_t stream;
+    std::vector<void*> blocks;
+    explicit Arena(cudaStream_t s) : stream(s) {}
+    template <typename T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream));
+        blocks.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~Arena() {
+        for (void* p : blocks) cudaFreeAsync(p, stream);
+        cudaStreamSynchronize(stream);
+    }
+};
+
+struct Timer {  // device-time spans on one stream
+    cudaStream_t stream;
+    std::vector<cudaEvent_t> evs;
+    explicit Timer(cudaStream_t s) : stream(s) {}
+    cudaEvent_t mark() {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, stream));
+        evs.push_back(e);
+        return e;
+    }
+    static double ms(cudaEvent_t a, cudaEvent_t b) {
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, a, b));
+        return f;
+    }
+    ~Timer() {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+};
+
+void register_host(const Collection& c) {
+    // Page-lock the canonical arrays once so every upload is a pinned DMA.
+    if (c.host_registered) return;
+    if (!c.tokens.empty())
+        cudaHostRegister(const_cast<uint32_t*>(c.tokens.data()), c.tokens.size() * sizeof(uint32_t),
+                         cudaHostRegisterDefault);
+    cudaHostRegister(const_cast<uint64_t*>(c.offsets.data()), c.offsets.size() * sizeof(uint64_t),
+                     cudaHostRegisterDefault);
+    cudaGetLastError();  // registration is an optimisation; ignore failures
+    c.host_registered = true;
+}
+
+}  // namespace
+
+// Device copy of a canonical collection: tokens, offsets and sizes (padded).
+struct DeviceReplica {
+    int device = -1;
+    uint32_t* tokens = nullptr;
+    uint64_t* offsets = nullptr;
+    uint32_t* sizes = nullptr;
+    size_t n = 0;
+    uint64_t bytes = 0;
+    ~DeviceReplica() {
+        if (device >= 0) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(device);
+            cudaFree(tokens);
+            cudaFree(offsets);
+            cudaFree(sizes);
+            cudaSetDevice(cur);
+        }
+    }
+};
+
+namespace {
+
+__global__ void sizes_from_offsets(const uint64_t* off, uint32_t* sizes, size_t n) {
+    size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (r < n) sizes[r] = static_cast<uint32_t>(off[r + 1] - off[r]);
+    else if (r < n + kPadRows) sizes[r] = 0;
+}
+
+std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
+                                      uint64_t& launches) {
+    register_host(c);
+    auto rep = std::make_shared<DeviceReplica>();
+    const size_t n = c.size();
+    CK(cudaMalloc(&rep->tokens, std::max<size_t>(c.tokens.size(), 4) * sizeof(uint32_t) + 16));
+    CK(cudaMalloc(&rep->offsets, (n + 1) * sizeof(uint64_t)));
+    CK(cudaMalloc(&rep->sizes, (n + kPadRows) * sizeof(uint32_t)));
+    rep->device = device;
+    rep->n = n;
+    if (!c.tokens.empty())
+        CK(cudaMemcpyAsync(rep->tokens, c.tokens.data(), c.tokens.size() * sizeof(uint32_t),
+                           cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       stream));
+    rep->bytes = c.tokens.size() * sizeof(uint32_t) + (n + 1) * sizeof(uint64_t);
+    h2d += rep->bytes;
+    const size_t tot = n + kPadRows;
+    sizes_from_offsets<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(rep->offsets, rep->sizes, n);
+    ++launches;
+    CK(cudaGetLastError());
+    return rep;
+}
+
+std::shared_ptr<DeviceReplica> replica_for(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
+                                           uint64_t& launches) {
+    {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        if (c.pinned[device & 15] && c.pinned[device & 15]->device == device) return c.pinned[device & 15];
+        register_host(c);
+    }
+    return upload(c, device, stream, h2d, launches);
+}
+
+// ---------------------------------------------------------------- launchers
+using FilterFn = void (*)(dev::FilterParams);
+using BuildFn = void (*)(dev::BuildParams);
+
+FilterFn filter_fn(int words) {
+    switch (words) {
+        case 1: return dev::filter_kernel<1>;
+        case 2: return dev::filter_kernel<2>;
+        case 3: return dev::filter_kernel<3>;
+        case 4: return dev::filter_kernel<4>;
+        case 5: return dev::filter_kernel<5>;
+        case 6: return dev::filter_kernel<6>;
+        case 7: return dev::filter_kernel<7>;
+        case 8: return dev::filter_kernel<8>;
+        default: return dev::filter_kernel<0>;
+    }
+}
+
+BuildFn build_fn(int words) {
+    switch (words) {
+        case 1: return dev::build_sketches<1>;
+        case 2: return dev::build_sketches<2>;
+        case 3: return dev::build_sketches<3>;
+        case 4: return dev::build_sketches<4>;
+        case 5: return dev::build_sketches<5>;
+        case 6: return dev::build_sketches<6>;
+        case 7: return dev::build_sketches<7>;
+        case 8: return dev::build_sketches<8>;
+        default: return dev::build_sketches<0>;
+    }
+}
+
+int filter_colsub(int words) {
+    if (words <= dev::kMaxInlineWords) return dev::kColSub;
+    int c = (2048 / words) & ~31;
+    return std::max(32, c);
+}
+
+size_t filter_smem(int words) {
+    const size_t cs = static_cast<size_t>(filter_colsub(words));
+    return 2 * cs * words * 8 + 2 * cs * 4 + 4 * dev::kWarpQueue * sizeof(uint2);
+}
+
+void launch_build(const DeviceReplica& rep, uint64_t* bits, Method method, int width, int hash, cudaStream_t s,
+                  uint64_t& launches) {
+    if (rep.n == 0) return;
+    dev::BuildParams P{};
+    P.tokens = rep.tokens;
+    P.offsets = rep.offsets;
+    P.bits = bits;
+    P.n = static_cast<uint32_t>(rep.n);
+    P.width = static_cast<uint32_t>(width);
+    P.words = width / 64;
+    P.method = static_cast<int>(method);
+    P.hash_mult = hash == 1 ? 1 : 0;
+    P.pow2 = (width & (width - 1)) == 0;
+    const unsigned grid = static_cast<unsigned>((rep.n + dev::kBuildRecs - 1) / dev::kBuildRecs);
+    build_fn(P.words)<<<grid, dev::kBuildRecs, 0, s>>>(P);
+    ++launches;
+    CK(cudaGetLastError());
+}
+
+// Sort keys/vals in place by key bits [0, 32+bits) skipping constant bytes;
+// returns the buffer holding the result (a or b).
+struct SortBufs {
+    unsigned long long* ka;
+    uint32_t* va;
+    unsigned long long* kb;
+    uint32_t* vb;
+    uint32_t* hist;
+    uint32_t* sums;
+};
+
+__global__ void small_sort(unsigned long long* keys, uint32_t* vals, uint32_t n) {
+    // single CTA bitonic sort, n <= 4096
+    __shared__ unsigned long long k[4096];
+    __shared__ uint32_t v[4096];
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t t = threadIdx.x; t < m; t += blockDim.x) {
+        k[t] = t < n ? keys[t] : ~0ull;
+        v[t] = t < n ? vals[t] : 0u;
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= m; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t t = threadIdx.x; t < m; t += blockDim.x) {
+                uint32_t p = t ^ stride;
+                if (p > t) {
+                    bool up = (t & size) == 0;
+                    if ((k[t] > k[p]) == up) {
+                        unsigned long long tk = k[t];
+                        k[t] = k[p];
+                        k[p] = tk;
+                        uint32_t tv = v[t];
+                        v[t] = v[p];
+                        v[p] = tv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+        keys[t] = k[t];
+        vals[t] = v[t];
+    }
+}
+
+bool sort_results(SortBufs& B, unsigned long long n, int idbits, cudaStream_t s, uint64_t& launches) {
+    // returns true when the sorted data ended in (kb, vb)
+    if (n <= 1) return false;
+    if (n <= 4096) {
+        small_sort<<<1, 1024, 0, s>>>(B.ka, B.va, static_cast<uint32_t>(n));
+        ++launches;
+        CK(cudaGetLastError());
+        return false;
+    }
+    const uint32_t ntiles = static_cast<uint32_t>((n + dev::kSortTile - 1) / dev::kSortTile);
+    const uint32_t hlen = 256u * ntiles;
+    const uint32_t nblk = (hlen + dev::kScanBlock - 1) / dev::kScanBlock;
+    std::vector<int> shifts;
+    for (int sh = 0; sh < idbits; sh += 8) shifts.push_back(sh);
+    for (int sh = 0; sh < idbits; sh += 8) shifts.push_back(32 + sh);
+    bool flip = false;
+    for (int sh : shifts) {
+        unsigned long long* kin = flip ? B.kb : B.ka;
+        uint32_t* vin = flip ? B.vb : B.va;
+        unsigned long long* kout = flip ? B.ka : B.kb;
+        uint32_t* vout = flip ? B.va : B.vb;
+        dev::radix_hist<<<ntiles, dev::kSortThreads, 0, s>>>(kin, n, sh, B.hist, ntiles);
+        if (nblk == 1) {
+            dev::scan_single<<<1, dev::kScanBlock, 0, s>>>(B.hist, hlen);
+            launches += 1;
+        } else {
+            dev::scan_blocks<<<nblk, dev::kScanBlock, 0, s>>>(B.hist, hlen, B.sums);
+            dev::scan_single<<<1, dev::kScanBlock, 0, s>>>(B.sums, nblk);
+            dev::scan_add<<<nblk, dev::kScanBlock, 0, s>>>(B.hist, hlen, B.sums);
+            launches += 3;
+        }
+        dev::radix_scatter<<<ntiles, dev::kSortThreads, 0, s>>>(kin, vin, kout, vout, n, sh, B.hist, ntiles);
+        launches += 2;
+        CK(cudaGetLastError());
+        flip = !flip;
+    }
+    return flip;
+}
+
+struct Tiling {
+    uint32_t ntiles = 0;
+    std::vector<uint64_t> item_base;  // ntiles + 1
+    std::vector<uint32_t> col_lo;     // ntiles
+};
+
+Tiling make_tiling(const Collection& c, const JoinPlan& plan) {
+    Tiling t;
+    const size_t rows = plan.row_end - plan.row_begin;
+    t.ntiles = static_cast<uint32_t>((rows + dev::kRowTile - 1) / dev::kRowTile);
+    t.item_base.assign(t.ntiles + 1, 0);
+    t.col_lo.assign(t.ntiles, 0);
+    for (uint32_t k = 0; k < t.ntiles; ++k) {
+        const size_t r0 = plan.row_begin + static_cast<size_t>(k) * dev::kRowTile;
+        const size_t rl = std::min(r0 + dev::kRowTile, plan.row_end) - 1;  // last row
+        const uint32_t j0 = window_start_of(c, plan, r0);                   // smallest j0 of the tile
+        const uint32_t lo = j0 & ~31u;
+        t.col_lo[k] = lo;
+        uint64_t items = 0;
+        if (rl > lo && j0 < rl) items = (rl - lo + dev::kColChunk - 1) / dev::kColChunk;
+        t.item_base[k + 1] = t.item_base[k] + items;
+    }
+    return t;
+}
+
+}  // namespace
+
+int engine_device_count() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+
+void engine_pin(const Collection& c, int device) {
+    set_device(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint64_t h2d = 0, launches = 0;
+    std::shared_ptr<DeviceReplica> rep;
+    {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        register_host(c);
+    }
+    rep = upload(c, device, s, h2d, launches);
+    CK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+    std::lock_guard<std::mutex> lk(c.dev_mu);
+    c.pinned[device & 15] = rep;
+}
+
+void engine_unpin(const Collection& c, int device) {
+    std::lock_guard<std::mutex> lk(c.dev_mu);
+    c.pinned[device & 15].reset();
+}
+
+void engine_release_host(const Collection& c) {
+    if (!c.host_registered) return;
+    if (!c.tokens.empty()) cudaHostUnregister(const_cast<uint32_t*>(c.tokens.data()));
+    cudaHostUnregister(const_cast<uint64_t*>(c.offsets.data()));
+    cudaGetLastError();
+    c.host_registered = false;
+}
+
+void engine_build_bitmaps(const Collection& c, Method method, int width, int hash, int device,
+                          uint64_t* out_host) {
+    set_device(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    {
+        uint64_t h2d = 0, launches = 0;
+        auto rep = replica_for(c, device, s, h2d, launches);
+        Arena A(s);
+        const int W = width / 64;
+        uint64_t* bits = A.alloc<uint64_t>((c.size() + kPadRows) * W);
+        launch_build(*rep, bits, method, width, hash, s, launches);
+        if (c.size())
+            CK(cudaMemcpyAsync(out_host, bits, c.size() * W * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    cudaStreamDestroy(s);
+}
+
+void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
+    using Clock = std::chrono::steady_clock;
+    set_device(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{s};
+    EngineStats& st = out.stats;
+    st.window_pairs = plan.window_pairs;
+    const auto t_start = Clock::now();
+    Timer T(s);
+    Arena A(s);
+
+    const size_t n = c.size();
+    const uint32_t rows = static_cast<uint32_t>(plan.row_end - plan.row_begin);
+    const bool naive = plan.naive;
+    const bool enabled = !naive && plan.bitmap.enabled;
+    const int width = enabled ? plan.bitmap.width : 64;
+    const int W = width / 64;
+    if (enabled && (width <= 0 || width % 64 != 0))
+        throw std::invalid_argument("bitmap width must be a positive multiple of 64");
+    if (enabled && plan.bitmap.cutoff < 0) throw std::invalid_argument("bitmap cutoff must be >= 0");
+
+    cudaEvent_t e0 = T.mark();
+    auto rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
+    // plan tables
+    int32_t* d_maxham = A.alloc<int32_t>(plan.minov.size());
+    int32_t* d_minov = A.alloc<int32_t>(plan.minov.size());
+    uint32_t* d_wstart = A.alloc<uint32_t>(plan.window_start.size());
+    std::vector<int32_t> maxham(plan.minov.size());
+    for (size_t S = 0; S < maxham.size(); ++S) maxham[S] = static_cast<int32_t>(S) - 2 * plan.minov[S];
+    Tiling tl = make_tiling(c, plan);
+    uint64_t* d_item_base = A.alloc<uint64_t>(tl.item_base.size());
+    uint32_t* d_col_lo = A.alloc<uint32_t>(tl.col_lo.size());
+    CK(cudaMemcpyAsync(d_maxham, maxham.data(), maxham.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_minov, plan.minov.data(), plan.minov.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_wstart, plan.window_start.data(), plan.window_start.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_item_base, tl.item_base.data(), tl.item_base.size() * 8, cudaMemcpyHostToDevice, s));
+    if (tl.ntiles) CK(cudaMemcpyAsync(d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4, cudaMemcpyHostToDevice, s));
+    st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4 + tl.item_base.size() * 8 + tl.col_lo.size() * 4;
+    cudaEvent_t e_up = T.mark();
+
+    // K1: sketches
+    uint64_t* d_bits = A.alloc<uint64_t>((n + kPadRows) * W);
+    if (enabled) {
+        CK(cudaMemsetAsync(d_bits + n * W, 0, kPadRows * W * 8, s));
+        launch_build(*rep, d_bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
+    }
+    cudaEvent_t e_build = T.mark();
+
+    // buffers
+    const uint64_t surv_cap = std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << 27), 1u << 20);
+    const uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
+    uint2* d_surv = A.alloc<uint2>(surv_cap);
+    uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
+    uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
+    uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
+    dev::Control* d_ctl = A.alloc<dev::Control>(1);
+    SortBufs SB{};
+    SB.ka = A.alloc<unsigned long long>(res_cap);
+    SB.va = A.alloc<uint32_t>(res_cap);
+    SB.kb = A.alloc<unsigned long long>(res_cap);
+    SB.vb = A.alloc<uint32_t>(res_cap);
+    const uint32_t max_tiles = static_cast<uint32_t>((res_cap + dev::kSortTile - 1) / dev::kSortTile);
+    SB.hist = A.alloc<uint32_t>(256ull * max_tiles);
+    SB.sums = A.alloc<uint32_t>((256ull * max_tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+    CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4, s));
+    CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
+    dev::Control h_ctl{};
+
+    // filter launch configuration
+    const FilterFn ffn = filter_fn(W);
+    const size_t fsmem = filter_smem(W);
+    CK(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+    int sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn, dev::kRowTile, fsmem));
+    per_sm = std::max(per_sm, 1);
+
+    dev::FilterParams FP{};
+    FP.bits = d_bits;
+    FP.sizes = rep->sizes;
+    FP.maxham = d_maxham;
+    FP.wstart = d_wstart;
+    FP.item_base = d_item_base;
+    FP.tile_col_lo = d_col_lo;
+    FP.surv = d_surv;
+    FP.rowcnt = d_rowcnt;
+    FP.ctl = d_ctl;
+    FP.surv_cap = surv_cap;
+    FP.ntiles = tl.ntiles;
+    FP.row_begin = static_cast<uint32_t>(plan.row_begin);
+    FP.row_end = static_cast<uint32_t>(plan.row_end);
+    FP.cutoff = enabled ? plan.bitmap.cutoff : kUnlimited;
+    FP.words = W;
+    FP.colsub = filter_colsub(W);
+    FP.bypass_all = enabled ? 0 : 1;
+    FP.naive = naive ? 1 : 0;
+
+    dev::VerifyParams VP{};
+    VP.tokens = rep->tokens;
+    VP.offsets = rep->offsets;
+    VP.minov = d_minov;
+    VP.surv = d_surv;
+    VP.res_keys = SB.ka;
+    VP.res_ov = SB.va;
+    VP.res_cap = res_cap;
+    VP.ctl = d_ctl;
+
+    std::vector<std::vector<PairOut>> runs;
+    uint64_t res_count = 0;
+    int idbits = 1;
+    while ((uint64_t(1) << idbits) < n + 1) ++idbits;
+
+    auto flush_results = [&](uint64_t count) {
+        // K4 on the current result buffer, then download one sorted run
+        cudaEvent_t a = T.mark();
+        bool inb = sort_results(SB, count, idbits, s, st.launches);
+        cudaEvent_t b = T.mark();
+        std::vector<unsigned long long> keys(count);
+        std::vector<uint32_t> ov(count);
+        if (count) {
+            CK(cudaMemcpyAsync(keys.data(), inb ? SB.kb : SB.ka, count * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(ov.data(), inb ? SB.vb : SB.va, count * 4, cudaMemcpyDeviceToHost, s));
+        }
+        cudaEvent_t d = T.mark();
+        CK(cudaStreamSynchronize(s));
+        st.d2h_bytes += count * 12;
+        st.ms_sort += Timer::ms(a, b);
+        st.ms_download += Timer::ms(b, d);
+        std::vector<PairOut> run(count);
+        for (uint64_t k = 0; k < count; ++k)
+            run[k] = PairOut{static_cast<uint32_t>(keys[k] >> 32), static_cast<uint32_t>(keys[k] & 0xFFFFFFFFu),
+                             static_cast<int64_t>(ov[k])};
+        runs.push_back(std::move(run));
+        CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
+    };
+
+    // batches of work items sized so the survivors fit the buffer
+    const uint64_t total_items = tl.item_base.back();
+    uint64_t ib = 0;
+    uint64_t batch = total_items;
+    double ms_filter = 0, ms_verify = 0;
+    while (ib < total_items) {
+        const uint64_t ie = std::min(total_items, ib + std::max<uint64_t>(batch, 1));
+        // rows touched by this batch (for rollback on overflow)
+        const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
+                                                  tl.item_base.begin() - 1);
+        const uint32_t te = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ie - 1) -
+                                                  tl.item_base.begin() - 1);
+        const uint32_t rb = tb * dev::kRowTile, re = std::min<uint32_t>(rows, (te + 1) * dev::kRowTile);
+        const bool whole = ib == 0 && ie == total_items;
+        if (!whole) CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
+        CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
+        FP.item_begin = ib;
+        FP.item_end = ie;
+        FP.tile_begin = tb;
+        const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms) * per_sm);
+        cudaEvent_t a = T.mark();
+        ffn<<<static_cast<unsigned>(grid), dev::kRowTile, fsmem, s>>>(FP);
+        ++st.launches;
+        CK(cudaGetLastError());
+        cudaEvent_t b = T.mark();
+        CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ms_filter += Timer::ms(a, b);
+        const uint64_t S = h_ctl.survivors;
+        if (S > surv_cap) {
+            // overflow: roll the row counts back and retry a smaller batch
+            if (whole) {
+                CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4ull, s));
+            } else {
+                CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+            }
+            batch = std::max<uint64_t>(1, (ie - ib) * surv_cap / S * 7 / 10);
+            if (batch >= ie - ib) batch = (ie - ib) / 2;
+            continue;
+        }
+        ++st.batches;
+        st.survivors += S;
+        if (S) {
+            if (res_count + S > res_cap) {
+                flush_results(res_count);
+                res_count = 0;
+            }
+            VP.count = S;
+            const unsigned vgrid = static_cast<unsigned>(std::min<uint64_t>((S + 255) / 256, uint64_t(sms) * 16));
+            cudaEvent_t c0 = T.mark();
+            dev::verify_pairs<<<vgrid, 256, 0, s>>>(VP);
+            ++st.launches;
+            CK(cudaGetLastError());
+            cudaEvent_t c1 = T.mark();
+            CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ms_verify += Timer::ms(c0, c1);
+            res_count = h_ctl.results;
+        }
+        // grow the next batch towards the capacity at the observed survivor rate
+        const uint64_t done_items = ie - ib;
+        ib = ie;
+        batch = S ? std::max<uint64_t>(1, static_cast<uint64_t>(double(done_items) * 0.7 * double(surv_cap) / double(S)))
+                  : total_items;
+    }
+
+    // K2b + counters
+    cudaEvent_t r0 = T.mark();
+    if (!naive && rows) {
+        dev::RescanParams RP{};
+        RP.bits = d_bits;
+        RP.sizes = rep->sizes;
+        RP.maxham = d_maxham;
+        RP.wstart = d_wstart;
+        RP.rowcnt = d_rowcnt;
+        RP.jstar = d_jstar;
+        RP.row_begin = static_cast<uint32_t>(plan.row_begin);
+        RP.row_end = static_cast<uint32_t>(plan.row_end);
+        RP.capacity = plan.capacity;
+        RP.cutoff = FP.cutoff;
+        RP.words = W;
+        RP.bypass_all = FP.bypass_all;
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, uint64_t(sms) * 8));
+        dev::rescan_saturated<<<g, 256, 0, s>>>(RP);
+        ++st.launches;
+        CK(cudaGetLastError());
+    }
+    cudaEvent_t r1 = T.mark();
+    if (rows) {
+        dev::CountParams CP{};
+        CP.sizes = rep->sizes;
+        CP.wstart = d_wstart;
+        CP.rowcnt = d_rowcnt;
+        CP.jstar = d_jstar;
+        CP.ctl = d_ctl;
+        CP.row_begin = static_cast<uint32_t>(plan.row_begin);
+        CP.row_end = static_cast<uint32_t>(plan.row_end);
+        CP.capacity = plan.capacity;
+        CP.bitmap_enabled = enabled ? 1 : 0;
+        CP.naive = naive ? 1 : 0;
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 255) / 256, uint64_t(sms) * 4));
+        dev::reduce_counters<<<g, 256, 0, s>>>(CP);
+        ++st.launches;
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    st.ms_rescan = Timer::ms(r0, r1);
+    flush_results(res_count);
+
+    // merge sorted runs (one run unless the result buffer overflowed)
+    if (runs.size() == 1) {
+        out.pairs = std::move(runs[0]);
+    } else {
+        std::vector<PairOut> merged;
+        for (auto& r : runs) {
+            std::vector<PairOut> tmp(merged.size() + r.size());
+            std::merge(merged.begin(), merged.end(), r.begin(), r.end(), tmp.begin(),
+                       [](const PairOut& x, const PairOut& y) {
+                           return x.id_r != y.id_r ? x.id_r < y.id_r : x.id_s < y.id_s;
+                       });
+            merged.swap(tmp);
+        }
+        out.pairs = std::move(merged);
+    }
+
+    out.candidates = plan.window_pairs;
+    out.bitmap_tested = h_ctl.tested;
+    out.pruned_bitmap = h_ctl.pruned;
+    out.verified = h_ctl.verified;
+    out.saturated = h_ctl.saturated;
+    out.matched = out.pairs.size();
+    st.ms_upload = Timer::ms(e0, e_up);
+    st.ms_build = Timer::ms(e_up, e_build);
+    st.ms_filter = ms_filter;
+    st.ms_verify = ms_verify;
+    out.index_s = (st.ms_upload + st.ms_build) * 1e-3;
+    out.candidates_s = (st.ms_filter + st.ms_rescan) * 1e-3;
+    const double total = std::chrono::duration<double>(Clock::now() - t_start).count();
+    out.verify_s = std::max(0.0, total - out.index_s - out.candidates_s);
+    st.filter_kernel = 0;
+}
+
+}  // namespace ssjb

@@ -1,0 +1,50 @@
+// Device engine of the B200 Bitmap-Filter join (implemented in engine.cu).
+//
+// The host (capi.cpp / host_core.cpp) resolves options into a JoinPlan; the
+// engine uploads the canonical CSR collection, runs the four sm_100a kernel
+// stages (sketch build, windowed xor/popcount filter, exact verification,
+// canonical ordering) over the plan's row range on one GPU and returns the
+// sorted pairs plus reference-exact counters.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "host_core.hpp"
+
+namespace ssjb {
+
+struct PairOut {  // layout of ssj_pair (reference include/ssjoin.h:125-129)
+    uint32_t id_r;
+    uint32_t id_s;
+    int64_t overlap;
+};
+static_assert(sizeof(PairOut) == 16, "ssj_pair layout");
+
+struct EngineStats {
+    uint64_t window_pairs = 0, survivors = 0, batches = 0, launches = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    double ms_upload = 0, ms_build = 0, ms_filter = 0, ms_rescan = 0, ms_verify = 0, ms_sort = 0,
+           ms_download = 0;
+    int filter_kernel = 0;
+};
+
+struct EngineResult {
+    std::vector<PairOut> pairs;  // sorted by (id_r, id_s)
+    uint64_t candidates = 0, bitmap_tested = 0, pruned_bitmap = 0, verified = 0, matched = 0;
+    uint64_t saturated = 0;
+    double index_s = 0, candidates_s = 0, verify_s = 0;
+    EngineStats stats;
+};
+
+int engine_device_count();
+// One shard (plan.row_begin..row_end) of a self-join on `device`.
+void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out);
+// The sketch-build kernel alone; copies the store (n * width/64 words) to out_host.
+void engine_build_bitmaps(const Collection& c, Method method, int width, int hash, int device,
+                          uint64_t* out_host);
+void engine_pin(const Collection& c, int device);
+void engine_unpin(const Collection& c, int device);
+void engine_release_host(const Collection& c);  // undo host page registration
+
+}  // namespace ssjb

@@ -1,0 +1,582 @@
+// Host-side core: see host_core.hpp.  Every behaviour that defines record
+// ids, thresholds or error codes cites the reference line it reproduces.
+#include "host_core.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <random>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+
+namespace ssjb {
+
+// ================================================================ rational
+Rational::Rational(int64_t n, int64_t d) : num(n), den(d) {
+    // reference src/rational.hpp:21-26
+    if (den == 0) throw std::invalid_argument("rational: zero denominator");
+    if (den < 0) {
+        num = -num;
+        den = -den;
+    }
+    int64_t g = std::gcd(num < 0 ? -num : num, den);
+    if (g > 1) {
+        num /= g;
+        den /= g;
+    }
+}
+
+namespace {
+int64_t parse_digits(const std::string& s, const char* what) {
+    // <= 18 decimal digits, digits only (reference src/rational.cpp:10-19)
+    if (s.empty() || s.size() > 18) throw std::invalid_argument(std::string("rational: bad ") + what);
+    int64_t v = 0;
+    for (char c : s) {
+        if (c < '0' || c > '9') throw std::invalid_argument(std::string("rational: bad ") + what);
+        v = v * 10 + (c - '0');
+    }
+    return v;
+}
+}  // namespace
+
+Rational parse_rational(const std::string& text) {
+    // reference src/rational.cpp:23-41
+    size_t slash = text.find('/');
+    if (slash != std::string::npos) {
+        int64_t p = parse_digits(text.substr(0, slash), "numerator");
+        int64_t q = parse_digits(text.substr(slash + 1), "denominator");
+        if (q == 0) throw std::invalid_argument("rational: zero denominator");
+        return Rational(p, q);
+    }
+    size_t dot = text.find('.');
+    if (dot == std::string::npos) return Rational(parse_digits(text, "integer"), 1);
+    std::string whole = text.substr(0, dot), frac = text.substr(dot + 1);
+    if (frac.size() > 9) throw std::invalid_argument("rational: too many fractional digits");
+    int64_t w = whole.empty() ? 0 : parse_digits(whole, "integer part");
+    int64_t f = frac.empty() ? 0 : parse_digits(frac, "fractional part");
+    int64_t scale = 1;
+    for (size_t i = 0; i < frac.size(); ++i) scale *= 10;
+    return Rational(w * scale + f, scale);
+}
+
+// ============================================================== similarity
+void validate_threshold(Sim f, const Rational& t) {
+    // reference src/similarity.cpp:18-27
+    if (f == Sim::Overlap) {
+        if (t.den != 1 || t.num < 1)
+            throw std::invalid_argument("overlap threshold must be a positive integer");
+    } else if (t.num <= 0 || Rational(1, 1) < t) {
+        throw std::invalid_argument("normalized threshold must be in (0, 1]");
+    }
+}
+
+Rational jaccard_space(Sim f, const Rational& t) {
+    switch (f) {  // reference src/join.cpp:37-50
+        case Sim::Jaccard: return t;
+        case Sim::Dice:
+        case Sim::Cosine: return Rational(t.num, 2 * t.den - t.num);
+        case Sim::Overlap: break;
+    }
+    throw std::invalid_argument("no jaccard-space equivalent for overlap thresholds");
+}
+
+Method resolve_combined(Method m, const Rational& t) {
+    if (m != Method::Combined) return m;  // reference src/bitmap.cpp:30-36
+    if (t <= Rational(56, 100)) return Method::Next;
+    if (t >= Rational(73, 100)) return Method::Xor;
+    return Method::Set;
+}
+
+// =============================================================== analytics
+double expected_bound(Method m, int b, int64_t n) {
+    // reference src/bounds.cpp:13-35
+    if (b < 1) throw std::invalid_argument("bitmap width must be >= 1");
+    if (n < 0) throw std::invalid_argument("token count must be >= 0");
+    const double bn = static_cast<double>(b), nn = static_cast<double>(n);
+    switch (m) {
+        case Method::Set: {
+            double lx = std::log1p(-1.0 / bn);
+            return nn + bn * std::exp(2.0 * nn * lx) - bn * std::exp(nn * lx);
+        }
+        case Method::Xor: {
+            if (b == 1) return nn - 0.25 * (1.0 - ((2 * n) % 2 == 0 ? 1.0 : -1.0));
+            double lx = std::log1p(-2.0 / bn);
+            return nn - bn / 4.0 * (1.0 - std::exp(2.0 * nn * lx));
+        }
+        case Method::Next: return std::min(nn * nn / bn, nn);
+        case Method::Combined: break;
+    }
+    throw std::invalid_argument("expected_bound needs a concrete method");
+}
+
+namespace {
+// Largest n >= 1 with a monotone predicate true: doubling then bisection,
+// capped at 2^26 (reference src/bounds.cpp:78-92).
+int64_t largest_true(const std::function<bool(int64_t)>& pred) {
+    constexpr int64_t kCap = int64_t{1} << 26;
+    if (!pred(1)) return 0;
+    int64_t lo = 1, hi = 2;
+    while (hi <= kCap && pred(hi)) {
+        lo = hi;
+        hi *= 2;
+    }
+    if (hi > kCap) return kUnlimited;
+    while (lo + 1 < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        (pred(mid) ? lo : hi) = mid;
+    }
+    return lo;
+}
+}  // namespace
+
+int64_t cutoff(Method m, int b, const Rational& t, bool space_jaccard) {
+    // reference src/bounds.cpp:96-107
+    if (t.num <= 0 || Rational(1, 1) < t)
+        throw std::invalid_argument("cutoff threshold must be in (0, 1]");
+    Rational tau = space_jaccard ? Rational(2 * t.num, t.num + t.den) : t;
+    const double td = tau.to_double();
+    return largest_true([&](int64_t n) { return expected_bound(m, b, n) / static_cast<double>(n) <= td; });
+}
+
+int64_t cutoff_for_overlap(Method m, int b, int64_t tau) {
+    if (tau < 1) throw std::invalid_argument("overlap threshold must be >= 1");
+    return largest_true([&](int64_t n) { return expected_bound(m, b, n) <= static_cast<double>(tau); });
+}
+
+namespace {
+uint32_t hash_token(uint32_t t, int width, int hash) {
+    if (hash == 1) return static_cast<uint32_t>(((static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull) >> 33) %
+                                                static_cast<uint64_t>(width));
+    return t % static_cast<uint32_t>(width);
+}
+
+// Host sketch of one record: used only by the Monte-Carlo analytics entry point.
+void host_sketch(std::vector<uint64_t>& row, const std::vector<uint32_t>& toks, int width, Method m) {
+    std::fill(row.begin(), row.end(), 0);
+    const int nw = width / 64;
+    if (m == Method::Next) {
+        if (static_cast<int64_t>(toks.size()) >= width) {
+            std::fill(row.begin(), row.end(), ~0ull);
+            return;
+        }
+        for (uint32_t t : toks) {
+            int bit = static_cast<int>(hash_token(t, width, 0));
+            int word = bit / 64;
+            uint64_t fb = ~row[word] & (~0ull << (bit % 64));
+            for (int step = 0; step <= nw; ++step) {
+                if (fb) {
+                    row[word] |= 1ull << __builtin_ctzll(fb);
+                    break;
+                }
+                word = (word + 1) % nw;
+                fb = ~row[word];
+            }
+        }
+        return;
+    }
+    for (uint32_t t : toks) {
+        uint32_t bit = hash_token(t, width, 0);
+        if (m == Method::Set)
+            row[bit / 64] |= 1ull << (bit % 64);
+        else
+            row[bit / 64] ^= 1ull << (bit % 64);
+    }
+}
+}  // namespace
+
+double monte_carlo_bound(Method m, int b, int64_t n, int64_t trials, uint64_t seed) {
+    // reference src/bounds.cpp:37-71
+    if (trials < 1) throw std::invalid_argument("trials must be >= 1");
+    if (b <= 0 || b % 64 != 0) throw std::invalid_argument("bitmap width must be a positive multiple of 64");
+    if (m == Method::Combined) throw std::invalid_argument("combined method must be resolved before building");
+    if (n < 0) throw std::length_error("token count must be >= 0");
+    std::mt19937_64 rng(seed);
+    const size_t count = static_cast<size_t>(n);
+    std::vector<uint32_t> tr(count), ts(count);
+    std::vector<uint64_t> rr(b / 64), rs(b / 64);
+    std::unordered_set<uint32_t> seen;
+    seen.reserve(2 * count);
+    double total = 0.0;
+    for (int64_t t = 0; t < trials; ++t) {
+        seen.clear();
+        auto draw = [&]() {
+            uint32_t v;
+            do { v = static_cast<uint32_t>(rng()); } while (!seen.insert(v).second);
+            return v;
+        };
+        for (size_t i = 0; i < count; ++i) tr[i] = draw();
+        for (size_t i = 0; i < count; ++i) ts[i] = draw();
+        host_sketch(rr, tr, b, m);
+        host_sketch(rs, ts, b, m);
+        int64_t ham = 0;
+        for (size_t w = 0; w < rr.size(); ++w) ham += __builtin_popcountll(rr[w] ^ rs[w]);
+        total += static_cast<double>(2 * n - ham) / 2.0;
+    }
+    return total / static_cast<double>(trials);
+}
+
+// ============================================================== collection
+int64_t Collection::median_size() const {
+    if (size() == 0) return 0;
+    return rec_size((size() - 1) / 2);  // reference src/collection.cpp:13-17
+}
+
+double Collection::mean_size() const {
+    if (size() == 0) return 0.0;
+    return static_cast<double>(tokens.size()) / static_cast<double>(size());
+}
+
+void canonicalize(Collection& c, std::vector<uint32_t>&& raw, const std::vector<uint64_t>& off) {
+    // reference src/collection.cpp:44-54: per-record sort + dedup, then records
+    // by (size, lexicographic tokens); id = position.
+    const size_t n = off.size() - 1;
+    std::vector<uint32_t> len(n);
+    for (size_t r = 0; r < n; ++r) {
+        auto b = raw.begin() + static_cast<ptrdiff_t>(off[r]);
+        auto e = raw.begin() + static_cast<ptrdiff_t>(off[r + 1]);
+        std::sort(b, e);
+        len[r] = static_cast<uint32_t>(std::unique(b, e) - b);
+    }
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    auto less = [&](uint32_t a, uint32_t b) {
+        if (len[a] != len[b]) return len[a] < len[b];
+        const uint32_t* pa = raw.data() + off[a];
+        const uint32_t* pb = raw.data() + off[b];
+        return std::lexicographical_compare(pa, pa + len[a], pb, pb + len[b]);
+    };
+    std::sort(order.begin(), order.end(), less);
+    c.offsets.assign(n + 1, 0);
+    uint64_t total = 0;
+    for (size_t k = 0; k < n; ++k) {
+        total += len[order[k]];
+        c.offsets[k + 1] = total;
+    }
+    c.tokens.resize(total);
+    c.max_size = 0;
+    for (size_t k = 0; k < n; ++k) {
+        uint32_t r = order[k];
+        std::memcpy(c.tokens.data() + c.offsets[k], raw.data() + off[r], len[r] * sizeof(uint32_t));
+        c.max_size = std::max(c.max_size, len[r]);
+    }
+}
+
+Collection::~Collection() = default;
+
+std::unique_ptr<Collection> collection_from_csr(const uint32_t* tokens, const uint64_t* offsets, size_t n) {
+    std::vector<uint64_t> off(offsets, offsets + n + 1);
+    if (off[0] != 0) {
+        uint64_t base = off[0];
+        for (auto& v : off) v -= base;
+        tokens += base;
+    }
+    for (size_t r = 0; r < n; ++r)
+        if (off[r + 1] < off[r]) throw std::invalid_argument("offsets must be non-decreasing");
+    std::vector<uint32_t> raw(tokens, tokens + off[n]);
+    uint32_t max_id = 0;
+    for (uint32_t t : raw) max_id = std::max(max_id, t);
+    auto c = std::make_unique<Collection>();
+    c->universe = raw.empty() ? 0 : static_cast<uint64_t>(max_id) + 1;
+    canonicalize(*c, std::move(raw), off);
+    return c;
+}
+
+namespace {
+
+std::unique_ptr<Collection> read_id_lines(std::istream& in) {
+    // reference src/collection.cpp:97-137 (ids as-is; line-numbered parse errors)
+    std::vector<uint32_t> raw;
+    std::vector<uint64_t> off{0};
+    std::string line;
+    size_t line_no = 0;
+    uint32_t max_id = 0;
+    bool any = false;
+    while (std::getline(in, line)) {
+        ++line_no;
+        size_t pos = 0;
+        const size_t L = line.size();
+        while (pos < L) {
+            while (pos < L && line[pos] == ' ') ++pos;
+            if (pos >= L) break;
+            size_t end = pos;
+            uint64_t value = 0;
+            while (end < L && line[end] != ' ') {
+                char ch = line[end];
+                if (ch < '0' || ch > '9' || value > 0xFFFFFFFFull)
+                    throw ParseError("parse error at line " + std::to_string(line_no) + ": expected a token id");
+                value = value * 10 + static_cast<uint64_t>(ch - '0');
+                ++end;
+            }
+            if (value > 0xFFFFFFFFull)
+                throw ParseError("parse error at line " + std::to_string(line_no) + ": token id out of range");
+            raw.push_back(static_cast<uint32_t>(value));
+            max_id = std::max(max_id, static_cast<uint32_t>(value));
+            any = true;
+            pos = end;
+        }
+        off.push_back(raw.size());
+    }
+    auto c = std::make_unique<Collection>();
+    c->universe = any ? static_cast<uint64_t>(max_id) + 1 : 0;
+    canonicalize(*c, std::move(raw), off);
+    return c;
+}
+
+std::vector<std::string> tokenize(const std::string& text, int kind, int q) {
+    // reference src/collection.cpp:26-40
+    std::vector<std::string> out;
+    if (kind == 0) {
+        std::istringstream in(text);
+        std::string w;
+        while (in >> w) out.push_back(w);
+        return out;
+    }
+    if (q < 1) throw std::invalid_argument("q-gram size must be >= 1");
+    const size_t qq = static_cast<size_t>(q);
+    if (text.size() < qq) return out;
+    for (size_t i = 0; i + qq <= text.size(); ++i) out.push_back(text.substr(i, qq));
+    return out;
+}
+
+// Rarest-first renumbering with ties broken by token text, then canonical
+// order (reference src/collection.cpp:58-93).  Keys are any totally ordered
+// token type whose order matches the reference's std::string order.
+template <typename Key, typename KeyLess>
+std::unique_ptr<Collection> build_renumbered(std::vector<std::vector<Key>>& sets, KeyLess key_less) {
+    std::unordered_map<Key, uint64_t> freq;
+    for (auto& rec : sets) {
+        std::sort(rec.begin(), rec.end(), key_less);
+        rec.erase(std::unique(rec.begin(), rec.end()), rec.end());
+        for (const auto& t : rec) ++freq[t];
+    }
+    std::vector<std::pair<Key, uint64_t>> order(freq.begin(), freq.end());
+    std::sort(order.begin(), order.end(), [&](const auto& a, const auto& b) {
+        if (a.second != b.second) return a.second < b.second;
+        return key_less(a.first, b.first);
+    });
+    std::unordered_map<Key, uint32_t> ids;
+    ids.reserve(order.size());
+    for (size_t k = 0; k < order.size(); ++k) ids.emplace(order[k].first, static_cast<uint32_t>(k));
+    std::vector<uint32_t> raw;
+    std::vector<uint64_t> off{0};
+    for (const auto& rec : sets) {
+        for (const auto& t : rec) raw.push_back(ids.at(t));
+        off.push_back(raw.size());
+    }
+    auto c = std::make_unique<Collection>();
+    c->universe = order.size();
+    canonicalize(*c, std::move(raw), off);
+    return c;
+}
+
+// Decimal-string order of non-negative integers: the order std::map<std::string>
+// gives the reference generator's std::to_string tokens ("10" < "2").
+bool decimal_less(int64_t a, int64_t b) {
+    char sa[24], sb[24];
+    int la = std::snprintf(sa, sizeof sa, "%lld", static_cast<long long>(a));
+    int lb = std::snprintf(sb, sizeof sb, "%lld", static_cast<long long>(b));
+    int c = std::memcmp(sa, sb, static_cast<size_t>(std::min(la, lb)));
+    return c != 0 ? c < 0 : la < lb;
+}
+
+double uniform01(std::mt19937_64& rng) {
+    return static_cast<double>(rng() >> 11) * 0x1.0p-53;  // reference src/collection.cpp:174-176
+}
+
+int64_t poisson_draw(std::mt19937_64& rng, double mean) {
+    // Knuth with long double, reference src/collection.cpp:180-189
+    long double limit = std::exp(static_cast<long double>(-mean));
+    int64_t k = 0;
+    long double p = 1.0L;
+    do {
+        ++k;
+        p *= static_cast<long double>(uniform01(rng));
+    } while (p > limit);
+    return k - 1;
+}
+
+}  // namespace
+
+std::unique_ptr<Collection> read_collection(const std::string& path, int input_format, int q) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open " + path);
+    if (input_format == 0) return read_id_lines(in);
+    // Any other code is text; q-grams only for SSJ_INPUT_QGRAMS (reference src/capi.cpp:134-140).
+    const int kind = input_format == 2 ? 1 : 0;
+    const int qq = input_format == 2 ? q : 2;
+    std::vector<std::vector<std::string>> sets;
+    std::string line;
+    while (std::getline(in, line)) sets.push_back(tokenize(line, kind, qq));
+    return build_renumbered(sets, std::less<std::string>());
+}
+
+void write_collection(const Collection& c, const std::string& path) {
+    // reference src/collection.cpp:153-168
+    std::ofstream out(path);
+    if (!out) throw IoError("cannot open " + path + " for writing");
+    std::string buf;
+    buf.reserve(1 << 20);
+    char num[16];
+    for (size_t r = 0; r < c.size(); ++r) {
+        for (uint64_t k = c.offsets[r]; k < c.offsets[r + 1]; ++k) {
+            if (k != c.offsets[r]) buf.push_back(' ');
+            int l = std::snprintf(num, sizeof num, "%u", c.tokens[k]);
+            buf.append(num, static_cast<size_t>(l));
+        }
+        buf.push_back('\n');
+        if (buf.size() > (1u << 20)) {
+            out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+            buf.clear();
+        }
+    }
+    out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+    out.flush();
+    if (!out) throw IoError("write failed for " + path);
+}
+
+std::unique_ptr<Collection> generate(const GeneratorConfig& cfg) {
+    // reference src/collection.cpp:193-254: same RNG stream, same draws, same
+    // renumbering (tokens are the decimal strings of the drawn ranks).
+    if (cfg.num_sets <= 0) throw std::invalid_argument("generator: num_sets must be > 0");
+    if (cfg.mean_size <= 0) throw std::invalid_argument("generator: mean_size must be > 0");
+    if (cfg.universe <= 0) throw std::invalid_argument("generator: universe must be > 0");
+    std::mt19937_64 rng(cfg.seed);
+    std::vector<double> cumulative;
+    if (cfg.distribution == 1) {
+        cumulative.resize(static_cast<size_t>(cfg.universe));
+        double total = 0.0;
+        for (int64_t k = 0; k < cfg.universe; ++k) {
+            total += 1.0 / std::pow(static_cast<double>(k + 1), cfg.zipf_exponent);
+            cumulative[static_cast<size_t>(k)] = total;
+        }
+        for (auto& v : cumulative) v /= total;
+    }
+    const uint64_t span = static_cast<uint64_t>(cfg.universe);
+    const uint64_t limit = std::numeric_limits<uint64_t>::max() - std::numeric_limits<uint64_t>::max() % span;
+    auto draw_token = [&]() -> int64_t {
+        if (cfg.distribution != 1) {
+            uint64_t v;
+            do { v = rng(); } while (v >= limit);
+            return static_cast<int64_t>(v % span);
+        }
+        double u = uniform01(rng);
+        auto it = std::upper_bound(cumulative.begin(), cumulative.end(), u);
+        if (it == cumulative.end()) --it;
+        return static_cast<int64_t>(it - cumulative.begin());
+    };
+    std::vector<std::vector<int64_t>> sets;
+    sets.reserve(static_cast<size_t>(cfg.num_sets));
+    std::unordered_set<int64_t> drawn;
+    for (int64_t i = 0; i < cfg.num_sets; ++i) {
+        int64_t size = 0;
+        while (size == 0) size = poisson_draw(rng, cfg.mean_size);
+        size = std::min(size, cfg.universe);
+        drawn.clear();
+        int64_t attempts = 0;
+        const int64_t budget = 1000 * size + 1000;
+        while (static_cast<int64_t>(drawn.size()) < size && attempts < budget) {
+            drawn.insert(draw_token());
+            ++attempts;
+        }
+        for (int64_t t = 0; static_cast<int64_t>(drawn.size()) < size; ++t) drawn.insert(t);
+        sets.emplace_back(drawn.begin(), drawn.end());
+    }
+    return build_renumbered(sets, decimal_less);
+}
+
+// ================================================================= options
+ResolvedBitmap resolve_bitmap(const Collection& c, const Options& o) {
+    // reference src/join.cpp:52-89
+    ResolvedBitmap r;
+    r.enabled = o.bitmap_enabled;
+    if (!r.enabled) return r;
+    r.width = o.bits > 0 ? o.bits : (c.median_size() > 64 ? 128 : 64);
+    r.hash = o.hash;
+    Method m = o.method;
+    if (m == Method::Combined)
+        m = o.sim == Sim::Overlap ? Method::Set : resolve_combined(m, jaccard_space(o.sim, o.threshold));
+    switch (o.cutoff_mode) {
+        case CutoffMode::Off: r.cutoff = kUnlimited; break;
+        case CutoffMode::Explicit: r.cutoff = o.cutoff_value; break;
+        case CutoffMode::Auto:
+            r.cutoff = o.sim == Sim::Overlap ? cutoff_for_overlap(m, r.width, o.threshold.num)
+                                             : cutoff(m, r.width, jaccard_space(o.sim, o.threshold), true);
+            break;
+    }
+    r.method = m;
+    return r;
+}
+
+// ==================================================================== plan
+uint32_t window_start_of(const Collection& c, const JoinPlan& plan, size_t row) {
+    return plan.naive ? 0u : plan.window_start[c.rec_size(row)];
+}
+
+JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size_t row_end) {
+    JoinPlan plan;
+    plan.naive = o.algorithm == Algo::Naive;
+    const size_t n = c.size();
+    plan.row_begin = std::min(row_begin, n);
+    plan.row_end = std::min(row_end, n);
+    if (plan.row_end < plan.row_begin) plan.row_end = plan.row_begin;
+    plan.p = o.threshold.num;
+    plan.q = o.threshold.den;
+    plan.capacity = static_cast<uint32_t>(o.buffer_capacity);
+    if (!plan.naive) plan.bitmap = resolve_bitmap(c, o);
+    const uint32_t ms = c.max_size;
+    // minov over S in [0, 2*max_size] (reference src/similarity.cpp:99-100,113-115)
+    plan.minov.resize(2 * static_cast<size_t>(ms) + 1);
+    for (size_t S = 0; S < plan.minov.size(); ++S) {
+        int64_t v = ceil_div(static_cast<__int128>(plan.p) * static_cast<int64_t>(S),
+                             static_cast<__int128>(plan.p) + plan.q);
+        plan.minov[S] = static_cast<int32_t>(std::max<int64_t>(1, v));
+    }
+    // first index per size, then j0 per size (reference src/parallel_join.cpp:65-70)
+    std::vector<uint32_t> first_ge(static_cast<size_t>(ms) + 2, static_cast<uint32_t>(n));
+    for (size_t r = n; r-- > 0;) first_ge[c.rec_size(r)] = static_cast<uint32_t>(r);
+    for (size_t s = ms + 1; s-- > 0;) first_ge[s] = std::min(first_ge[s], first_ge[s + 1]);
+    plan.window_start.resize(static_cast<size_t>(ms) + 1);
+    for (size_t s = 0; s <= ms; ++s) {
+        int64_t lo = ceil_div(static_cast<__int128>(plan.p) * static_cast<int64_t>(s), plan.q);
+        plan.window_start[s] = lo > static_cast<int64_t>(ms) ? static_cast<uint32_t>(n)
+                                                             : first_ge[static_cast<size_t>(lo)];
+    }
+    uint64_t w = 0;
+    for (size_t i = plan.row_begin; i < plan.row_end; ++i) {
+        uint32_t j0 = window_start_of(c, plan, i);
+        if (j0 < i) w += i - j0;
+    }
+    plan.window_pairs = w;
+    return plan;
+}
+
+std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, int parts) {
+    if (parts < 1) throw std::invalid_argument("parts must be >= 1");
+    const size_t n = c.size();
+    std::vector<uint64_t> bounds(static_cast<size_t>(parts) + 1, n);
+    bounds[0] = 0;
+    uint64_t total = 0;
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t j0 = window_start_of(c, plan, i);
+        total += j0 < i ? i - j0 : 0;
+    }
+    // cut where the running window-pair sum crosses g*total/parts (+1 per row
+    // so empty-window rows still spread)
+    const double per = (static_cast<double>(total) + static_cast<double>(n)) / parts;
+    double run = 0;
+    int g = 1;
+    for (size_t i = 0; i < n && g < parts; ++i) {
+        uint32_t j0 = window_start_of(c, plan, i);
+        run += static_cast<double>(j0 < i ? i - j0 : 0) + 1.0;
+        while (g < parts && run >= per * g) bounds[static_cast<size_t>(g++)] = i + 1;
+    }
+    return bounds;
+}
+
+}  // namespace ssjb

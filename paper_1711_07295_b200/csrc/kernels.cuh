@@ -1,0 +1,727 @@
+// sm_100a kernels of the Bitmap-Filter self-join (paper Alg. 8; reference
+// hot loop src/parallel_join.cpp:61-136).  Included by engine.cu only.
+//
+//   K1 build_sketches   one b-bit sketch per record (Set / Xor / Next)
+//   K2 filter           row tile x column chunk; TMA-staged column sketches,
+//                       xor + POPC against an exact per-(|r|+|s|) threshold,
+//                       survivors compacted through warp ballots
+//   K2b rescan_saturated  position of the capacity-th survivor of rows whose
+//                       reference buffer would saturate (counter semantics)
+//   K3 verify           exact merge intersection with early exit
+//   K4 radix sort       canonical (id_r, id_s) order of the matches
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ssjb {
+namespace dev {
+
+constexpr int kRowTile = 128;     // rows per work item == threads per filter CTA
+constexpr int kColSub = 256;      // columns per TMA stage
+constexpr int kColChunk = 4096;   // columns per work item
+constexpr int kWarpQueue = 512;   // survivor staging entries per warp
+constexpr int kMaxInlineWords = 8;
+
+struct Control {
+    unsigned long long survivors;   // survivors emitted (may exceed capacity: overflow)
+    unsigned long long results;     // matches emitted
+    unsigned long long work_next;   // persistent-kernel work counter
+    unsigned long long tested, pruned, verified, saturated;  // counter sums
+    unsigned long long pad[8];
+};
+
+// ------------------------------------------------------------------ hashing
+// reference src/bitmap.hpp:30-36
+__device__ __forceinline__ uint32_t hash_token(uint32_t t, uint32_t width, int hash_mult, bool pow2) {
+    if (hash_mult) {
+        uint32_t h = static_cast<uint32_t>((static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull) >> 33);
+        return pow2 ? (h & (width - 1)) : (h % width);
+    }
+    return pow2 ? (t & (width - 1)) : (t % width);
+}
+
+// =============================================================== K1: sketches
+struct BuildParams {
+    const uint32_t* tokens;
+    const uint64_t* offsets;
+    uint64_t* bits;        // n * W words, row-major
+    uint32_t n;
+    uint32_t width;        // b
+    int words;             // W = b / 64
+    int method;            // 0 Set, 1 Xor, 2 Next
+    int hash_mult;
+    int pow2;
+};
+
+constexpr int kBuildRecs = 128;           // records (threads) per CTA
+constexpr int kBuildStage = 8192;         // staged tokens per CTA (32 KB)
+
+// One thread per record.  The CTA first stages the token range of its 128
+// records into shared memory with coalesced 128-bit loads, then each thread
+// folds its record into a register sketch.  Next (linear probing into the
+// next free bit, reference src/bitmap.cpp:40-62) is insertion-order
+// independent (reference tests/test_bitmap.cpp:108-122), so the probe order
+// is free; a record with |s| >= b is all ones.
+template <int W>
+__global__ void __launch_bounds__(kBuildRecs) build_sketches(BuildParams P) {
+    __shared__ __align__(16) uint32_t stage[kBuildStage + 8];
+    const uint32_t r0 = blockIdx.x * kBuildRecs;
+    const uint32_t r = r0 + threadIdx.x;
+    const uint32_t rl = min(r0 + kBuildRecs, P.n);
+    const uint64_t t_begin = P.offsets[r0];
+    const uint64_t t_end = P.offsets[rl];
+    const uint64_t a_begin = t_begin & ~uint64_t(3);  // 16-byte aligned start
+    const bool staged = (t_end - a_begin) <= kBuildStage;
+    if (staged) {
+        const uint64_t nvec = (t_end - a_begin + 3) / 4;
+        const uint4* src = reinterpret_cast<const uint4*>(P.tokens + a_begin);
+        uint4* dst = reinterpret_cast<uint4*>(stage);
+        for (uint64_t k = threadIdx.x; k < nvec; k += kBuildRecs) dst[k] = __ldg(src + k);
+    }
+    __syncthreads();
+    if (r >= P.n) return;
+    const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
+    const uint32_t cnt = static_cast<uint32_t>(e - b);
+    const uint32_t* tok = staged ? stage + (b - a_begin) : P.tokens + b;
+    const int words = W > 0 ? W : P.words;
+    uint64_t row[W > 0 ? W : kMaxInlineWords];
+    if constexpr (W > 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) row[w] = 0;
+        if (P.method == 2 && cnt >= P.width) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) row[w] = ~0ull;
+        } else {
+            for (uint32_t k = 0; k < cnt; ++k) {
+                uint32_t h = hash_token(tok[k], P.width, P.hash_mult, P.pow2);
+                uint32_t hw = h >> 6;
+                uint64_t bit = 1ull << (h & 63);
+                if (P.method == 0) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) row[w] |= (hw == uint32_t(w)) ? bit : 0ull;
+                } else if (P.method == 1) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) row[w] ^= (hw == uint32_t(w)) ? bit : 0ull;
+                } else {
+                    // first free bit at or after h, then wrap to the front
+                    bool placed = false;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        uint64_t fb = uint32_t(w) < hw ? 0ull : ~row[w];
+                        if (uint32_t(w) == hw) fb &= ~0ull << (h & 63);
+                        if (!placed && fb) {
+                            row[w] |= fb & (~fb + 1);
+                            placed = true;
+                        }
+                    }
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        uint64_t fb = ~row[w];
+                        if (uint32_t(w) <= hw && !placed && fb) {
+                            row[w] |= fb & (~fb + 1);
+                            placed = true;
+                        }
+                    }
+                }
+            }
+        }
+        uint64_t* out = P.bits + static_cast<uint64_t>(r) * W;
+#pragma unroll
+        for (int w = 0; w < W; ++w) out[w] = row[w];
+    } else {
+        // Wide sketches (b > 512): build directly in global memory, one thread
+        // per record; rare and off the hot path.
+        uint64_t* out = P.bits + static_cast<uint64_t>(r) * words;
+        for (int w = 0; w < words; ++w) out[w] = 0;
+        if (P.method == 2 && cnt >= P.width) {
+            for (int w = 0; w < words; ++w) out[w] = ~0ull;
+        } else {
+            for (uint32_t k = 0; k < cnt; ++k) {
+                uint32_t h = hash_token(tok[k], P.width, P.hash_mult, P.pow2);
+                if (P.method == 0) {
+                    out[h >> 6] |= 1ull << (h & 63);
+                } else if (P.method == 1) {
+                    out[h >> 6] ^= 1ull << (h & 63);
+                } else {
+                    int word = static_cast<int>(h >> 6);
+                    uint64_t fb = ~out[word] & (~0ull << (h & 63));
+                    for (int step = 0; step <= words; ++step) {
+                        if (fb) {
+                            out[word] |= fb & (~fb + 1);
+                            break;
+                        }
+                        word = (word + 1) % words;
+                        fb = ~out[word];
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ================================================================ K2: filter
+struct FilterParams {
+    const uint64_t* bits;        // sketches, n * W words (padded by kColSub rows)
+    const uint32_t* sizes;       // |r| per record (padded)
+    const int32_t* maxham;       // maxham[S] = S - 2*minov[S], S in [0, 2*max_size]
+    const uint32_t* wstart;      // j0 per record size
+    const uint64_t* item_base;   // work items per tile, prefix (ntiles + 1)
+    const uint32_t* tile_col_lo; // first (32-aligned) column of each tile's span
+    uint2* surv;                 // survivors (j, i)
+    uint32_t* rowcnt;            // survivors per row (row - row_begin)
+    Control* ctl;
+    unsigned long long surv_cap;
+    unsigned long long item_begin, item_end;
+    uint32_t tile_begin;         // tile index of item_begin's tile (search lower bound)
+    uint32_t ntiles;
+    uint32_t row_begin, row_end;
+    int64_t cutoff;              // bypass the filter for rows with |r| > cutoff
+    int words;
+    int colsub;                  // columns per TMA stage for the generic-width kernel
+    int bypass_all;              // bitmap disabled or NAIVE: every window pair survives
+    int naive;                   // NAIVE: window [0, i)
+};
+
+__device__ __forceinline__ uint32_t low_mask(int x) {
+    return x >= 32 ? 0xFFFFFFFFu : (x <= 0 ? 0u : ((1u << x) - 1u));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// Survivor emission for one 32-column group: lane l owns row i and the
+// survivor bitmap m (bit k = column base+k).  Staged per warp in shared
+// memory; flushed to the global survivor array with one atomic per flush.
+__device__ __forceinline__ void warp_flush(uint2* q, int& qlen, const FilterParams& P, int lane) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(qlen));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int k = lane; k < qlen; k += 32)
+        if (base + k < P.surv_cap) P.surv[base + k] = q[k];
+    qlen = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void emit_group(uint32_t m, uint32_t base_col, uint32_t row, uint2* q, int& qlen,
+                                           const FilterParams& P, int lane) {
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const int excl = incl - c;
+    if (total > kWarpQueue) {
+        // bulk (bypassed rows): reserve directly in the global array
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(total));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + excl;
+        while (m) {
+            int k = __ffs(m) - 1;
+            m &= m - 1;
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + k, row);
+            ++base;
+        }
+        return;
+    }
+    if (qlen + total > kWarpQueue) warp_flush(q, qlen, P, lane);
+    int pos = qlen + excl;
+    while (m) {
+        int k = __ffs(m) - 1;
+        m &= m - 1;
+        q[pos++] = make_uint2(base_col + k, row);
+    }
+    qlen += total;
+    __syncwarp();
+}
+
+// Persistent filter kernel.  Work item = (tile of 128 consecutive rows, chunk
+// of <= kColChunk columns of the tile's window span).  Thread t owns row
+// i = tile*128 + t with its sketch in registers; the chunk's column sketches
+// and sizes stream through a 2-stage TMA (cp.async.bulk) ring in shared
+// memory and every lane reads the same column (smem broadcast).  Per pair:
+// W x (2 LOP3 + 2 POPC) + IADD3 + SHF.  skip <=> popcount(b_i ^ b_j) >
+// maxham[|r_i|+|r_j|], the exact integer form of reference
+// src/bitmap.cpp:125-143 with src/similarity.cpp:113-115.
+template <int W>
+__global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
+    constexpr int WS = W > 0 ? W : 1;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* s_bits = reinterpret_cast<uint64_t*>(smem_raw);                  // [2][colsub*W]
+    const int words = W > 0 ? W : P.words;
+    const int colsub = W > 0 ? kColSub : P.colsub;  // columns per stage
+    uint32_t* s_size = reinterpret_cast<uint32_t*>(s_bits + 2 * colsub * words);  // [2][colsub]
+    uint2* s_queue = reinterpret_cast<uint2*>(s_size + 2 * colsub);            // [4][kWarpQueue]
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ unsigned long long s_item;
+    __shared__ uint32_t s_tile;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint2* q = s_queue + warp * kWarpQueue;
+    int qlen = 0;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase[2] = {0, 0};
+
+    for (;;) {
+        if (tid == 0) {
+            unsigned long long it = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+            uint32_t t = 0;
+            if (it < P.item_end) {
+                uint32_t lo = P.tile_begin, hi = P.ntiles;  // largest t with item_base[t] <= it
+                while (hi - lo > 1) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    if (P.item_base[mid] <= it) lo = mid; else hi = mid;
+                }
+                t = lo;
+            }
+            s_item = it;
+            s_tile = t;
+        }
+        __syncthreads();
+        const unsigned long long item = s_item;
+        const uint32_t tile = s_tile;
+        if (item >= P.item_end) break;
+        const uint32_t chunk = static_cast<uint32_t>(item - P.item_base[tile]);
+
+        const uint32_t tile_row0 = P.row_begin + tile * kRowTile;
+        const uint32_t tile_rows_end = min(tile_row0 + kRowTile, P.row_end);
+        const uint32_t i = tile_row0 + tid;
+        const bool valid = i < tile_rows_end;
+        const uint32_t c0 = P.tile_col_lo[tile] + chunk * kColChunk;
+        const uint32_t c1 = min(c0 + kColChunk, tile_rows_end - 1);  // columns < last row
+
+        uint64_t mine[WS];
+        uint32_t si = 0, j0 = 0;
+        bool bypass = P.bypass_all != 0;
+        if (valid) {
+            si = P.sizes[i];
+            j0 = P.naive ? 0u : P.wstart[si];
+            if (static_cast<int64_t>(si) > P.cutoff) bypass = true;
+            if constexpr (W > 0) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) mine[w] = P.bits[static_cast<uint64_t>(i) * W + w];
+            }
+        } else {
+            if constexpr (W > 0) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) mine[w] = 0;
+            }
+        }
+        const uint32_t lo_i = valid ? max(j0, c0) : c1;
+        const uint32_t hi_i = valid ? min(i, c1) : c1;
+        uint32_t cnt = 0;
+
+        // stage 0 prefetch
+        const uint32_t nsub = (c1 - c0 + colsub - 1) / colsub;
+        auto issue = [&](uint32_t s, int buf) {
+            const uint32_t cs = c0 + s * colsub;
+            const uint32_t ncol = min(static_cast<uint32_t>(colsub), c1 - cs);
+            const uint32_t ncol4 = (ncol + 3) & ~3u;  // padded allocation keeps this in bounds
+            const uint32_t bb = ncol4 * 8u * static_cast<uint32_t>(words);
+            const uint32_t sb = ncol4 * 4u;
+            mbar_expect_tx(&bars[buf], bb + sb);
+            tma_load_1d(s_bits + buf * colsub * words, P.bits + static_cast<uint64_t>(cs) * words, bb, &bars[buf]);
+            tma_load_1d(s_size + buf * colsub, P.sizes + cs, sb, &bars[buf]);
+        };
+        if (tid == 0 && nsub > 0) issue(0, 0);
+
+        for (uint32_t s = 0; s < nsub; ++s) {
+            const int buf = s & 1;
+            if (tid == 0 && s + 1 < nsub) issue(s + 1, buf ^ 1);
+            mbar_wait(&bars[buf], phase[buf]);
+            phase[buf] ^= 1;
+            const uint32_t cs = c0 + s * colsub;
+            const uint32_t ncol = min(static_cast<uint32_t>(colsub), c1 - cs);
+            const uint64_t* cb = s_bits + buf * colsub * words;
+            const uint32_t* cz = s_size + buf * colsub;
+            const uint32_t sz_first = cz[0], sz_last = cz[ncol - 1];
+            const bool uniform = sz_first == sz_last;
+            // d = h - T - 1 < 0  <=> survive;  T = maxham[si + sj]
+            int negT1 = 0;
+            if (uniform) negT1 = -P.maxham[si + sz_first] - 1;
+            for (uint32_t g = 0; g < ncol; g += 32) {
+                const uint32_t gbase = cs + g;
+                const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
+                const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
+                const uint32_t rm = low_mask(kh) & ~low_mask(kl);
+                uint32_t m = 0;
+                if (__any_sync(0xFFFFFFFFu, rm != 0)) {
+                    const int kmax = min(32, static_cast<int>(ncol - g));
+                    if (uniform && kmax == 32) {
+#pragma unroll 8
+                        for (int k = 0; k < 32; ++k) {
+                            const uint64_t* col = cb + (g + k) * words;
+                            int h = 0;
+                            if constexpr (W > 0) {
+#pragma unroll
+                                for (int w = 0; w < W; ++w) h += __popcll(mine[w] ^ col[w]);
+                            } else {
+                                const uint64_t* me = P.bits + static_cast<uint64_t>(i) * words;
+                                for (int w = 0; w < words; ++w) h += __popcll(me[w] ^ col[w]);
+                            }
+                            m = __funnelshift_l(static_cast<uint32_t>(h + negT1), m, 1);
+                        }
+                        m = __brev(m);
+                    } else {
+                        for (int k = 0; k < kmax; ++k) {
+                            const uint64_t* col = cb + (g + k) * words;
+                            int h = 0;
+                            if constexpr (W > 0) {
+#pragma unroll
+                                for (int w = 0; w < W; ++w) h += __popcll(mine[w] ^ col[w]);
+                            } else {
+                                const uint64_t* me = P.bits + static_cast<uint64_t>(i) * words;
+                                for (int w = 0; w < words; ++w) h += __popcll(me[w] ^ col[w]);
+                            }
+                            const int T = __ldg(P.maxham + si + cz[g + k]);
+                            m |= (h <= T ? 1u : 0u) << k;
+                        }
+                    }
+                    m = bypass ? rm : (m & rm);
+                    cnt += __popc(m);
+                    if (__any_sync(0xFFFFFFFFu, m != 0)) emit_group(m, gbase, i, q, qlen, P, lane);
+                }
+            }
+            __syncthreads();  // stage buffer free for the TMA issued next iteration
+        }
+        if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
+        __syncthreads();  // s_item / s_tile / stage buffers are rewritten next item
+    }
+    if (qlen) warp_flush(q, qlen, P, lane);
+}
+
+// ======================================================= K2b: saturated rows
+struct RescanParams {
+    const uint64_t* bits;
+    const uint32_t* sizes;
+    const int32_t* maxham;
+    const uint32_t* wstart;
+    const uint32_t* rowcnt;
+    uint32_t* jstar;         // capacity-th survivor column per row (row - row_begin)
+    uint32_t row_begin, row_end;
+    uint32_t capacity;
+    int64_t cutoff;
+    int words;
+    int bypass_all;
+};
+
+// One warp per row whose survivor count reaches the capacity: walk the window
+// in order and locate the capacity-th survivor (the reference's saturation
+// point, src/parallel_join.cpp:83-94).
+__global__ void rescan_saturated(RescanParams P) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < P.row_end - P.row_begin; r += warps) {
+        const uint32_t c = P.rowcnt[r];
+        if (c < P.capacity) continue;
+        const uint32_t i = P.row_begin + r;
+        const uint32_t si = P.sizes[i];
+        const uint32_t j0 = P.wstart[si];
+        if (P.bypass_all || static_cast<int64_t>(si) > P.cutoff) {
+            if (lane == 0) P.jstar[r] = j0 + P.capacity - 1;
+            continue;
+        }
+        const uint64_t* me = P.bits + static_cast<uint64_t>(i) * P.words;
+        uint32_t seen = 0;
+        for (uint32_t jb = j0; jb < i; jb += 32) {
+            const uint32_t j = jb + lane;
+            bool surv = false;
+            if (j < i) {
+                const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
+                int h = 0;
+                for (int w = 0; w < P.words; ++w) h += __popcll(me[w] ^ o[w]);
+                surv = h <= P.maxham[si + P.sizes[j]];
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
+            const uint32_t pc = __popc(bal);
+            if (seen + pc >= P.capacity) {
+                uint32_t b2 = bal;  // drop the first (need-1) survivors of this group
+                for (uint32_t k = P.capacity - seen; k > 1; --k) b2 &= b2 - 1;
+                if (lane == 0) P.jstar[r] = jb + static_cast<uint32_t>(__ffs(b2) - 1);
+                break;
+            }
+            seen += pc;
+        }
+    }
+}
+
+// Counter reduction: per row, the reference's buffered/bypassed bookkeeping
+// reconstructed from (window, survivors, capacity-th survivor position).
+struct CountParams {
+    const uint32_t* sizes;
+    const uint32_t* wstart;
+    const uint32_t* rowcnt;
+    const uint32_t* jstar;
+    Control* ctl;
+    uint32_t row_begin, row_end;
+    uint32_t capacity;
+    int bitmap_enabled;
+    int naive;
+};
+
+__global__ void reduce_counters(CountParams P) {
+    unsigned long long tested = 0, pruned = 0, verified = 0, sat = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.row_end - P.row_begin;
+         r += gridDim.x * blockDim.x) {
+        const uint32_t i = P.row_begin + r;
+        const uint32_t j0 = P.naive ? 0u : P.wstart[P.sizes[i]];
+        const uint32_t w = j0 < i ? i - j0 : 0u;
+        if (P.naive) {
+            verified += w;
+            continue;
+        }
+        const uint32_t s = P.rowcnt[r];
+        if (s < P.capacity) {
+            if (P.bitmap_enabled) {
+                tested += w;
+                pruned += w - s;
+            }
+            verified += s;
+        } else {
+            const uint32_t js = P.jstar[r];
+            const uint32_t t = js - j0 + 1;
+            if (P.bitmap_enabled) {
+                tested += t;
+                pruned += t - P.capacity;
+            }
+            verified += P.capacity + (i - js - 1);
+            sat += 1;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tested += __shfl_down_sync(0xFFFFFFFFu, tested, o);
+        pruned += __shfl_down_sync(0xFFFFFFFFu, pruned, o);
+        verified += __shfl_down_sync(0xFFFFFFFFu, verified, o);
+        sat += __shfl_down_sync(0xFFFFFFFFu, sat, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (tested) atomicAdd(&P.ctl->tested, tested);
+        if (pruned) atomicAdd(&P.ctl->pruned, pruned);
+        if (verified) atomicAdd(&P.ctl->verified, verified);
+        if (sat) atomicAdd(&P.ctl->saturated, sat);
+    }
+}
+
+// ================================================================ K3: verify
+struct VerifyParams {
+    const uint32_t* tokens;
+    const uint64_t* offsets;
+    const int32_t* minov;     // minov[|r|+|s|]
+    const uint2* surv;
+    unsigned long long count;
+    unsigned long long* res_keys;  // (j << 32) | i
+    uint32_t* res_ov;
+    unsigned long long res_cap;
+    Control* ctl;
+};
+
+// One thread per surviving pair: branch-free sorted merge with the
+// reference's early exit (src/similarity.cpp:168-185).  A match's overlap is
+// exact because the exit only fires on pairs that cannot reach minov.
+__global__ void verify_pairs(VerifyParams P) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < P.count;
+         base += stride) {
+        const unsigned long long k = base + threadIdx.x;
+        bool matched = false;
+        uint32_t j = 0, i = 0, ov = 0;
+        if (k < P.count) {
+            const uint2 pr = P.surv[k];
+            j = pr.x;
+            i = pr.y;
+            const uint64_t ab = P.offsets[j], ae = P.offsets[j + 1];
+            const uint64_t bb = P.offsets[i], be = P.offsets[i + 1];
+            const uint32_t na = static_cast<uint32_t>(ae - ab), nb = static_cast<uint32_t>(be - bb);
+            const int32_t need = P.minov[na + nb];
+            const uint32_t* A = P.tokens + ab;
+            const uint32_t* B = P.tokens + bb;
+            uint32_t ia = 0, ib = 0;
+            int32_t o = 0;
+            while (ia < na && ib < nb) {
+                const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
+                if (o + rest < need) break;
+                const uint32_t x = __ldg(A + ia), y = __ldg(B + ib);
+                o += x == y;
+                ia += x <= y;
+                ib += y <= x;
+            }
+            matched = o >= need;
+            ov = static_cast<uint32_t>(o);
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, matched);
+        if (bal) {
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(&P.ctl->results, static_cast<unsigned long long>(__popc(bal)));
+            slot = __shfl_sync(0xFFFFFFFFu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
+            if (matched && slot < P.res_cap) {
+                P.res_keys[slot] = (static_cast<unsigned long long>(j) << 32) | i;
+                P.res_ov[slot] = ov;
+            }
+        }
+    }
+}
+
+// ============================================================ K4: radix sort
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;                       // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys per tile
+
+// Digit histogram of each tile: hist[digit * ntiles + tile].
+__global__ void __launch_bounds__(kSortThreads) radix_hist(const unsigned long long* keys, unsigned long long n,
+                                                          int shift, uint32_t* hist, uint32_t ntiles) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long t0 = static_cast<unsigned long long>(blockIdx.x) * kSortTile;
+    for (int k = 0; k < kSortItems; ++k) {
+        unsigned long long idx = t0 + k * kSortThreads + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    hist[threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of a u32 array in place, three phases (block sums, a
+// single-block scan of the sums, add-back).  Lengths here are 256 * ntiles.
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* tmp, uint32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) tmp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < static_cast<int>(blockDim.x >> 5) ? tmp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+            if (lane >= o) s += y;
+        }
+        tmp[lane] = s;
+    }
+    __syncthreads();
+    total = tmp[(blockDim.x >> 5) - 1];
+    uint32_t prefix = warp ? tmp[warp - 1] : 0;
+    __syncthreads();
+    return prefix + x - v;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_blocks(uint32_t* data, uint32_t n, uint32_t* block_sums) {
+    __shared__ uint32_t tmp[32];
+    const uint32_t idx = blockIdx.x * kScanBlock + threadIdx.x;
+    const uint32_t v = idx < n ? data[idx] : 0;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(v, tmp, total);
+    if (idx < n) data[idx] = ex;
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_single(uint32_t* data, uint32_t n) {
+    __shared__ uint32_t tmp[32];
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < n; base += kScanBlock) {
+        const uint32_t idx = base + threadIdx.x;
+        const uint32_t v = idx < n ? data[idx] : 0;
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(v, tmp, total);
+        if (idx < n) data[idx] = ex + carry;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(kScanBlock) scan_add(uint32_t* data, uint32_t n, const uint32_t* block_sums) {
+    const uint32_t idx = blockIdx.x * kScanBlock + threadIdx.x;
+    if (idx < n) data[idx] += block_sums[blockIdx.x];
+}
+
+// Stable scatter of one tile: keys are ranked in tile order (round by round,
+// warp-major inside a round) with __match_any_sync, so equal digits keep
+// their relative order -- the LSD invariant.
+__global__ void __launch_bounds__(kSortThreads) radix_scatter(const unsigned long long* keys_in, const uint32_t* vals_in,
+                                                             unsigned long long* keys_out, uint32_t* vals_out,
+                                                             unsigned long long n, int shift, const uint32_t* hist,
+                                                             uint32_t ntiles) {
+    constexpr int kWarps = kSortThreads / 32;
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t wcount[kWarps][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    base[threadIdx.x] = hist[threadIdx.x * ntiles + blockIdx.x];
+    const unsigned long long t0 = static_cast<unsigned long long>(blockIdx.x) * kSortTile;
+    for (int round = 0; round < kSortItems; ++round) {
+        for (int w = 0; w < kWarps; ++w) wcount[w][threadIdx.x] = 0;
+        __syncthreads();
+        const unsigned long long idx = t0 + static_cast<unsigned long long>(round) * kSortThreads + threadIdx.x;
+        const bool ok = idx < n;
+        unsigned long long key = ok ? keys_in[idx] : 0ull;
+        const uint32_t d = ok ? static_cast<uint32_t>((key >> shift) & 255) : 256u + lane;  // unique dummy
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (ok && rank == 0) wcount[warp][d] = __popc(peers);
+        __syncthreads();
+        // per digit: prefix over warps, then advance the running base
+        {
+            const uint32_t dd = threadIdx.x;
+            uint32_t run = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                uint32_t c = wcount[w][dd];
+                wcount[w][dd] = run;
+                run += c;
+            }
+            __syncthreads();
+            if (ok) {
+                const uint32_t pos = base[d] + wcount[warp][d] + rank;
+                keys_out[pos] = key;
+                vals_out[pos] = vals_in[idx];
+            }
+            __syncthreads();
+            base[dd] += run;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace dev
+}  // namespace ssjb
