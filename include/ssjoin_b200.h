@@ -53,6 +53,7 @@ typedef struct ssjb_stats {
     uint64_t launches;       /* kernel launches issued */
     uint64_t h2d_bytes;      /* host->device bytes copied */
     uint64_t d2h_bytes;      /* device->host bytes copied */
+    uint64_t verify_bytes;   /* algorithmic bytes of verification: 4*(|r|+|s|) per survivor + 16 per match */
     double ms_upload;        /* device event times per phase (max over GPUs) */
     double ms_build;
     double ms_filter;

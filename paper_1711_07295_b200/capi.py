@@ -102,7 +102,7 @@ SSJ_SYMBOLS = tuple(_PROTOS)
 class Stats(C.Structure):
     """``ssjb_stats`` (include/ssjoin_b200.h)."""
     _fields_ = [(n, C.c_uint64) for n in ("window_pairs", "survivors", "batches", "launches",
-                                          "h2d_bytes", "d2h_bytes")] + \
+                                          "h2d_bytes", "d2h_bytes", "verify_bytes")] + \
                [(n, C.c_double) for n in ("ms_upload", "ms_build", "ms_filter", "ms_rescan",
                                           "ms_verify", "ms_sort", "ms_download")] + \
                [("devices", C.c_int), ("filter_kernel", C.c_int)]

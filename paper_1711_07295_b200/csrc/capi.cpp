@@ -170,6 +170,7 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
         s.launches += p.stats.launches;
         s.h2d_bytes += p.stats.h2d_bytes;
         s.d2h_bytes += p.stats.d2h_bytes;
+        s.verify_bytes += p.stats.verify_bytes;
         s.ms_upload = std::max(s.ms_upload, p.stats.ms_upload);
         s.ms_build = std::max(s.ms_build, p.stats.ms_build);
         s.ms_filter = std::max(s.ms_filter, p.stats.ms_filter);

@@ -676,6 +676,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     out.pruned_bitmap = h_ctl.pruned;
     out.verified = h_ctl.verified;
     out.saturated = h_ctl.saturated;
+    st.verify_bytes = h_ctl.verify_bytes;
     out.matched = out.pairs.size();
     st.ms_upload = Timer::ms(e0, e_up);
     st.ms_build = Timer::ms(e_up, e_build);

@@ -23,7 +23,7 @@ static_assert(sizeof(PairOut) == 16, "ssj_pair layout");
 
 struct EngineStats {
     uint64_t window_pairs = 0, survivors = 0, batches = 0, launches = 0;
-    uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0, verify_bytes = 0;
     double ms_upload = 0, ms_build = 0, ms_filter = 0, ms_rescan = 0, ms_verify = 0, ms_sort = 0,
            ms_download = 0;
     int filter_kernel = 0;

@@ -351,7 +351,7 @@ template <typename Key, typename KeyLess>
 std::unique_ptr<Collection> build_renumbered(std::vector<std::vector<Key>>& sets, KeyLess key_less) {
     std::unordered_map<Key, uint64_t> freq;
     for (auto& rec : sets) {
-        std::sort(rec.begin(), rec.end(), key_less);
+        std::sort(rec.begin(), rec.end());  // any total order dedups; ids come from key_less below
         rec.erase(std::unique(rec.begin(), rec.end()), rec.end());
         for (const auto& t : rec) ++freq[t];
     }
@@ -377,12 +377,25 @@ std::unique_ptr<Collection> build_renumbered(std::vector<std::vector<Key>>& sets
 
 // Decimal-string order of non-negative integers: the order std::map<std::string>
 // gives the reference generator's std::to_string tokens ("10" < "2").
+// Digits are compared most-significant first without formatting.
+int decimal_digits(uint64_t v, unsigned char* d) {
+    int n = 0;
+    do {
+        d[n++] = static_cast<unsigned char>(v % 10);
+        v /= 10;
+    } while (v);
+    return n;  // least significant first
+}
+
 bool decimal_less(int64_t a, int64_t b) {
-    char sa[24], sb[24];
-    int la = std::snprintf(sa, sizeof sa, "%lld", static_cast<long long>(a));
-    int lb = std::snprintf(sb, sizeof sb, "%lld", static_cast<long long>(b));
-    int c = std::memcmp(sa, sb, static_cast<size_t>(std::min(la, lb)));
-    return c != 0 ? c < 0 : la < lb;
+    unsigned char da[24], db[24];
+    const int la = decimal_digits(static_cast<uint64_t>(a), da);
+    const int lb = decimal_digits(static_cast<uint64_t>(b), db);
+    for (int k = 0; k < la && k < lb; ++k) {
+        const unsigned char x = da[la - 1 - k], y = db[lb - 1 - k];
+        if (x != y) return x < y;
+    }
+    return la < lb;
 }
 
 double uniform01(std::mt19937_64& rng) {

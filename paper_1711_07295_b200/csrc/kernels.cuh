@@ -28,7 +28,8 @@ struct Control {
     unsigned long long results;     // matches emitted
     unsigned long long work_next;   // persistent-kernel work counter
     unsigned long long tested, pruned, verified, saturated;  // counter sums
-    unsigned long long pad[8];
+    unsigned long long verify_bytes;  // algorithmic bytes of K3
+    unsigned long long pad[7];
 };
 
 // ------------------------------------------------------------------ hashing
@@ -586,6 +587,12 @@ __global__ void verify_pairs(VerifyParams P) {
             matched = o >= need;
             ov = static_cast<uint32_t>(o);
         }
+        // algorithmic traffic: both token lists plus the 16-byte result record
+        unsigned long long vb = 0;
+        if (k < P.count) vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
+        if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, matched);
         if (bal) {
             unsigned long long slot = 0;

@@ -1,0 +1,179 @@
+"""GPU parity: the B200 library through its C ABI versus the reference's own
+outputs (tests/golden) and the C oracle.  Bit-exact: same sorted
+(id_r, id_s, overlap) list, same counters, same saturated_records."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, golden_collection
+from paper_1711_07295_b200 import capi, datasets as D
+from paper_1711_07295_b200 import ssjoin as S
+
+pytestmark = pytest.mark.gpu
+
+COUNTER_KEYS = ("candidates", "pruned_length", "pruned_positional", "pruned_suffix", "pruned_bitmap",
+                "bitmap_tested", "filter_evaluations", "verified", "matched")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def colls(lib, golden_arrays):
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = S.Collection.from_csr(lib, *golden_collection(golden_arrays, name))
+        return cache[name]
+    return get
+
+
+def options_of(lib, e):
+    o = S.default_options(lib)
+    for k, v in e["options"].items():
+        setattr(o, k, v)
+    return o
+
+
+def assert_same(rep, e, where=""):
+    assert len(rep.pairs) == e["pair_count"], (where, e["label"])
+    assert sha(rep.pairs) == e["pairs_sha256"], (where, e["label"])
+    for k in COUNTER_KEYS:
+        assert rep.counters[k] == e["counters"][k], (where, e["label"], k)
+    assert rep.saturated_records == e["saturated_records"], (where, e["label"])
+
+
+def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
+    for e in golden["bitmaps"]:
+        store = S.build_bitmaps(colls(e["collection"]), e["method"], e["width"], e["hash"])
+        assert sha(store) == e["sha256"], e
+
+
+def test_every_golden_join(lib, golden, colls):
+    for e in golden["joins"]:
+        rep = S.join(colls(e["collection"]), options_of(lib, e))
+        assert_same(rep, e)
+
+
+def test_row_shards_add_up(lib, golden, colls):
+    for e in golden["joins"]:
+        if e["options"]["algorithm"] != capi.SSJ_ALGO_PAR_BITMAP or e["collection"].startswith("acc1_"):
+            continue
+        coll = colls(e["collection"])
+        opts = options_of(lib, e)
+        for parts in (2, 3):
+            b = S.partition_rows(coll, opts, parts)
+            reps = [S.join_rows(coll, opts, int(b[k]), int(b[k + 1])) for k in range(parts)]
+            pairs = np.sort(np.concatenate([r.pairs for r in reps]), order=["id_r", "id_s"])
+            assert sha(pairs) == e["pairs_sha256"], e["label"]
+            for k in COUNTER_KEYS:
+                assert sum(r.counters[k] for r in reps) == e["counters"][k], (e["label"], k)
+            assert sum(r.saturated_records for r in reps) == e["saturated_records"]
+
+
+def test_random_collections_vs_oracle(lib, oracle):
+    rng = np.random.default_rng(2024)
+    for trial in range(40):
+        n = int(rng.integers(50, 1500))
+        universe = int(rng.integers(20, 3000))
+        mean = float(rng.uniform(2, 40))
+        dist = int(rng.integers(0, 2))
+        coll = S.Collection.generate(lib, n, mean, universe, int(rng.integers(1 << 30)), dist)
+        t, o = coll.csr()
+        p, q = [(1, 2), (3, 5), (2, 3), (7, 10), (4, 5), (9, 10), (1, 1), (1, 3)][trial % 8]
+        width = int(rng.choice([64, 128, 192, 256, 320, 512, 1024]))
+        method = int(rng.integers(0, 3))
+        hsh = int(rng.integers(0, 2))
+        cap = int(rng.choice([1, 2, 7, 64, 2048]))
+        enabled = bool(rng.integers(0, 5))
+        cutoff = int(rng.choice([oracle.INT64_MAX, 0, 5, 12, 30]))
+        mode = capi.SSJ_CUTOFF_OFF if cutoff == oracle.INT64_MAX else capi.SSJ_CUTOFF_EXPLICIT
+        opts = S.default_options(lib, algorithm=capi.SSJ_ALGO_PAR_BITMAP, threshold=(p, q),
+                                 bitmap_enabled=int(enabled), bitmap_method=method, bitmap_bits=width,
+                                 bitmap_hash=hsh, cutoff_mode=mode, cutoff_value=cutoff,
+                                 buffer_capacity=cap)
+        rep = S.join(coll, opts)
+        want, cnt = oracle.par_bitmap_join(t, o, p, q, enabled, method, width, hsh, cutoff, cap)
+        assert (rep.pairs == want).all() and len(rep.pairs) == len(want), trial
+        assert rep.counters["candidates"] == cnt["candidates"], trial
+        assert rep.counters["pruned_bitmap"] == cnt["pruned_bitmap"], trial
+        assert rep.counters["bitmap_tested"] == cnt["bitmap_tested"], trial
+        assert rep.counters["verified"] == cnt["verified"], trial
+        assert rep.counters["matched"] == cnt["matched"], trial
+        assert rep.saturated_records == cnt["saturated_records"], trial
+
+
+def test_naive_vs_oracle(lib, oracle):
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        coll = S.Collection.generate(lib, int(rng.integers(100, 900)), 6, 40, trial + 1)
+        t, o = coll.csr()
+        tau = [(1, 2), (7, 10), (1, 1)][trial % 3]
+        rep = S.join(coll, S.default_options(lib, algorithm=capi.SSJ_ALGO_NAIVE, threshold=tau))
+        want, cnt = oracle.naive_join(t, o, *tau)
+        assert (rep.pairs == want).all() and len(rep.pairs) == len(want)
+        assert rep.counters["candidates"] == cnt["candidates"] == rep.counters["verified"]
+
+
+def test_survivor_and_result_overflow_batches(lib, golden, colls, monkeypatch):
+    """Tiny survivor/result buffers force many filter batches and result runs."""
+    monkeypatch.setenv("SSJB_SURVIVOR_CAP", str(1 << 19))
+    monkeypatch.setenv("SSJB_RESULT_CAP", str(1 << 19))
+    for e in golden["joins"]:
+        if e["collection"] in ("dups_2500", "acc8_2000", "par_500") and e["pair_count"] > 0:
+            rep = S.join(colls(e["collection"]), options_of(lib, e))
+            assert_same(rep, e, "overflow")
+    e = next(x for x in golden["joins"] if x["collection"] == "dups_2500")
+    rep = S.join(colls("dups_2500"), options_of(lib, e))
+    assert rep.extra["batches"] > 1
+
+
+def test_pinned_replica_and_repeat_determinism(lib, golden, colls):
+    e = next(x for x in golden["joins"] if x["label"] == "acceptance criterion 8")
+    coll = colls(e["collection"])
+    S.pin_device(coll, 0)
+    try:
+        for _ in range(3):
+            assert_same(S.join(coll, options_of(lib, e)), e, "pinned")
+    finally:
+        S.unpin_device(coll, 0)
+    assert_same(S.join(coll, options_of(lib, e)), e, "unpinned")
+
+
+def _large():
+    path = os.path.join(GOLDEN_DIR, "large.jsonl")
+    if not os.path.exists(path):
+        return []
+    return [json.loads(line) for line in open(path)]
+
+
+@pytest.mark.parametrize("case", [c["case"] for c in _large()] or ["none"])
+def test_full_size_configs_match_reference(lib, case):
+    """BASELINE configs at full size vs the reference library's own run."""
+    entries = {c["case"]: c for c in _large()}
+    if case not in entries:
+        pytest.skip("no full-size fixtures")
+    e = entries[case]
+    coll = D.c1(lib) if case == "C1" else _c2(lib)
+    opts = S.par_bitmap_options(lib, threshold=tuple(e["tau"]), method=capi.SSJ_BITMAP_XOR,
+                                bits=e["bits"], cutoff_mode=capi.SSJ_CUTOFF_OFF)
+    rep = S.join(coll, opts)
+    assert len(rep.pairs) == e["pair_count"]
+    assert sha(rep.pairs) == e["pairs_sha256"]
+    for k in COUNTER_KEYS:
+        assert rep.counters[k] == e["counters"][k], k
+    assert rep.saturated_records == e["saturated_records"]
+
+
+_C2 = {}
+
+
+def _c2(lib):
+    if "c" not in _C2:
+        _C2["c"] = D.c2(lib)
+    return _C2["c"]
