@@ -175,18 +175,31 @@ std::shared_ptr<DeviceReplica> replica_for(const Collection& c, int device, cuda
 using FilterFn = void (*)(dev::FilterParams);
 using BuildFn = void (*)(dev::BuildParams);
 
-FilterFn filter_fn(int words) {
-    switch (words) {
-        case 1: return dev::filter_kernel<1>;
-        case 2: return dev::filter_kernel<2>;
-        case 3: return dev::filter_kernel<3>;
-        case 4: return dev::filter_kernel<4>;
-        case 5: return dev::filter_kernel<5>;
-        case 6: return dev::filter_kernel<6>;
-        case 7: return dev::filter_kernel<7>;
-        case 8: return dev::filter_kernel<8>;
-        default: return dev::filter_kernel<0>;
+// Level-2 sketch words for a level-1 width (see filter_kernel): b <= 128 -> 256,
+// b <= 256 -> 512, wider sketches filter well enough on their own.
+int level2_words(int words) { return words <= 2 ? 4 : (words <= 4 ? 8 : 0); }
+
+FilterFn filter_fn(int words, int words2) {
+    if (words2 == 0) {
+        switch (words) {
+            case 1: return dev::filter_kernel<1, 0>;
+            case 2: return dev::filter_kernel<2, 0>;
+            case 3: return dev::filter_kernel<3, 0>;
+            case 4: return dev::filter_kernel<4, 0>;
+            case 5: return dev::filter_kernel<5, 0>;
+            case 6: return dev::filter_kernel<6, 0>;
+            case 7: return dev::filter_kernel<7, 0>;
+            case 8: return dev::filter_kernel<8, 0>;
+            default: return dev::filter_kernel<0, 0>;
+        }
     }
+    switch (words) {
+        case 1: return dev::filter_kernel<1, 4>;
+        case 2: return dev::filter_kernel<2, 4>;
+        case 3: return dev::filter_kernel<3, 8>;
+        case 4: return dev::filter_kernel<4, 8>;
+    }
+    throw DeviceError("no level-2 filter kernel for this width");
 }
 
 BuildFn build_fn(int words) {
@@ -209,9 +222,10 @@ int filter_colsub(int words) {
     return std::max(32, c);
 }
 
-size_t filter_smem(int words) {
+size_t filter_smem(int words, int words2) {
     const size_t cs = static_cast<size_t>(filter_colsub(words));
-    return 2 * cs * words * 8 + 2 * cs * 4 + 4 * dev::kWarpQueue * sizeof(uint2);
+    const size_t w2 = static_cast<size_t>(words2);
+    return 2 * cs * (words + w2) * 8 + 2 * cs * 4 + 4 * dev::kWarpQueue * sizeof(uint2);
 }
 
 void launch_build(const DeviceReplica& rep, uint64_t* bits, Method method, int width, int hash, cudaStream_t s,
@@ -450,9 +464,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 
     // K1: sketches
     uint64_t* d_bits = A.alloc<uint64_t>((n + kPadRows) * W);
+    const int W2 = enabled ? level2_words(W) : 0;
+    uint64_t* d_bits2 = W2 ? A.alloc<uint64_t>((n + kPadRows) * W2) : nullptr;
     if (enabled) {
         CK(cudaMemsetAsync(d_bits + n * W, 0, kPadRows * W * 8, s));
         launch_build(*rep, d_bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
+        if (W2) {
+            CK(cudaMemsetAsync(d_bits2 + n * W2, 0, kPadRows * W2 * 8, s));
+            launch_build(*rep, d_bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
+        }
     }
     cudaEvent_t e_build = T.mark();
 
@@ -477,8 +497,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     dev::Control h_ctl{};
 
     // filter launch configuration
-    const FilterFn ffn = filter_fn(W);
-    const size_t fsmem = filter_smem(W);
+    const FilterFn ffn = filter_fn(W, W2);
+    const size_t fsmem = filter_smem(W, W2);
     CK(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -487,6 +507,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 
     dev::FilterParams FP{};
     FP.bits = d_bits;
+    FP.bits2 = d_bits2;
     FP.sizes = rep->sizes;
     FP.maxham = d_maxham;
     FP.wstart = d_wstart;

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kBuildRecs) build_sketches(BuildParams P) {
 // ================================================================ K2: filter
 struct FilterParams {
     const uint64_t* bits;        // sketches, n * W words (padded by kColSub rows)
+    const uint64_t* bits2;       // level-2 Xor sketches, n * W2 words (W2 = 0: none)
     const uint32_t* sizes;       // |r| per record (padded)
     const int32_t* maxham;       // maxham[S] = S - 2*minov[S], S in [0, 2*max_size]
     const uint32_t* wstart;      // j0 per record size
@@ -276,14 +277,25 @@ __device__ __forceinline__ void emit_group(uint32_t m, uint32_t base_col, uint32
 // W x (2 LOP3 + 2 POPC) + IADD3 + SHF.  skip <=> popcount(b_i ^ b_j) >
 // maxham[|r_i|+|r_j|], the exact integer form of reference
 // src/bitmap.cpp:125-143 with src/similarity.cpp:113-115.
-template <int W>
+//
+// Level 2 (W2 > 0): the level-1 mask m alone defines the reference counters
+// (per-row survivors); pairs in m are additionally tested against a wider
+// Xor sketch (b2 = 64*W2 bits, same exact threshold) before they are emitted
+// for verification.  Both tests are sound upper bounds on the overlap, so the
+// emitted set still contains every matching pair -- it only spares the
+// verifier the pairs a b-bit sketch cannot reject (at tau = 0.5 on C2 with
+// b = 128 that is 43% of all window pairs).  Dense groups test all 32 columns;
+// sparse ones only the surviving columns of each lane.
+template <int W, int W2>
 __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
     constexpr int WS = W > 0 ? W : 1;
+    constexpr int WS2 = W2 > 0 ? W2 : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* s_bits = reinterpret_cast<uint64_t*>(smem_raw);                  // [2][colsub*W]
     const int words = W > 0 ? W : P.words;
     const int colsub = W > 0 ? kColSub : P.colsub;  // columns per stage
-    uint32_t* s_size = reinterpret_cast<uint32_t*>(s_bits + 2 * colsub * words);  // [2][colsub]
+    uint64_t* s_bits = reinterpret_cast<uint64_t*>(smem_raw);                  // [2][colsub*W]
+    uint64_t* s_bits2 = s_bits + 2 * colsub * words;                           // [2][colsub*W2]
+    uint32_t* s_size = reinterpret_cast<uint32_t*>(s_bits2 + 2 * colsub * W2);  // [2][colsub]
     uint2* s_queue = reinterpret_cast<uint2*>(s_size + 2 * colsub);            // [4][kWarpQueue]
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ unsigned long long s_item;
@@ -298,7 +310,7 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t phase[2] = {0, 0};
+    uint32_t phase = 0;  // bit b = parity of stage buffer b
 
     for (;;) {
         if (tid == 0) {
@@ -328,9 +340,13 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
         const uint32_t c0 = P.tile_col_lo[tile] + chunk * kColChunk;
         const uint32_t c1 = min(c0 + kColChunk, tile_rows_end - 1);  // columns < last row
 
-        uint64_t mine[WS];
+        uint64_t mine[WS], mine2[WS2];
         uint32_t si = 0, j0 = 0;
         bool bypass = P.bypass_all != 0;
+#pragma unroll
+        for (int w = 0; w < WS; ++w) mine[w] = 0;
+#pragma unroll
+        for (int w = 0; w < WS2; ++w) mine2[w] = 0;
         if (valid) {
             si = P.sizes[i];
             j0 = P.naive ? 0u : P.wstart[si];
@@ -339,26 +355,27 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) mine[w] = P.bits[static_cast<uint64_t>(i) * W + w];
             }
-        } else {
-            if constexpr (W > 0) {
+            if constexpr (W2 > 0) {
 #pragma unroll
-                for (int w = 0; w < W; ++w) mine[w] = 0;
+                for (int w = 0; w < W2; ++w) mine2[w] = P.bits2[static_cast<uint64_t>(i) * W2 + w];
             }
         }
         const uint32_t lo_i = valid ? max(j0, c0) : c1;
         const uint32_t hi_i = valid ? min(i, c1) : c1;
         uint32_t cnt = 0;
 
-        // stage 0 prefetch
         const uint32_t nsub = (c1 - c0 + colsub - 1) / colsub;
         auto issue = [&](uint32_t s, int buf) {
             const uint32_t cs = c0 + s * colsub;
             const uint32_t ncol = min(static_cast<uint32_t>(colsub), c1 - cs);
             const uint32_t ncol4 = (ncol + 3) & ~3u;  // padded allocation keeps this in bounds
             const uint32_t bb = ncol4 * 8u * static_cast<uint32_t>(words);
+            const uint32_t bb2 = ncol4 * 8u * static_cast<uint32_t>(W2);
             const uint32_t sb = ncol4 * 4u;
-            mbar_expect_tx(&bars[buf], bb + sb);
+            mbar_expect_tx(&bars[buf], bb + bb2 + sb);
             tma_load_1d(s_bits + buf * colsub * words, P.bits + static_cast<uint64_t>(cs) * words, bb, &bars[buf]);
+            if constexpr (W2 > 0)
+                tma_load_1d(s_bits2 + buf * colsub * W2, P.bits2 + static_cast<uint64_t>(cs) * W2, bb2, &bars[buf]);
             tma_load_1d(s_size + buf * colsub, P.sizes + cs, sb, &bars[buf]);
         };
         if (tid == 0 && nsub > 0) issue(0, 0);
@@ -366,11 +383,12 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
         for (uint32_t s = 0; s < nsub; ++s) {
             const int buf = s & 1;
             if (tid == 0 && s + 1 < nsub) issue(s + 1, buf ^ 1);
-            mbar_wait(&bars[buf], phase[buf]);
-            phase[buf] ^= 1;
+            mbar_wait(&bars[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
             const uint32_t cs = c0 + s * colsub;
             const uint32_t ncol = min(static_cast<uint32_t>(colsub), c1 - cs);
             const uint64_t* cb = s_bits + buf * colsub * words;
+            const uint64_t* cb2 = s_bits2 + buf * colsub * W2;
             const uint32_t* cz = s_size + buf * colsub;
             const uint32_t sz_first = cz[0], sz_last = cz[ncol - 1];
             const bool uniform = sz_first == sz_last;
@@ -417,7 +435,36 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
                     }
                     m = bypass ? rm : (m & rm);
                     cnt += __popc(m);
-                    if (__any_sync(0xFFFFFFFFu, m != 0)) emit_group(m, gbase, i, q, qlen, P, lane);
+                    uint32_t e = m;  // emitted for verification
+                    if constexpr (W2 > 0) {
+                        const uint32_t most = __reduce_max_sync(0xFFFFFFFFu, static_cast<uint32_t>(__popc(m)));
+                        if (most > 8 && uniform && kmax == 32) {
+                            uint32_t m2 = 0;
+#pragma unroll 8
+                            for (int k = 0; k < 32; ++k) {
+                                const uint64_t* col = cb2 + (g + k) * W2;
+                                int h = 0;
+#pragma unroll
+                                for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
+                                m2 = __funnelshift_l(static_cast<uint32_t>(h + negT1), m2, 1);
+                            }
+                            e = m & __brev(m2);
+                        } else if (most > 0) {
+                            uint32_t mm = m;
+                            e = 0;
+                            while (mm) {
+                                const int k = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                const uint64_t* col = cb2 + (g + k) * W2;
+                                int h = 0;
+#pragma unroll
+                                for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
+                                const int T = uniform ? -negT1 - 1 : __ldg(P.maxham + si + cz[g + k]);
+                                e |= (h <= T ? 1u : 0u) << k;
+                            }
+                        }
+                    }
+                    if (__any_sync(0xFFFFFFFFu, e != 0)) emit_group(e, gbase, i, q, qlen, P, lane);
                 }
             }
             __syncthreads();  // stage buffer free for the TMA issued next iteration
