@@ -116,16 +116,22 @@ struct DeviceReplica {
     uint32_t* sizes = nullptr;
     size_t n = 0;
     uint64_t bytes = 0;
+    cudaStream_t stream = nullptr;  // set for per-join replicas: stream-ordered alloc/free
     ~DeviceReplica() {
-        if (device >= 0) {
-            int cur = 0;
-            cudaGetDevice(&cur);
-            cudaSetDevice(device);
-            cudaFree(tokens);
-            cudaFree(offsets);
-            cudaFree(sizes);
-            cudaSetDevice(cur);
+        if (device < 0) return;
+        if (stream) {
+            cudaFreeAsync(tokens, stream);
+            cudaFreeAsync(offsets, stream);
+            cudaFreeAsync(sizes, stream);
+            return;
         }
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaFree(tokens);
+        cudaFree(offsets);
+        cudaFree(sizes);
+        cudaSetDevice(cur);
     }
 };
 
@@ -138,13 +144,21 @@ __global__ void sizes_from_offsets(const uint64_t* off, uint32_t* sizes, size_t 
 }
 
 std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
-                                      uint64_t& launches) {
+                                      uint64_t& launches, bool resident = false) {
     register_host(c);
     auto rep = std::make_shared<DeviceReplica>();
     const size_t n = c.size();
-    CK(cudaMalloc(&rep->tokens, std::max<size_t>(c.tokens.size(), 4) * sizeof(uint32_t) + 16));
-    CK(cudaMalloc(&rep->offsets, (n + 1) * sizeof(uint64_t)));
-    CK(cudaMalloc(&rep->sizes, (n + kPadRows) * sizeof(uint32_t)));
+    const size_t tok_bytes = std::max<size_t>(c.tokens.size(), 4) * sizeof(uint32_t) + 16;
+    if (resident) {
+        CK(cudaMalloc(&rep->tokens, tok_bytes));
+        CK(cudaMalloc(&rep->offsets, (n + 1) * sizeof(uint64_t)));
+        CK(cudaMalloc(&rep->sizes, (n + kPadRows) * sizeof(uint32_t)));
+    } else {
+        rep->stream = stream;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->tokens), tok_bytes, stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->offsets), (n + 1) * sizeof(uint64_t), stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows) * sizeof(uint32_t), stream));
+    }
     rep->device = device;
     rep->n = n;
     if (!c.tokens.empty())
@@ -379,7 +393,7 @@ void engine_pin(const Collection& c, int device) {
         std::lock_guard<std::mutex> lk(c.dev_mu);
         register_host(c);
     }
-    rep = upload(c, device, s, h2d, launches);
+    rep = upload(c, device, s, h2d, launches, true);
     CK(cudaStreamSynchronize(s));
     cudaStreamDestroy(s);
     std::lock_guard<std::mutex> lk(c.dev_mu);
@@ -483,6 +497,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
+    // per-(item,row) survivor counts let the saturation rescan touch one chunk per row
+    const uint64_t n_items = tl.item_base.back();
+    const bool keep_item_counts = !naive && n_items * dev::kRowTile * 2 <= (uint64_t(1) << 30);
+    uint16_t* d_item_counts = keep_item_counts ? A.alloc<uint16_t>(n_items * dev::kRowTile) : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
     SB.ka = A.alloc<unsigned long long>(res_cap);
@@ -515,6 +533,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     FP.tile_col_lo = d_col_lo;
     FP.surv = d_surv;
     FP.rowcnt = d_rowcnt;
+    FP.item_counts = d_item_counts;
     FP.ctl = d_ctl;
     FP.surv_cap = surv_cap;
     FP.ntiles = tl.ntiles;
@@ -641,6 +660,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         RP.maxham = d_maxham;
         RP.wstart = d_wstart;
         RP.rowcnt = d_rowcnt;
+        RP.item_counts = d_item_counts;
+        RP.item_base = d_item_base;
+        RP.tile_col_lo = d_col_lo;
         RP.jstar = d_jstar;
         RP.row_begin = static_cast<uint32_t>(plan.row_begin);
         RP.row_end = static_cast<uint32_t>(plan.row_end);

@@ -172,6 +172,7 @@ struct FilterParams {
     const uint32_t* tile_col_lo; // first (32-aligned) column of each tile's span
     uint2* surv;                 // survivors (j, i)
     uint32_t* rowcnt;            // survivors per row (row - row_begin)
+    uint16_t* item_counts;       // survivors per (item, row-in-tile) for the rescan, or null
     Control* ctl;
     unsigned long long surv_cap;
     unsigned long long item_begin, item_end;
@@ -470,6 +471,7 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
             __syncthreads();  // stage buffer free for the TMA issued next iteration
         }
         if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
+        if (P.item_counts) P.item_counts[item * kRowTile + tid] = static_cast<uint16_t>(cnt);
         __syncthreads();  // s_item / s_tile / stage buffers are rewritten next item
     }
     if (qlen) warp_flush(q, qlen, P, lane);
@@ -482,7 +484,10 @@ struct RescanParams {
     const int32_t* maxham;
     const uint32_t* wstart;
     const uint32_t* rowcnt;
-    uint32_t* jstar;         // capacity-th survivor column per row (row - row_begin)
+    const uint16_t* item_counts;  // per (item, row-in-tile) survivors, or null
+    const uint64_t* item_base;    // per tile
+    const uint32_t* tile_col_lo;
+    uint32_t* jstar;              // capacity-th survivor column per row (row - row_begin)
     uint32_t row_begin, row_end;
     uint32_t capacity;
     int64_t cutoff;
@@ -490,9 +495,10 @@ struct RescanParams {
     int bypass_all;
 };
 
-// One warp per row whose survivor count reaches the capacity: walk the window
-// in order and locate the capacity-th survivor (the reference's saturation
-// point, src/parallel_join.cpp:83-94).
+// One warp per row whose survivor count reaches the capacity: locate the
+// capacity-th survivor in window order (the reference's saturation point,
+// src/parallel_join.cpp:83-94).  With per-item counts from the filter only the
+// single 4096-column chunk holding it is rescanned; 128 columns per step.
 __global__ void rescan_saturated(RescanParams P) {
     const int lane = threadIdx.x & 31;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -506,26 +512,49 @@ __global__ void rescan_saturated(RescanParams P) {
             if (lane == 0) P.jstar[r] = j0 + P.capacity - 1;
             continue;
         }
+        uint32_t start = j0, stop = i, seen = 0;
+        if (P.item_counts) {
+            const uint32_t tile = r / kRowTile, t = r % kRowTile;
+            const uint64_t ib = P.item_base[tile], ie = P.item_base[tile + 1];
+            for (uint64_t it = ib; it < ie; ++it) {
+                const uint32_t cc = P.item_counts[it * kRowTile + t];
+                if (seen + cc >= P.capacity) {
+                    const uint32_t c0 = P.tile_col_lo[tile] + static_cast<uint32_t>(it - ib) * kColChunk;
+                    start = max(j0, c0);
+                    stop = min(i, c0 + kColChunk);
+                    break;
+                }
+                seen += cc;
+            }
+        }
         const uint64_t* me = P.bits + static_cast<uint64_t>(i) * P.words;
-        uint32_t seen = 0;
-        for (uint32_t jb = j0; jb < i; jb += 32) {
-            const uint32_t j = jb + lane;
-            bool surv = false;
-            if (j < i) {
-                const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
-                int h = 0;
-                for (int w = 0; w < P.words; ++w) h += __popcll(me[w] ^ o[w]);
-                surv = h <= P.maxham[si + P.sizes[j]];
+        for (uint32_t jb = start; jb < stop; jb += 128) {
+            uint32_t bal[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t j = jb + q * 32 + lane;
+                bool surv = false;
+                if (j < stop) {
+                    const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
+                    int h = 0;
+                    for (int w = 0; w < P.words; ++w) h += __popcll(__ldg(me + w) ^ __ldg(o + w));
+                    surv = h <= __ldg(P.maxham + si + __ldg(P.sizes + j));
+                }
+                bal[q] = __ballot_sync(0xFFFFFFFFu, surv);
             }
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
-            const uint32_t pc = __popc(bal);
-            if (seen + pc >= P.capacity) {
-                uint32_t b2 = bal;  // drop the first (need-1) survivors of this group
-                for (uint32_t k = P.capacity - seen; k > 1; --k) b2 &= b2 - 1;
-                if (lane == 0) P.jstar[r] = jb + static_cast<uint32_t>(__ffs(b2) - 1);
-                break;
+            bool done = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t pc = __popc(bal[q]);
+                if (!done && seen + pc >= P.capacity) {
+                    uint32_t b2 = bal[q];  // drop the first (need-1) survivors of this group
+                    for (uint32_t k = P.capacity - seen; k > 1; --k) b2 &= b2 - 1;
+                    if (lane == 0) P.jstar[r] = jb + q * 32 + static_cast<uint32_t>(__ffs(b2) - 1);
+                    done = true;
+                }
+                if (!done) seen += pc;
             }
-            seen += pc;
+            if (done) break;
         }
     }
 }
