@@ -15,6 +15,7 @@
 
 #include "engine.hpp"
 #include "kernels.cuh"
+#include "filter_tc.cuh"
 
 namespace ssjb {
 
@@ -137,10 +138,12 @@ struct DeviceReplica {
 
 namespace {
 
+// |r| per record; the padding rows repeat the largest size so the array stays
+// sorted (the filters test size-uniform column groups by their end points).
 __global__ void sizes_from_offsets(const uint64_t* off, uint32_t* sizes, size_t n) {
     size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (r < n) sizes[r] = static_cast<uint32_t>(off[r + 1] - off[r]);
-    else if (r < n + kPadRows) sizes[r] = 0;
+    else if (r < n + kPadRows) sizes[r] = n ? static_cast<uint32_t>(off[n] - off[n - 1]) : 0u;
 }
 
 std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
@@ -240,6 +243,50 @@ size_t filter_smem(int words, int words2) {
     const size_t cs = static_cast<size_t>(filter_colsub(words));
     const size_t w2 = static_cast<size_t>(words2);
     return 2 * cs * (words + w2) * 8 + 2 * cs * 4 + 4 * dev::kWarpQueue * sizeof(uint2);
+}
+
+struct TcKernel {
+    void (*fn)(dev::TcParams);
+    int smem;
+};
+
+template <int KA, int K2, int W2, int NS>
+TcKernel tc_kernel() {
+    return TcKernel{dev::filter_tc_kernel<KA, K2, W2, NS>, dev::TcLayout<KA, K2, W2, NS>::kBytes};
+}
+
+// Tensor-core filter instantiations: level-1 width b = 64*words (K = b + 32),
+// level 2 as a second GEMM on 256-bit Xor sketches (l2gemm) or a POPC check.
+TcKernel tc_select(int words, bool l2gemm) {
+    if (l2gemm) {
+        switch (words) {
+            case 1: return tc_kernel<96, 288, 4, 2>();
+            case 2: return tc_kernel<160, 288, 4, 2>();
+        }
+    } else {
+        switch (words) {
+            case 1: return tc_kernel<96, 0, 4, 4>();
+            case 2: return tc_kernel<160, 0, 4, 4>();
+            case 3: return tc_kernel<224, 0, 8, 4>();
+            case 4: return tc_kernel<288, 0, 8, 3>();
+        }
+    }
+    throw DeviceError("no tensor-core filter instantiation for this width");
+}
+
+void launch_expand(const uint64_t* bits, int words, uint8_t* opA, uint8_t* opB, uint32_t rows, cudaStream_t s,
+                   uint64_t& launches) {
+    dev::ExpandParams E{};
+    E.bits = bits;
+    E.opA = opA;
+    E.opB = opB;
+    E.rows = rows;
+    E.words = words;
+    E.K = 64 * words + 32;
+    const uint64_t threads = static_cast<uint64_t>(rows) * (E.K / 16);
+    dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
+    ++launches;
+    CK(cudaGetLastError());
 }
 
 void launch_build(const DeviceReplica& rep, uint64_t* bits, Method method, int width, int hash, cudaStream_t s,
@@ -477,15 +524,46 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     cudaEvent_t e_up = T.mark();
 
     // K1: sketches
-    uint64_t* d_bits = A.alloc<uint64_t>((n + kPadRows) * W);
+    uint64_t* d_bits = A.alloc<uint64_t>((n + kPadRows + 8) * W);
     const int W2 = enabled ? level2_words(W) : 0;
-    uint64_t* d_bits2 = W2 ? A.alloc<uint64_t>((n + kPadRows) * W2) : nullptr;
+    uint64_t* d_bits2 = W2 ? A.alloc<uint64_t>((n + kPadRows + 8) * W2) : nullptr;
     if (enabled) {
-        CK(cudaMemsetAsync(d_bits + n * W, 0, kPadRows * W * 8, s));
+        CK(cudaMemsetAsync(d_bits + n * W, 0, (kPadRows + 8) * W * 8, s));
         launch_build(*rep, d_bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
         if (W2) {
-            CK(cudaMemsetAsync(d_bits2 + n * W2, 0, kPadRows * W2 * 8, s));
+            CK(cudaMemsetAsync(d_bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
             launch_build(*rep, d_bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
+        }
+    }
+    // K2 flavour: tcgen05 int8 GEMM filter where it applies, POPC otherwise
+    const char* fenv = std::getenv("SSJB_FILTER");
+    const bool tc_ok = enabled && W <= 4 && plan.row_begin % 8 == 0;
+    const bool use_tc = tc_ok && !(fenv && std::string(fenv) == "popc");
+    bool l2gemm = false;
+    if (use_tc && W <= 2 && W2 == 4) {
+        const char* genv = std::getenv("SSJB_L2GEMM");
+        if (genv && *genv) {
+            l2gemm = std::atoi(genv) != 0;
+        } else {
+            // dense regime: the b-bit Xor sketch stops discriminating near the
+            // median record size (the paper's cutoff analysis), so most window
+            // pairs survive level 1 and the level-2 check runs as a GEMM too
+            const int64_t cx = cutoff(Method::Xor, width, Rational(plan.p, plan.q), true);
+            l2gemm = static_cast<double>(cx) < 1.25 * static_cast<double>(c.median_size());
+        }
+    }
+    const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
+    uint8_t *d_opA = nullptr, *d_opB = nullptr, *d_opA2 = nullptr, *d_opB2 = nullptr;
+    if (use_tc) {
+        const size_t KA = 64 * W + 32;
+        d_opA = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * KA);
+        d_opB = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * KA);
+        launch_expand(d_bits, W, d_opA, d_opB, n_pad, s, st.launches);
+        if (l2gemm) {
+            const size_t K2 = 64 * W2 + 32;
+            d_opA2 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * K2);
+            d_opB2 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * K2);
+            launch_expand(d_bits2, W2, d_opA2, d_opB2, n_pad, s, st.launches);
         }
     }
     cudaEvent_t e_build = T.mark();
@@ -499,8 +577,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
     // per-(item,row) survivor counts let the saturation rescan touch one chunk per row
     const uint64_t n_items = tl.item_base.back();
-    const bool keep_item_counts = !naive && n_items * dev::kRowTile * 2 <= (uint64_t(1) << 30);
-    uint16_t* d_item_counts = keep_item_counts ? A.alloc<uint16_t>(n_items * dev::kRowTile) : nullptr;
+    const bool keep_item_counts = !naive && n_items * dev::kRowTile * 4 <= (uint64_t(1) << 30);
+    uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * dev::kRowTile) : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
     SB.ka = A.alloc<unsigned long long>(res_cap);
@@ -544,6 +622,35 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     FP.colsub = filter_colsub(W);
     FP.bypass_all = enabled ? 0 : 1;
     FP.naive = naive ? 1 : 0;
+
+    dev::TcParams TP{};
+    TcKernel tck{nullptr, 0};
+    if (use_tc) {
+        tck = tc_select(W, l2gemm);
+        CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
+        TP.opA = d_opA;
+        TP.opB = d_opB;
+        TP.opA2 = d_opA2;
+        TP.opB2 = d_opB2;
+        TP.bits = d_bits;
+        TP.bits2 = d_bits2;
+        TP.sizes = rep->sizes;
+        TP.maxham = d_maxham;
+        TP.wstart = d_wstart;
+        TP.item_base = d_item_base;
+        TP.tile_col_lo = d_col_lo;
+        TP.surv = d_surv;
+        TP.rowcnt = d_rowcnt;
+        TP.item_counts = d_item_counts;
+        TP.ctl = d_ctl;
+        TP.surv_cap = surv_cap;
+        TP.ntiles = tl.ntiles;
+        TP.row_begin = static_cast<uint32_t>(plan.row_begin);
+        TP.row_end = static_cast<uint32_t>(plan.row_end);
+        TP.cutoff = FP.cutoff;
+        TP.neg1 = -1;
+        st.filter_kernel = l2gemm ? 2 : 1;
+    }
 
     dev::VerifyParams VP{};
     VP.tokens = rep->tokens;
@@ -604,9 +711,18 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         FP.item_begin = ib;
         FP.item_end = ie;
         FP.tile_begin = tb;
-        const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms) * per_sm);
+        if (d_item_counts) CK(cudaMemsetAsync(d_item_counts + ib * dev::kRowTile, 0, (ie - ib) * dev::kRowTile * 4, s));
         cudaEvent_t a = T.mark();
-        ffn<<<static_cast<unsigned>(grid), dev::kRowTile, fsmem, s>>>(FP);
+        if (use_tc) {
+            TP.item_begin = ib;
+            TP.item_end = ie;
+            TP.tile_begin = tb;
+            const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms));
+            tck.fn<<<static_cast<unsigned>(grid), dev::kTcThreads, tck.smem, s>>>(TP);
+        } else {
+            const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms) * per_sm);
+            ffn<<<static_cast<unsigned>(grid), dev::kRowTile, fsmem, s>>>(FP);
+        }
         ++st.launches;
         CK(cudaGetLastError());
         cudaEvent_t b = T.mark();
@@ -729,7 +845,6 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     out.candidates_s = (st.ms_filter + st.ms_rescan) * 1e-3;
     const double total = std::chrono::duration<double>(Clock::now() - t_start).count();
     out.verify_s = std::max(0.0, total - out.index_s - out.candidates_s);
-    st.filter_kernel = 0;
 }
 
 }  // namespace ssjb

@@ -1,0 +1,486 @@
+// Tensor-core Bitmap Filter (K2, tcgen05 path).  Included by engine.cu.
+//
+// The xor/popcount bound is a dot product:  popcount(b_i ^ b_j) =
+// pc_i + pc_j - 2 <b_i, b_j>.  So the filter for a 128-row x 128-column tile
+// is one int8 GEMM.  Operands are the sketches expanded to one byte per bit
+// (kernel expand_operands), K-major, in the tcgen05 core-matrix layout
+// (8 rows x 16 bytes per 128-byte core matrix), with a 32-byte extension block:
+//
+//   A_i = [ bit_k(b_i) in {0,1}  (k < b) | 1, 1, 0 ... ]                  (u8)
+//   B_j = [ 2*bit_k(b_j) in {0,2} (k < b) | -ceil(pc_j/2), -floor(pc_j/2), 0...] (s8)
+//   D_ij = sum_k A_ik B_jk = 2 <b_i, b_j> - pc_j                          (s32, TMEM)
+//
+// survive  <=>  popcount <= T(|r_i|+|r_j|)  <=>  D_ij >= pc_i - T  -- exact
+// integers throughout, identical to the POPC kernel and to reference
+// src/bitmap.cpp:125-143.
+//
+// Warp roles (320 threads, one CTA per SM, persistent over work items):
+//   warp 0      TMA producer: row tile A (once per item), column tiles B
+//               + sizes (+ level-2 sketches) into an NS-stage ring
+//   warp 1      TMEM allocator and MMA issuer (one elected lane, kind::i8,
+//               M=128, N=128, K=32 per instruction) into 2 accumulator slots
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32, exact threshold, survivor
+//               masks, per-row counts, level-2 check, warp-queued emission
+// Level 2 is either a second GEMM on the 256-bit Xor sketches (dense regimes,
+// L2G) or a POPC check of the level-1 survivors against staged sketches.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace ssjb {
+namespace dev {
+
+constexpr int kTcN = 128;          // columns per MMA tile
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
+constexpr int kTcQueue = 256;      // survivor staging per epilogue warp
+
+struct TcParams {
+    const uint8_t* opA;        // expanded level-1 rows, core layout, n_pad x KA
+    const uint8_t* opB;        // expanded level-1 columns (s8), n_pad x KA
+    const uint8_t* opA2;       // level-2 GEMM operands (L2G), n_pad x K2
+    const uint8_t* opB2;
+    const uint64_t* bits;      // level-1 sketches (row popcounts)
+    const uint64_t* bits2;     // level-2 Xor sketches (rows; staged columns for the POPC check)
+    const uint32_t* sizes;
+    const int32_t* maxham;
+    const uint32_t* wstart;
+    const uint64_t* item_base;
+    const uint32_t* tile_col_lo;
+    uint2* surv;
+    uint32_t* rowcnt;
+    uint32_t* item_counts;     // per (item, row-in-tile), u32 (two column halves add)
+    Control* ctl;
+    unsigned long long surv_cap;
+    unsigned long long item_begin, item_end;
+    uint32_t tile_begin, ntiles;
+    uint32_t row_begin, row_end;
+    int64_t cutoff;
+    int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo) {
+    // K-major, SWIZZLE_NONE: LBO = 128 B between the two 16-byte K halves of
+    // an instruction, SBO = stride between 8-row core-matrix groups.
+    uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(128 >> 4) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // sm100 descriptor version
+    return d;
+}
+
+// kind::i8, D s32, A u8, B s8, K-major both, M = 128, N = kTcN
+constexpr uint32_t kTcIdesc = (2u << 4) | (0u << 7) | (1u << 10) | ((kTcN >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+          "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Survivor mask of 32 accumulator columns: column k survives iff
+// cim1_k - D_k < 0 (sign bit set).  Four independent funnel-shift chains
+// (8 columns each) keep the ALU pipe fed; the subtraction is an IMAD on the
+// FMA pipe (neg1 == -1 arrives as a kernel parameter so ptxas keeps it there).
+// Result: bit k = column k.
+template <bool kUniform>
+__device__ __forceinline__ uint32_t survivors32(const uint32_t (&d)[32], int cim1, const int (&cims)[32], int neg1) {
+    uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int c0 = kUniform ? cim1 : cims[j], c1 = kUniform ? cim1 : cims[8 + j];
+        const int c2 = kUniform ? cim1 : cims[16 + j], c3 = kUniform ? cim1 : cims[24 + j];
+        m0 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[j]) * neg1 + c0), m0, 1);
+        m1 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[8 + j]) * neg1 + c1), m1, 1);
+        m2 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[16 + j]) * neg1 + c2), m2, 1);
+        m3 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[24 + j]) * neg1 + c3), m3, 1);
+    }
+    // m_c bit (7-j) = column 8c+j  ->  bit 31-k = column k  ->  brev
+    return __brev((m0 << 24) | (m1 << 16) | (m2 << 8) | m3);
+}
+
+__device__ __forceinline__ uint32_t survivors_tile(const uint32_t (&d)[32], bool uniform, int base,
+                                                   const int32_t* maxham, uint32_t si, const uint32_t* cz, int neg1) {
+    int dummy[32];
+    if (uniform) return survivors32<true>(d, base - __ldg(maxham + si + cz[0]) - 1, dummy, neg1);
+    int cims[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cims[k] = base - __ldg(maxham + si + cz[k]) - 1;
+    return survivors32<false>(d, 0, cims, neg1);
+}
+
+__device__ __forceinline__ void tc_flush(uint2* q, int& qlen, const TcParams& P, int lane) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(qlen));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int k = lane; k < qlen; k += 32)
+        if (base + k < P.surv_cap) P.surv[base + k] = q[k];
+    qlen = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void tc_emit(uint32_t m, uint32_t base_col, uint32_t row, uint2* q, int& qlen,
+                                        const TcParams& P, int lane) {
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const int excl = incl - c;
+    if (total > kTcQueue) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(total));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + excl;
+        while (m) {
+            int k = __ffs(m) - 1;
+            m &= m - 1;
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + k, row);
+            ++base;
+        }
+        return;
+    }
+    if (qlen + total > kTcQueue) tc_flush(q, qlen, P, lane);
+    int pos = qlen + excl;
+    while (m) {
+        int k = __ffs(m) - 1;
+        m &= m - 1;
+        q[pos++] = make_uint2(base_col + k, row);
+    }
+    qlen += total;
+    __syncwarp();
+}
+
+struct TcItem {
+    unsigned long long item;
+    uint32_t tile, c0, c1, ntiles, done;
+};
+
+// KA: level-1 operand bytes per row; K2: level-2 GEMM operand bytes (0: none);
+// W2: level-2 Xor sketch words for the POPC check (used when K2 == 0); NS: B stages.
+template <int KA, int K2, int W2, int NS>
+struct TcLayout {
+    static constexpr int kA = 128 * (KA + K2);                 // one A slot
+    static constexpr int kBop = kTcN * (KA + K2);              // B operands per stage
+    static constexpr int kBsk = K2 ? 0 : kTcN * W2 * 8;        // staged level-2 sketches
+    static constexpr int kBsz = kTcN * 4;                      // sizes
+    static constexpr int kB = kBop + kBsk + kBsz;
+    static constexpr int kAslots = K2 ? 1 : 2;
+    static constexpr int kQueue = kTcEpiWarps * kTcQueue * 8;
+    static constexpr int kBytes = kAslots * kA + NS * kB + kQueue;
+};
+
+template <int KA, int K2, int W2, int NS>
+__global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
+    using L = TcLayout<KA, K2, W2, NS>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;                                   // [2][kA]
+    uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
+    uint2* sQ = reinterpret_cast<uint2*>(sB + NS * L::kB);  // [8][kTcQueue]
+    __shared__ __align__(8) uint64_t item_full[2], item_empty[2], a_full[2], a_empty[2];
+    __shared__ __align__(8) uint64_t b_full[NS], b_empty[NS], acc_full[2], acc_empty[2];
+    __shared__ TcItem items[2];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t kTmemCols = K2 ? 512 : 256;  // 2 slots x (L1 [+ L2]) x 128 columns
+
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&item_full[s], 1);
+            mbar_init(&item_empty[s], 1 + kTcEpiWarps);
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 1);
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], kTcEpiWarps);
+        }
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1 + kTcEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem_base = tmem_base_sh;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t iseq = 0, tseq = 0;
+            for (;;) {
+                const int slot = iseq & 1;
+                mbar_wait(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
+                const unsigned long long it = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                TcItem info{};
+                info.item = it;
+                if (it >= P.item_end) {
+                    info.done = 1;
+                    items[slot] = info;
+                    mbar_arrive(&item_full[slot]);
+                    break;
+                }
+                uint32_t lo = P.tile_begin, hi = P.ntiles;
+                while (hi - lo > 1) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    if (P.item_base[mid] <= it) lo = mid; else hi = mid;
+                }
+                const uint32_t tile = lo;
+                const uint32_t chunk = static_cast<uint32_t>(it - P.item_base[tile]);
+                const uint32_t row0 = P.row_begin + tile * kRowTile;
+                const uint32_t rows_end = min(row0 + kRowTile, P.row_end);
+                info.tile = tile;
+                info.c0 = P.tile_col_lo[tile] + chunk * kColChunk;
+                info.c1 = min(info.c0 + kColChunk, rows_end - 1);
+                info.ntiles = (info.c1 - info.c0 + kTcN - 1) / kTcN;
+                info.done = 0;
+                items[slot] = info;
+                // row operand (A): 128 rows, contiguous in the core layout
+                const int aslot = iseq % L::kAslots;
+                mbar_wait(&a_empty[aslot], ((iseq / L::kAslots) & 1) ^ 1);
+                mbar_expect_tx(&a_full[aslot], L::kA);
+                tma_load_1d(sA + aslot * L::kA, P.opA + static_cast<uint64_t>(row0) * KA, 128 * KA, &a_full[aslot]);
+                if constexpr (K2 > 0)
+                    tma_load_1d(sA + aslot * L::kA + 128 * KA, P.opA2 + static_cast<uint64_t>(row0) * K2, 128 * K2,
+                                &a_full[aslot]);
+                mbar_arrive(&item_full[slot]);
+                for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
+                    const int st = tseq % NS;
+                    mbar_wait(&b_empty[st], ((tseq / NS) & 1) ^ 1);
+                    const uint32_t col = info.c0 + t * kTcN;
+                    uint8_t* dst = sB + st * L::kB;
+                    mbar_expect_tx(&b_full[st], L::kB);
+                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * KA, kTcN * KA, &b_full[st]);
+                    if constexpr (K2 > 0)
+                        tma_load_1d(dst + kTcN * KA, P.opB2 + static_cast<uint64_t>(col) * K2, kTcN * K2, &b_full[st]);
+                    if constexpr (K2 == 0 && W2 > 0)
+                        tma_load_1d(dst + L::kBop, P.bits2 + static_cast<uint64_t>(col) * W2, L::kBsk, &b_full[st]);
+                    tma_load_1d(dst + L::kBop + L::kBsk, P.sizes + col, L::kBsz, &b_full[st]);
+                }
+                ++iseq;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t iseq = 0, tseq = 0, aseq = 0;
+            for (;;) {
+                const int slot = iseq & 1;
+                mbar_wait(&item_full[slot], (iseq >> 1) & 1);
+                const TcItem info = items[slot];
+                mbar_arrive(&item_empty[slot]);
+                if (info.done) break;
+                const int aslot = iseq % L::kAslots;
+                mbar_wait(&a_full[aslot], (iseq / L::kAslots) & 1);
+                const uint32_t a0 = smem_u32(sA + aslot * L::kA);
+                for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
+                    const int st = tseq % NS;
+                    const int as = aseq & 1;
+                    mbar_wait(&b_full[st], (tseq / NS) & 1);
+                    mbar_wait(&acc_empty[as], ((aseq >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t b0 = smem_u32(sB + st * L::kB);
+                    const uint32_t d1 = tmem_base + as * kTcN;
+#pragma unroll
+                    for (int s = 0; s < KA / 32; ++s)
+                        umma_i8(d1, umma_desc(a0 + s * 256, (KA / 16) * 128), umma_desc(b0 + s * 256, (KA / 16) * 128),
+                                s > 0);
+                    if constexpr (K2 > 0) {
+                        const uint32_t d2 = tmem_base + 256 + as * kTcN;
+#pragma unroll
+                        for (int s = 0; s < K2 / 32; ++s)
+                            umma_i8(d2, umma_desc(a0 + 128 * KA + s * 256, (K2 / 16) * 128),
+                                    umma_desc(b0 + kTcN * KA + s * 256, (K2 / 16) * 128), s > 0);
+                    }
+                    umma_commit(&b_empty[st]);
+                    umma_commit(&acc_full[as]);
+                }
+                umma_commit(&a_empty[aslot]);
+                ++iseq;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int ew = warp - 2;
+        const int quarter = warp & 3;          // TMEM lanes 32*quarter .. +31
+        const int half = ew >> 2;              // columns 64*half .. +63 of each tile
+        const int rit = quarter * 32 + lane;   // row in tile
+        uint2* q = sQ + ew * kTcQueue;
+        int qlen = 0;
+        uint32_t iseq = 0, tseq = 0, aseq = 0;
+        for (;;) {
+            const int slot = iseq & 1;
+            mbar_wait(&item_full[slot], (iseq >> 1) & 1);
+            const TcItem info = items[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&item_empty[slot]);
+            if (info.done) break;
+            const uint32_t row0 = P.row_begin + info.tile * kRowTile;
+            const uint32_t rows_end = min(row0 + kRowTile, P.row_end);
+            const uint32_t i = row0 + rit;
+            const bool valid = i < rows_end;
+            uint32_t si = 0, j0 = 0;
+            int pc = 0;
+            bool bypass = false;
+            uint64_t mine2[W2 > 0 ? W2 : 1];
+#pragma unroll
+            for (int w = 0; w < (W2 > 0 ? W2 : 1); ++w) mine2[w] = 0;
+            if (valid) {
+                si = P.sizes[i];
+                j0 = P.wstart[si];
+                bypass = static_cast<int64_t>(si) > P.cutoff;
+#pragma unroll
+                for (int w = 0; w < KA / 64; ++w) pc += __popcll(P.bits[static_cast<uint64_t>(i) * (KA / 64) + w]);
+                if constexpr (W2 > 0) {
+#pragma unroll
+                    for (int w = 0; w < W2; ++w) mine2[w] = P.bits2[static_cast<uint64_t>(i) * W2 + w];
+                }
+            }
+            int pc2 = 0;
+            if constexpr (K2 > 0) {
+#pragma unroll
+                for (int w = 0; w < W2; ++w) pc2 += __popcll(mine2[w]);
+            }
+            const uint32_t lo_i = valid ? max(j0, info.c0) : info.c1;
+            const uint32_t hi_i = valid ? min(i, info.c1) : info.c1;
+            uint32_t cnt = 0;
+            for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
+                const int st = tseq % NS;
+                const int as = aseq & 1;
+                mbar_wait(&b_full[st], (tseq / NS) & 1);
+                mbar_wait(&acc_full[as], (aseq >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint8_t* stage = sB + st * L::kB;
+                const uint32_t* cz = reinterpret_cast<const uint32_t*>(stage + L::kBop + L::kBsk);
+                const uint64_t* cb2 = reinterpret_cast<const uint64_t*>(stage + L::kBop);
+#pragma unroll 1
+                for (int g = 0; g < 2; ++g) {
+                    const int cl = half * 64 + g * 32;  // column within the tile
+                    const uint32_t gbase = info.c0 + t * kTcN + cl;
+                    const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
+                    const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
+                    const uint32_t rm = low_mask(kh) & ~low_mask(kl);
+                    if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
+                    uint32_t d[32];
+                    tmem_ld32(tmem_base + ((quarter * 32) << 16) + as * kTcN + cl, d);
+                    const bool uni = cz[cl] == cz[cl + 31];
+                    uint32_t m = survivors_tile(d, uni, pc, P.maxham, si, cz + cl, P.neg1);
+                    m = bypass ? rm : (m & rm);
+                    cnt += __popc(m);
+                    uint32_t e = m;
+                    if constexpr (K2 > 0) {
+                        if (__any_sync(0xFFFFFFFFu, m != 0)) {
+                            uint32_t d2[32];
+                            tmem_ld32(tmem_base + ((quarter * 32) << 16) + 256 + as * kTcN + cl, d2);
+                            e = m & survivors_tile(d2, uni, pc2, P.maxham, si, cz + cl, P.neg1);
+                        }
+                    } else if constexpr (W2 > 0) {
+                        uint32_t mm = m;
+                        e = 0;
+                        while (mm) {
+                            const int k = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const uint64_t* col = cb2 + (cl + k) * W2;
+                            int h = 0;
+#pragma unroll
+                            for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
+                            e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
+                        }
+                    }
+                    if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&acc_empty[as]);
+                    mbar_arrive(&b_empty[st]);
+                }
+            }
+            if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
+            if (P.item_counts && cnt) atomicAdd(P.item_counts + info.item * kRowTile + rit, cnt);
+            ++iseq;
+        }
+        if (qlen) tc_flush(q, qlen, P, lane);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
+// Expanded GEMM operands in the core-matrix layout (see the header comment).
+// One thread per (row, 16-byte K chunk).
+struct ExpandParams {
+    const uint64_t* bits;  // n_pad x W sketches
+    uint8_t* opA;
+    uint8_t* opB;
+    uint32_t rows;         // n_pad (multiple of 8)
+    int words;             // W
+    int K;                 // bytes per row = 64 W + 32
+};
+
+__global__ void expand_operands(ExpandParams P) {
+    const int KC = P.K / 16;
+    const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<uint64_t>(P.rows) * KC) return;
+    const uint32_t r = static_cast<uint32_t>(idx / KC);
+    const int c = static_cast<int>(idx % KC);
+    uint32_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
+    const int bitsn = 64 * P.words;
+    if (16 * c < bitsn) {
+        const uint64_t w = P.bits[static_cast<uint64_t>(r) * P.words + (16 * c) / 64];
+        const uint32_t bits16 = static_cast<uint32_t>(w >> ((16 * c) % 64)) & 0xFFFFu;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t bit = (bits16 >> k) & 1u;
+            a[k >> 2] |= bit << (8 * (k & 3));
+            b[k >> 2] |= (bit * 2u) << (8 * (k & 3));
+        }
+    } else if (16 * c == bitsn) {
+        int pcnt = 0;
+        for (int w = 0; w < P.words; ++w) pcnt += __popcll(P.bits[static_cast<uint64_t>(r) * P.words + w]);
+        const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
+        a[0] = 0x0101u;
+        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) | (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
+    }
+    const uint64_t off = ((static_cast<uint64_t>(r / 8) * KC + c) * 8 + (r % 8)) * 16;
+    *reinterpret_cast<uint4*>(P.opA + off) = make_uint4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<uint4*>(P.opB + off) = make_uint4(b[0], b[1], b[2], b[3]);
+}
+
+}  // namespace dev
+}  // namespace ssjb

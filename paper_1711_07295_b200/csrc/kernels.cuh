@@ -172,7 +172,7 @@ struct FilterParams {
     const uint32_t* tile_col_lo; // first (32-aligned) column of each tile's span
     uint2* surv;                 // survivors (j, i)
     uint32_t* rowcnt;            // survivors per row (row - row_begin)
-    uint16_t* item_counts;       // survivors per (item, row-in-tile) for the rescan, or null
+    uint32_t* item_counts;       // survivors per (item, row-in-tile) for the rescan, or null
     Control* ctl;
     unsigned long long surv_cap;
     unsigned long long item_begin, item_end;
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
             __syncthreads();  // stage buffer free for the TMA issued next iteration
         }
         if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
-        if (P.item_counts) P.item_counts[item * kRowTile + tid] = static_cast<uint16_t>(cnt);
+        if (P.item_counts) P.item_counts[item * kRowTile + tid] = cnt;
         __syncthreads();  // s_item / s_tile / stage buffers are rewritten next item
     }
     if (qlen) warp_flush(q, qlen, P, lane);
@@ -484,7 +484,7 @@ struct RescanParams {
     const int32_t* maxham;
     const uint32_t* wstart;
     const uint32_t* rowcnt;
-    const uint16_t* item_counts;  // per (item, row-in-tile) survivors, or null
+    const uint32_t* item_counts;  // per (item, row-in-tile) survivors, or null
     const uint64_t* item_base;    // per tile
     const uint32_t* tile_col_lo;
     uint32_t* jstar;              // capacity-th survivor column per row (row - row_begin)

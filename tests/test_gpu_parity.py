@@ -54,10 +54,22 @@ def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
         assert sha(store) == e["sha256"], e
 
 
-def test_every_golden_join(lib, golden, colls):
+FILTERS = ["tc", "popc", "tc-l2gemm"]
+
+
+def set_filter(monkeypatch, flavour):
+    monkeypatch.setenv("SSJB_FILTER", "popc" if flavour == "popc" else "tc")
+    monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour == "tc-l2gemm" else "0")
+
+
+@pytest.mark.parametrize("flavour", FILTERS)
+def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
+    """Every reference fixture, through each filter kernel (tcgen05 GEMM, POPC,
+    tcgen05 with the level-2 GEMM)."""
+    set_filter(monkeypatch, flavour)
     for e in golden["joins"]:
         rep = S.join(colls(e["collection"]), options_of(lib, e))
-        assert_same(rep, e)
+        assert_same(rep, e, flavour)
 
 
 def test_row_shards_add_up(lib, golden, colls):
@@ -76,7 +88,9 @@ def test_row_shards_add_up(lib, golden, colls):
             assert sum(r.saturated_records for r in reps) == e["saturated_records"]
 
 
-def test_random_collections_vs_oracle(lib, oracle):
+@pytest.mark.parametrize("flavour", FILTERS)
+def test_random_collections_vs_oracle(lib, oracle, flavour, monkeypatch):
+    set_filter(monkeypatch, flavour)
     rng = np.random.default_rng(2024)
     for trial in range(40):
         n = int(rng.integers(50, 1500))
