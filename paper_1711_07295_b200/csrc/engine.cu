@@ -250,25 +250,26 @@ struct TcKernel {
     int smem;
 };
 
-template <int KA, int K2, int W2, int NS>
+template <int KA, int K2, int W2, int NS, int NT>
 TcKernel tc_kernel() {
-    return TcKernel{dev::filter_tc_kernel<KA, K2, W2, NS>, dev::TcLayout<KA, K2, W2, NS>::kBytes};
+    return TcKernel{dev::filter_tc_kernel<KA, K2, W2, NS, NT>, dev::TcLayout<KA, K2, W2, NS, NT>::kBytes};
 }
 
 // Tensor-core filter instantiations: level-1 width b = 64*words (K = b + 32),
-// level 2 as a second GEMM on 256-bit Xor sketches (l2gemm) or a POPC check.
+// level 2 as a second GEMM on 256-bit Xor sketches (l2gemm, 128-column
+// tiles) or a POPC check of level-1 survivors (256-column tiles).
 TcKernel tc_select(int words, bool l2gemm) {
     if (l2gemm) {
         switch (words) {
-            case 1: return tc_kernel<96, 288, 4, 2>();
-            case 2: return tc_kernel<160, 288, 4, 2>();
+            case 1: return tc_kernel<96, 288, 4, 2, 128>();
+            case 2: return tc_kernel<160, 288, 4, 2, 128>();
         }
     } else {
         switch (words) {
-            case 1: return tc_kernel<96, 0, 4, 4>();
-            case 2: return tc_kernel<160, 0, 4, 4>();
-            case 3: return tc_kernel<224, 0, 8, 4>();
-            case 4: return tc_kernel<288, 0, 8, 3>();
+            case 1: return tc_kernel<96, 0, 4, 4, 256>();
+            case 2: return tc_kernel<160, 0, 4, 3, 256>();
+            case 3: return tc_kernel<224, 0, 8, 2, 256>();
+            case 4: return tc_kernel<288, 0, 8, 3, 128>();
         }
     }
     throw DeviceError("no tensor-core filter instantiation for this width");

@@ -30,10 +30,9 @@
 namespace ssjb {
 namespace dev {
 
-constexpr int kTcN = 128;          // columns per MMA tile
-constexpr int kTcEpiWarps = 8;
+constexpr int kTcEpiWarps = 16;   // 4 per TMEM lane quarter
 constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-constexpr int kTcQueue = 256;      // survivor staging per epilogue warp
+constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
 
 struct TcParams {
     const uint8_t* opA;        // expanded level-1 rows, core layout, n_pad x KA
@@ -77,14 +76,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo) {
     return d;
 }
 
-// kind::i8, D s32, A u8, B s8, K-major both, M = 128, N = kTcN
-constexpr uint32_t kTcIdesc = (2u << 4) | (0u << 7) | (1u << 10) | ((kTcN >> 3) << 17) | ((128u >> 4) << 24);
-
+// kind::i8, D s32, A u8, B s8, K-major both, M = 128, N = NT
+template <int NT>
 __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+    constexpr uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((NT >> 3) << 17) | ((128u >> 4) << 24);
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-        "l"(da), "l"(db), "r"(kTcIdesc), "r"(acc));
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -126,14 +125,14 @@ __device__ __forceinline__ uint32_t survivors32(const uint32_t (&d)[32], int cim
     return __brev((m0 << 24) | (m1 << 16) | (m2 << 8) | m3);
 }
 
-__device__ __forceinline__ uint32_t survivors_tile(const uint32_t (&d)[32], bool uniform, int base,
-                                                   const int32_t* maxham, uint32_t si, const uint32_t* cz, int neg1) {
-    int dummy[32];
-    if (uniform) return survivors32<true>(d, base - __ldg(maxham + si + cz[0]) - 1, dummy, neg1);
-    int cims[32];
+// Non-uniform group (column sizes change inside it): per-column threshold.
+__device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int base, const int32_t* maxham,
+                                                    uint32_t si, const uint32_t* cz) {
+    uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cims[k] = base - __ldg(maxham + si + cz[k]) - 1;
-    return survivors32<false>(d, 0, cims, neg1);
+    for (int k = 0; k < 32; ++k)
+        m |= ((base - __ldg(maxham + si + cz[k]) - 1 - static_cast<int>(d[k])) < 0 ? 1u : 0u) << k;
+    return m;
 }
 
 __device__ __forceinline__ void tc_flush(uint2* q, int& qlen, const TcParams& P, int lane) {
@@ -186,22 +185,26 @@ struct TcItem {
 };
 
 // KA: level-1 operand bytes per row; K2: level-2 GEMM operand bytes (0: none);
-// W2: level-2 Xor sketch words for the POPC check (used when K2 == 0); NS: B stages.
-template <int KA, int K2, int W2, int NS>
+// W2: level-2 Xor sketch words for the POPC check (used when K2 == 0);
+// NS: B stages; NT: columns per MMA tile (accumulator slots of NT columns).
+template <int KA, int K2, int W2, int NS, int NT>
 struct TcLayout {
     static constexpr int kA = 128 * (KA + K2);                 // one A slot
-    static constexpr int kBop = kTcN * (KA + K2);              // B operands per stage
-    static constexpr int kBsk = K2 ? 0 : kTcN * W2 * 8;        // staged level-2 sketches
-    static constexpr int kBsz = kTcN * 4;                      // sizes
+    static constexpr int kBop = NT * (KA + K2);                // B operands per stage
+    static constexpr int kBsk = K2 ? 0 : NT * W2 * 8;          // staged level-2 sketches
+    static constexpr int kBsz = NT * 4;                        // sizes
     static constexpr int kB = kBop + kBsk + kBsz;
     static constexpr int kAslots = K2 ? 1 : 2;
     static constexpr int kQueue = kTcEpiWarps * kTcQueue * 8;
     static constexpr int kBytes = kAslots * kA + NS * kB + kQueue;
+    static constexpr int kColsPerWarp = NT / 4;                // 4 epilogue warps per lane quarter
+    static constexpr uint32_t kTmemCols = K2 ? 4 * NT : 2 * NT;
+    static_assert(kTmemCols <= 512, "TMEM");
 };
 
-template <int KA, int K2, int W2, int NS>
+template <int KA, int K2, int W2, int NS, int NT>
 __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
-    using L = TcLayout<KA, K2, W2, NS>;
+    using L = TcLayout<KA, K2, W2, NS, NT>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;                                   // [2][kA]
     uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kTmemCols = K2 ? 512 : 256;  // 2 slots x (L1 [+ L2]) x 128 columns
+    constexpr uint32_t kTmemCols = L::kTmemCols < 32 ? 32 : L::kTmemCols;  // 2 slots x (L1 [+ L2]) x NT
 
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                 info.tile = tile;
                 info.c0 = P.tile_col_lo[tile] + chunk * kColChunk;
                 info.c1 = min(info.c0 + kColChunk, rows_end - 1);
-                info.ntiles = (info.c1 - info.c0 + kTcN - 1) / kTcN;
+                info.ntiles = (info.c1 - info.c0 + NT - 1) / NT;
                 info.done = 0;
                 items[slot] = info;
                 // row operand (A): 128 rows, contiguous in the core layout
@@ -282,12 +285,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
                     mbar_wait(&b_empty[st], ((tseq / NS) & 1) ^ 1);
-                    const uint32_t col = info.c0 + t * kTcN;
+                    const uint32_t col = info.c0 + t * NT;
                     uint8_t* dst = sB + st * L::kB;
                     mbar_expect_tx(&b_full[st], L::kB);
-                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * KA, kTcN * KA, &b_full[st]);
+                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * KA, NT * KA, &b_full[st]);
                     if constexpr (K2 > 0)
-                        tma_load_1d(dst + kTcN * KA, P.opB2 + static_cast<uint64_t>(col) * K2, kTcN * K2, &b_full[st]);
+                        tma_load_1d(dst + NT * KA, P.opB2 + static_cast<uint64_t>(col) * K2, NT * K2, &b_full[st]);
                     if constexpr (K2 == 0 && W2 > 0)
                         tma_load_1d(dst + L::kBop, P.bits2 + static_cast<uint64_t>(col) * W2, L::kBsk, &b_full[st]);
                     tma_load_1d(dst + L::kBop + L::kBsk, P.sizes + col, L::kBsz, &b_full[st]);
@@ -315,17 +318,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                     mbar_wait(&acc_empty[as], ((aseq >> 1) & 1) ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
-                    const uint32_t d1 = tmem_base + as * kTcN;
+                    const uint32_t d1 = tmem_base + as * NT;
 #pragma unroll
                     for (int s = 0; s < KA / 32; ++s)
-                        umma_i8(d1, umma_desc(a0 + s * 256, (KA / 16) * 128), umma_desc(b0 + s * 256, (KA / 16) * 128),
-                                s > 0);
+                        umma_i8<NT>(d1, umma_desc(a0 + s * 256, (KA / 16) * 128),
+                                    umma_desc(b0 + s * 256, (KA / 16) * 128), s > 0);
                     if constexpr (K2 > 0) {
-                        const uint32_t d2 = tmem_base + 256 + as * kTcN;
+                        const uint32_t d2 = tmem_base + 2 * NT + as * NT;
 #pragma unroll
                         for (int s = 0; s < K2 / 32; ++s)
-                            umma_i8(d2, umma_desc(a0 + 128 * KA + s * 256, (K2 / 16) * 128),
-                                    umma_desc(b0 + kTcN * KA + s * 256, (K2 / 16) * 128), s > 0);
+                            umma_i8<NT>(d2, umma_desc(a0 + 128 * KA + s * 256, (K2 / 16) * 128),
+                                        umma_desc(b0 + NT * KA + s * 256, (K2 / 16) * 128), s > 0);
                     }
                     umma_commit(&b_empty[st]);
                     umma_commit(&acc_full[as]);
@@ -337,9 +340,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
     } else {
         // ------------------------------------------------------------ epilogue
         const int ew = warp - 2;
-        const int quarter = warp & 3;          // TMEM lanes 32*quarter .. +31
-        const int half = ew >> 2;              // columns 64*half .. +63 of each tile
+        const int quarter = warp & 3;          // TMEM lanes 32*quarter .. +31 (hardware rule)
+        const int part = ew >> 2;              // this warp's column range of each tile
         const int rit = quarter * 32 + lane;   // row in tile
+        const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         uint2* q = sQ + ew * kTcQueue;
         int qlen = 0;
         uint32_t iseq = 0, tseq = 0, aseq = 0;
@@ -378,7 +382,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
             }
             const uint32_t lo_i = valid ? max(j0, info.c0) : info.c1;
             const uint32_t hi_i = valid ? min(i, info.c1) : info.c1;
+            // warp-uniform interior: groups inside every lane's window need no mask
+            uint32_t lo_max = lo_i, hi_min = hi_i;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo_max = max(lo_max, __shfl_xor_sync(0xFFFFFFFFu, lo_max, o));
+                hi_min = min(hi_min, __shfl_xor_sync(0xFFFFFFFFu, hi_min, o));
+            }
             uint32_t cnt = 0;
+            uint32_t last_sz = 0xFFFFFFFFu;  // cim1 cache: sizes are sorted, so it rarely changes
+            int cim1 = 0, cim1_2 = 0;
             for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
                 const int st = tseq % NS;
                 const int as = aseq & 1;
@@ -389,37 +402,56 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                 const uint32_t* cz = reinterpret_cast<const uint32_t*>(stage + L::kBop + L::kBsk);
                 const uint64_t* cb2 = reinterpret_cast<const uint64_t*>(stage + L::kBop);
 #pragma unroll 1
-                for (int g = 0; g < 2; ++g) {
-                    const int cl = half * 64 + g * 32;  // column within the tile
-                    const uint32_t gbase = info.c0 + t * kTcN + cl;
-                    const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
-                    const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
-                    const uint32_t rm = low_mask(kh) & ~low_mask(kl);
-                    if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
+                for (int g = 0; g < L::kColsPerWarp / 32; ++g) {
+                    const int cl = part * L::kColsPerWarp + g * 32;  // column within the tile
+                    const uint32_t gbase = info.c0 + t * NT + cl;
+                    uint32_t rm = 0xFFFFFFFFu;
+                    if (!(gbase >= lo_max && gbase + 32 <= hi_min)) {
+                        const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
+                        const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
+                        rm = low_mask(kh) & ~low_mask(kl);
+                        if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
+                    }
                     uint32_t d[32];
-                    tmem_ld32(tmem_base + ((quarter * 32) << 16) + as * kTcN + cl, d);
-                    const bool uni = cz[cl] == cz[cl + 31];
-                    uint32_t m = survivors_tile(d, uni, pc, P.maxham, si, cz + cl, P.neg1);
+                    tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
+                    const uint32_t sz0 = cz[cl], sz1 = cz[cl + 31];
+                    const bool uni = sz0 == sz1;
+                    uint32_t m;
+                    if (uni) {
+                        if (sz0 != last_sz) {
+                            last_sz = sz0;
+                            const int T = __ldg(P.maxham + si + sz0);
+                            cim1 = pc - T - 1;
+                            cim1_2 = pc2 - T - 1;
+                        }
+                        int dummy[32];
+                        m = survivors32<true>(d, cim1, dummy, P.neg1);
+                    } else {
+                        m = survivors_mixed(d, pc, P.maxham, si, cz + cl);
+                    }
                     m = bypass ? rm : (m & rm);
                     cnt += __popc(m);
                     uint32_t e = m;
                     if constexpr (K2 > 0) {
                         if (__any_sync(0xFFFFFFFFu, m != 0)) {
-                            uint32_t d2[32];
-                            tmem_ld32(tmem_base + ((quarter * 32) << 16) + 256 + as * kTcN + cl, d2);
-                            e = m & survivors_tile(d2, uni, pc2, P.maxham, si, cz + cl, P.neg1);
+                            tmem_ld32(tmem_base + lane_base + 2 * NT + as * NT + cl, d);
+                            int dummy[32];
+                            e = m & (uni ? survivors32<true>(d, cim1_2, dummy, P.neg1)
+                                         : survivors_mixed(d, pc2, P.maxham, si, cz + cl));
                         }
                     } else if constexpr (W2 > 0) {
-                        uint32_t mm = m;
-                        e = 0;
-                        while (mm) {
-                            const int k = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            const uint64_t* col = cb2 + (cl + k) * W2;
-                            int h = 0;
+                        if (__any_sync(0xFFFFFFFFu, m != 0)) {
+                            uint32_t mm = m;
+                            e = 0;
+                            while (mm) {
+                                const int k = __ffs(mm) - 1;
+                                mm &= mm - 1;
+                                const uint64_t* col = cb2 + (cl + k) * W2;
+                                int h = 0;
 #pragma unroll
-                            for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
-                            e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
+                                for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
+                                e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
+                            }
                         }
                     }
                     if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
