@@ -109,6 +109,31 @@ void register_host(const Collection& c) {
 
 }  // namespace
 
+// Sketch stores and expanded GEMM operands derived from a collection for one
+// (method, width, hash).  Pinned replicas keep the last set, so a threshold
+// sweep over a resident collection builds them once.
+struct SketchSet {
+    int device = -1;
+    int method = -1, width = 0, hash = 0, words2 = 0;
+    uint64_t* bits = nullptr;
+    uint64_t* bits2 = nullptr;
+    uint8_t *opA = nullptr, *opB = nullptr, *opA2 = nullptr, *opB2 = nullptr;
+    bool owned = false;  // cudaMalloc'd (persistent) rather than arena memory
+    ~SketchSet() {
+        if (!owned) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaFree(bits);
+        cudaFree(bits2);
+        cudaFree(opA);
+        cudaFree(opB);
+        cudaFree(opA2);
+        cudaFree(opB2);
+        cudaSetDevice(cur);
+    }
+};
+
 // Device copy of a canonical collection: tokens, offsets and sizes (padded).
 struct DeviceReplica {
     int device = -1;
@@ -118,6 +143,7 @@ struct DeviceReplica {
     size_t n = 0;
     uint64_t bytes = 0;
     cudaStream_t stream = nullptr;  // set for per-join replicas: stream-ordered alloc/free
+    std::shared_ptr<SketchSet> sketches;  // resident replicas only
     ~DeviceReplica() {
         if (device < 0) return;
         if (stream) {
@@ -261,13 +287,13 @@ TcKernel tc_kernel() {
 TcKernel tc_select(int words, bool l2gemm) {
     if (l2gemm) {
         switch (words) {
-            case 1: return tc_kernel<96, 288, 4, 2, 128>();
+            case 1: return tc_kernel<96, 288, 4, 3, 128>();
             case 2: return tc_kernel<160, 288, 4, 2, 128>();
         }
     } else {
         switch (words) {
             case 1: return tc_kernel<96, 0, 4, 4, 256>();
-            case 2: return tc_kernel<160, 0, 4, 3, 256>();
+            case 2: return tc_kernel<160, 0, 4, 4, 256>();
             case 3: return tc_kernel<224, 0, 8, 2, 256>();
             case 4: return tc_kernel<288, 0, 8, 3, 128>();
         }
@@ -312,6 +338,7 @@ void launch_build(const DeviceReplica& rep, uint64_t* bits, Method method, int w
 // Sort keys/vals in place by key bits [0, 32+bits) skipping constant bytes;
 // returns the buffer holding the result (a or b).
 struct SortBufs {
+    const unsigned long long* count;  // device-side element count (small-sort path)
     unsigned long long* ka;
     uint32_t* va;
     unsigned long long* kb;
@@ -320,10 +347,17 @@ struct SortBufs {
     uint32_t* sums;
 };
 
-__global__ void small_sort(unsigned long long* keys, uint32_t* vals, uint32_t n) {
-    // single CTA bitonic sort, n <= 4096
-    __shared__ unsigned long long k[4096];
-    __shared__ uint32_t v[4096];
+constexpr uint32_t kSmallSort = 4096;
+
+// Single-CTA bitonic sort of up to 4096 (key, value) pairs; the count comes
+// from device memory so it runs in the same stream-ordered chain as the
+// verifier (a larger count leaves the data for the radix path).
+__global__ void small_sort(unsigned long long* keys, uint32_t* vals, const unsigned long long* count) {
+    const unsigned long long cnt = *count;
+    if (cnt <= 1 || cnt > kSmallSort) return;
+    const uint32_t n = static_cast<uint32_t>(cnt);
+    __shared__ unsigned long long k[kSmallSort];
+    __shared__ uint32_t v[kSmallSort];
     uint32_t m = 1;
     while (m < n) m <<= 1;
     for (uint32_t t = threadIdx.x; t < m; t += blockDim.x) {
@@ -359,8 +393,8 @@ __global__ void small_sort(unsigned long long* keys, uint32_t* vals, uint32_t n)
 bool sort_results(SortBufs& B, unsigned long long n, int idbits, cudaStream_t s, uint64_t& launches) {
     // returns true when the sorted data ended in (kb, vb)
     if (n <= 1) return false;
-    if (n <= 4096) {
-        small_sort<<<1, 1024, 0, s>>>(B.ka, B.va, static_cast<uint32_t>(n));
+    if (n <= kSmallSort) {
+        small_sort<<<1, 1024, 0, s>>>(B.ka, B.va, B.count);
         ++launches;
         CK(cudaGetLastError());
         return false;
@@ -483,12 +517,10 @@ void engine_build_bitmaps(const Collection& c, Method method, int width, int has
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
     using Clock = std::chrono::steady_clock;
     set_device(device);
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{s};
+    // one non-blocking stream per (host thread, device), reused across joins
+    static thread_local cudaStream_t streams[16] = {};
+    if (!streams[device & 15]) CK(cudaStreamCreateWithFlags(&streams[device & 15], cudaStreamNonBlocking));
+    cudaStream_t s = streams[device & 15];
     EngineStats& st = out.stats;
     st.window_pairs = plan.window_pairs;
     const auto t_start = Clock::now();
@@ -524,18 +556,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4 + tl.item_base.size() * 8 + tl.col_lo.size() * 4;
     cudaEvent_t e_up = T.mark();
 
-    // K1: sketches
-    uint64_t* d_bits = A.alloc<uint64_t>((n + kPadRows + 8) * W);
+    // K1: sketches (+ level-2 Xor sketches), reused from a resident replica's cache
     const int W2 = enabled ? level2_words(W) : 0;
-    uint64_t* d_bits2 = W2 ? A.alloc<uint64_t>((n + kPadRows + 8) * W2) : nullptr;
-    if (enabled) {
-        CK(cudaMemsetAsync(d_bits + n * W, 0, (kPadRows + 8) * W * 8, s));
-        launch_build(*rep, d_bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
-        if (W2) {
-            CK(cudaMemsetAsync(d_bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
-            launch_build(*rep, d_bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
-        }
-    }
     // K2 flavour: tcgen05 int8 GEMM filter where it applies, POPC otherwise
     const char* fenv = std::getenv("SSJB_FILTER");
     const bool tc_ok = enabled && W <= 4 && plan.row_begin % 8 == 0;
@@ -554,19 +576,61 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
     }
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
-    uint8_t *d_opA = nullptr, *d_opB = nullptr, *d_opA2 = nullptr, *d_opB2 = nullptr;
-    if (use_tc) {
-        const size_t KA = 64 * W + 32;
-        d_opA = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * KA);
-        d_opB = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * KA);
-        launch_expand(d_bits, W, d_opA, d_opB, n_pad, s, st.launches);
-        if (l2gemm) {
-            const size_t K2 = 64 * W2 + 32;
-            d_opA2 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * K2);
-            d_opB2 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * K2);
-            launch_expand(d_bits2, W2, d_opA2, d_opB2, n_pad, s, st.launches);
-        }
+    const size_t KA = 64 * W + 32, K2b = 64 * W2 + 32;
+    const bool resident = rep->stream == nullptr;
+    std::shared_ptr<SketchSet> sk;
+    if (resident) {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        sk = rep->sketches;
     }
+    const int mcode = enabled ? static_cast<int>(plan.bitmap.method) : -2;
+    const bool hit = sk && sk->method == mcode && sk->width == width && sk->hash == plan.bitmap.hash &&
+                     sk->words2 == W2 && (!use_tc || sk->opA) && (!l2gemm || sk->opA2);
+    if (!hit && enabled) {
+        auto fresh = std::make_shared<SketchSet>();
+        fresh->device = device;
+        fresh->method = mcode;
+        fresh->width = width;
+        fresh->hash = plan.bitmap.hash;
+        fresh->words2 = W2;
+        fresh->owned = resident;
+        auto get = [&](size_t bytes) -> void* {
+            void* p = nullptr;
+            if (resident) CK(cudaMalloc(&p, bytes));
+            else p = A.alloc<uint8_t>(bytes);
+            return p;
+        };
+        fresh->bits = static_cast<uint64_t*>(get((n + kPadRows + 8) * W * 8));
+        CK(cudaMemsetAsync(fresh->bits + n * W, 0, (kPadRows + 8) * W * 8, s));
+        launch_build(*rep, fresh->bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
+        if (W2) {
+            fresh->bits2 = static_cast<uint64_t*>(get((n + kPadRows + 8) * W2 * 8));
+            CK(cudaMemsetAsync(fresh->bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
+            launch_build(*rep, fresh->bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
+        }
+        if (use_tc) {
+            fresh->opA = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+            fresh->opB = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+            launch_expand(fresh->bits, W, fresh->opA, fresh->opB, n_pad, s, st.launches);
+            if (W2 == 4) {  // level-2 GEMM operands (cheap; kept with the set)
+                fresh->opA2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
+                fresh->opB2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
+                launch_expand(fresh->bits2, W2, fresh->opA2, fresh->opB2, n_pad, s, st.launches);
+            }
+        }
+        if (resident) {
+            CK(cudaStreamSynchronize(s));  // publish only finished sketches
+            std::lock_guard<std::mutex> lk(c.dev_mu);
+            rep->sketches = fresh;
+        }
+        sk = fresh;
+    }
+    uint64_t* d_bits = enabled ? sk->bits : A.alloc<uint64_t>((n + kPadRows + 8) * W);
+    uint64_t* d_bits2 = enabled && W2 ? sk->bits2 : nullptr;
+    uint8_t* d_opA = use_tc ? sk->opA : nullptr;
+    uint8_t* d_opB = use_tc ? sk->opB : nullptr;
+    uint8_t* d_opA2 = l2gemm ? sk->opA2 : nullptr;
+    uint8_t* d_opB2 = l2gemm ? sk->opB2 : nullptr;
     cudaEvent_t e_build = T.mark();
 
     // buffers
@@ -650,6 +714,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.row_end = static_cast<uint32_t>(plan.row_end);
         TP.cutoff = FP.cutoff;
         TP.neg1 = -1;
+        TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
         st.filter_kernel = l2gemm ? 2 : 1;
     }
 
@@ -667,6 +732,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint64_t res_count = 0;
     int idbits = 1;
     while ((uint64_t(1) << idbits) < n + 1) ++idbits;
+    SB.count = &d_ctl->results;
+
+    auto take_run = [&](const unsigned long long* keys, const uint32_t* ov, uint64_t count) {
+        std::vector<PairOut> run(count);
+        for (uint64_t k = 0; k < count; ++k)
+            run[k] = PairOut{static_cast<uint32_t>(keys[k] >> 32), static_cast<uint32_t>(keys[k] & 0xFFFFFFFFu),
+                             static_cast<int64_t>(ov[k])};
+        runs.push_back(std::move(run));
+    };
 
     auto flush_results = [&](uint64_t count) {
         // K4 on the current result buffer, then download one sorted run
@@ -684,36 +758,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         st.d2h_bytes += count * 12;
         st.ms_sort += Timer::ms(a, b);
         st.ms_download += Timer::ms(b, d);
-        std::vector<PairOut> run(count);
-        for (uint64_t k = 0; k < count; ++k)
-            run[k] = PairOut{static_cast<uint32_t>(keys[k] >> 32), static_cast<uint32_t>(keys[k] & 0xFFFFFFFFu),
-                             static_cast<int64_t>(ov[k])};
-        runs.push_back(std::move(run));
+        take_run(keys.data(), ov.data(), count);
         CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
     };
 
-    // batches of work items sized so the survivors fit the buffer
     const uint64_t total_items = tl.item_base.back();
-    uint64_t ib = 0;
-    uint64_t batch = total_items;
-    double ms_filter = 0, ms_verify = 0;
-    while (ib < total_items) {
-        const uint64_t ie = std::min(total_items, ib + std::max<uint64_t>(batch, 1));
-        // rows touched by this batch (for rollback on overflow)
-        const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
-                                                  tl.item_base.begin() - 1);
-        const uint32_t te = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ie - 1) -
-                                                  tl.item_base.begin() - 1);
-        const uint32_t rb = tb * dev::kRowTile, re = std::min<uint32_t>(rows, (te + 1) * dev::kRowTile);
-        const bool whole = ib == 0 && ie == total_items;
-        if (!whole) CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+    auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb) {
         CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
         CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
+        if (d_item_counts && ie > ib)
+            CK(cudaMemsetAsync(d_item_counts + ib * dev::kRowTile, 0, (ie - ib) * dev::kRowTile * 4, s));
+        if (ie <= ib) return;
         FP.item_begin = ib;
         FP.item_end = ie;
         FP.tile_begin = tb;
-        if (d_item_counts) CK(cudaMemsetAsync(d_item_counts + ib * dev::kRowTile, 0, (ie - ib) * dev::kRowTile * 4, s));
-        cudaEvent_t a = T.mark();
         if (use_tc) {
             TP.item_begin = ib;
             TP.item_end = ie;
@@ -726,74 +784,39 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
         ++st.launches;
         CK(cudaGetLastError());
-        cudaEvent_t b = T.mark();
-        CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        ms_filter += Timer::ms(a, b);
-        const uint64_t S = h_ctl.survivors;
-        if (S > surv_cap) {
-            // overflow: roll the row counts back and retry a smaller batch
-            if (whole) {
-                CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4ull, s));
-            } else {
-                CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
-            }
-            batch = std::max<uint64_t>(1, (ie - ib) * surv_cap / S * 7 / 10);
-            if (batch >= ie - ib) batch = (ie - ib) / 2;
-            continue;
-        }
-        ++st.batches;
-        st.survivors += S;
-        if (S) {
-            if (res_count + S > res_cap) {
-                flush_results(res_count);
-                res_count = 0;
-            }
-            VP.count = S;
-            const unsigned vgrid = static_cast<unsigned>(std::min<uint64_t>((S + 255) / 256, uint64_t(sms) * 16));
-            cudaEvent_t c0 = T.mark();
-            dev::verify_pairs<<<vgrid, 256, 0, s>>>(VP);
-            ++st.launches;
-            CK(cudaGetLastError());
-            cudaEvent_t c1 = T.mark();
-            CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            ms_verify += Timer::ms(c0, c1);
-            res_count = h_ctl.results;
-        }
-        // grow the next batch towards the capacity at the observed survivor rate
-        const uint64_t done_items = ie - ib;
-        ib = ie;
-        batch = S ? std::max<uint64_t>(1, static_cast<uint64_t>(double(done_items) * 0.7 * double(surv_cap) / double(S)))
-                  : total_items;
-    }
-
-    // K2b + counters
-    cudaEvent_t r0 = T.mark();
-    if (!naive && rows) {
-        dev::RescanParams RP{};
-        RP.bits = d_bits;
-        RP.sizes = rep->sizes;
-        RP.maxham = d_maxham;
-        RP.wstart = d_wstart;
-        RP.rowcnt = d_rowcnt;
-        RP.item_counts = d_item_counts;
-        RP.item_base = d_item_base;
-        RP.tile_col_lo = d_col_lo;
-        RP.jstar = d_jstar;
-        RP.row_begin = static_cast<uint32_t>(plan.row_begin);
-        RP.row_end = static_cast<uint32_t>(plan.row_end);
-        RP.capacity = plan.capacity;
-        RP.cutoff = FP.cutoff;
-        RP.words = W;
-        RP.bypass_all = FP.bypass_all;
-        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, uint64_t(sms) * 8));
-        dev::rescan_saturated<<<g, 256, 0, s>>>(RP);
+    };
+    auto launch_verify = [&]() {
+        // survivor count read on the device: no host round trip between K2 and K3
+        VP.count_ptr = &d_ctl->survivors;
+        VP.count_cap = surv_cap;
+        dev::verify_pairs<<<static_cast<unsigned>(sms) * 8, 256, 0, s>>>(VP);
         ++st.launches;
         CK(cudaGetLastError());
-    }
-    cudaEvent_t r1 = T.mark();
-    if (rows) {
+    };
+    auto launch_counters = [&]() {
+        if (!rows) return;
+        if (!naive) {
+            dev::RescanParams RP{};
+            RP.bits = d_bits;
+            RP.sizes = rep->sizes;
+            RP.maxham = d_maxham;
+            RP.wstart = d_wstart;
+            RP.rowcnt = d_rowcnt;
+            RP.item_counts = d_item_counts;
+            RP.item_base = d_item_base;
+            RP.tile_col_lo = d_col_lo;
+            RP.jstar = d_jstar;
+            RP.row_begin = static_cast<uint32_t>(plan.row_begin);
+            RP.row_end = static_cast<uint32_t>(plan.row_end);
+            RP.capacity = plan.capacity;
+            RP.cutoff = FP.cutoff;
+            RP.words = W;
+            RP.bypass_all = FP.bypass_all;
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, uint64_t(sms) * 8));
+            dev::rescan_saturated<<<g, 256, 0, s>>>(RP);
+            ++st.launches;
+            CK(cudaGetLastError());
+        }
         dev::CountParams CP{};
         CP.sizes = rep->sizes;
         CP.wstart = d_wstart;
@@ -809,11 +832,109 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         dev::reduce_counters<<<g, 256, 0, s>>>(CP);
         ++st.launches;
         CK(cudaGetLastError());
+    };
+
+    // Fast path: the whole shard as one batch, K2 -> K3 -> K2b -> counters ->
+    // K4 chained on the stream with a single host synchronisation.
+    double ms_filter = 0, ms_verify = 0;
+    bool done = false;
+    {
+        cudaEvent_t a = T.mark();
+        launch_filter(0, total_items, 0);
+        cudaEvent_t b = T.mark();
+        launch_verify();
+        cudaEvent_t c1 = T.mark();
+        launch_counters();
+        cudaEvent_t r1 = T.mark();
+        small_sort<<<1, 1024, 0, s>>>(SB.ka, SB.va, &d_ctl->results);
+        ++st.launches;
+        CK(cudaGetLastError());
+        cudaEvent_t so = T.mark();
+        std::vector<unsigned long long> keys(kSmallSort);
+        std::vector<uint32_t> ov(kSmallSort);
+        CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(keys.data(), SB.ka, kSmallSort * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ov.data(), SB.va, kSmallSort * 4, cudaMemcpyDeviceToHost, s));
+        cudaEvent_t dl = T.mark();
+        CK(cudaStreamSynchronize(s));
+        if (h_ctl.survivors <= surv_cap) {
+            done = true;
+            ms_filter = Timer::ms(a, b);
+            ms_verify = Timer::ms(b, c1);
+            st.ms_rescan = Timer::ms(c1, r1);
+            st.batches = 1;
+            st.survivors = h_ctl.survivors;
+            if (h_ctl.results <= kSmallSort) {
+                st.ms_sort = Timer::ms(r1, so);
+                st.ms_download = Timer::ms(so, dl);
+                st.d2h_bytes += kSmallSort * 12 + sizeof(h_ctl);
+                take_run(keys.data(), ov.data(), h_ctl.results);
+            } else {
+                flush_results(h_ctl.results);
+            }
+        } else {
+            // survivor buffer overflow: discard and redo in batches
+            CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4ull, s));
+            CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
+        }
     }
-    CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    st.ms_rescan = Timer::ms(r0, r1);
-    flush_results(res_count);
+
+    if (!done) {
+        // batches of work items sized so the survivors fit the buffer
+        uint64_t ib = 0;
+        uint64_t batch = std::max<uint64_t>(1, total_items * surv_cap / std::max<uint64_t>(h_ctl.survivors, 1) * 7 / 10);
+        while (ib < total_items) {
+            const uint64_t ie = std::min(total_items, ib + std::max<uint64_t>(batch, 1));
+            // rows touched by this batch (for rollback on overflow)
+            const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
+                                                      tl.item_base.begin() - 1);
+            const uint32_t te = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ie - 1) -
+                                                      tl.item_base.begin() - 1);
+            const uint32_t rb = tb * dev::kRowTile, re = std::min<uint32_t>(rows, (te + 1) * dev::kRowTile);
+            CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+            cudaEvent_t a = T.mark();
+            launch_filter(ib, ie, tb);
+            cudaEvent_t b = T.mark();
+            CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ms_filter += Timer::ms(a, b);
+            const uint64_t S = h_ctl.survivors;
+            if (S > surv_cap) {
+                // overflow: roll the row counts back and retry a smaller batch
+                CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+                batch = std::max<uint64_t>(1, (ie - ib) * surv_cap / S * 7 / 10);
+                if (batch >= ie - ib) batch = (ie - ib) / 2;
+                continue;
+            }
+            ++st.batches;
+            st.survivors += S;
+            if (S) {
+                if (res_count + S > res_cap) {
+                    flush_results(res_count);
+                    res_count = 0;
+                }
+                cudaEvent_t c0 = T.mark();
+                launch_verify();
+                cudaEvent_t c1 = T.mark();
+                CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                ms_verify += Timer::ms(c0, c1);
+                res_count = h_ctl.results;
+            }
+            // grow the next batch towards the capacity at the observed survivor rate
+            const uint64_t done_items = ie - ib;
+            ib = ie;
+            batch = S ? std::max<uint64_t>(1, static_cast<uint64_t>(double(done_items) * 0.7 * double(surv_cap) / double(S)))
+                      : total_items;
+        }
+        cudaEvent_t r0 = T.mark();
+        launch_counters();
+        cudaEvent_t r1 = T.mark();
+        CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        st.ms_rescan = Timer::ms(r0, r1);
+        flush_results(res_count);
+    }
 
     // merge sorted runs (one run unless the result buffer overflowed)
     if (runs.size() == 1) {

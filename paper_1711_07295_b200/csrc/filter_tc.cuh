@@ -56,6 +56,7 @@ struct TcParams {
     uint32_t row_begin, row_end;
     int64_t cutoff;
     int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
+    int debug;                 // bit 0: skip the epilogue math (pipeline probe)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -191,7 +192,7 @@ template <int KA, int K2, int W2, int NS, int NT>
 struct TcLayout {
     static constexpr int kA = 128 * (KA + K2);                 // one A slot
     static constexpr int kBop = NT * (KA + K2);                // B operands per stage
-    static constexpr int kBsk = K2 ? 0 : NT * W2 * 8;          // staged level-2 sketches
+    static constexpr int kBsk = 0;  // level-2 column sketches are read from L2 for survivors only
     static constexpr int kBsz = NT * 4;                        // sizes
     static constexpr int kB = kBop + kBsk + kBsz;
     static constexpr int kAslots = K2 ? 1 : 2;
@@ -291,8 +292,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                     tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * KA, NT * KA, &b_full[st]);
                     if constexpr (K2 > 0)
                         tma_load_1d(dst + NT * KA, P.opB2 + static_cast<uint64_t>(col) * K2, NT * K2, &b_full[st]);
-                    if constexpr (K2 == 0 && W2 > 0)
-                        tma_load_1d(dst + L::kBop, P.bits2 + static_cast<uint64_t>(col) * W2, L::kBsk, &b_full[st]);
                     tma_load_1d(dst + L::kBop + L::kBsk, P.sizes + col, L::kBsz, &b_full[st]);
                 }
                 ++iseq;
@@ -400,58 +399,70 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint8_t* stage = sB + st * L::kB;
                 const uint32_t* cz = reinterpret_cast<const uint32_t*>(stage + L::kBop + L::kBsk);
-                const uint64_t* cb2 = reinterpret_cast<const uint64_t*>(stage + L::kBop);
+                const int cw = part * L::kColsPerWarp;               // this warp's first column
+                const uint32_t wbase = info.c0 + t * NT + cw;
+                const uint32_t szw0 = cz[cw], szw1 = cz[cw + L::kColsPerWarp - 1];
+                // fast path: every group of this warp's range is inside all 32
+                // windows and of one column size (the bulk of the pair space)
+                const bool fast = szw0 == szw1 && wbase >= lo_max && wbase + L::kColsPerWarp <= hi_min;
+                if (fast && szw0 != last_sz) {
+                    last_sz = szw0;
+                    const int T = __ldg(P.maxham + si + szw0);
+                    cim1 = pc - T - 1;
+                    cim1_2 = pc2 - T - 1;
+                }
 #pragma unroll 1
                 for (int g = 0; g < L::kColsPerWarp / 32; ++g) {
-                    const int cl = part * L::kColsPerWarp + g * 32;  // column within the tile
-                    const uint32_t gbase = info.c0 + t * NT + cl;
-                    uint32_t rm = 0xFFFFFFFFu;
-                    if (!(gbase >= lo_max && gbase + 32 <= hi_min)) {
+                    if (P.debug & 1) break;
+                    const int cl = cw + g * 32;  // column within the tile
+                    const uint32_t gbase = wbase + g * 32;
+                    uint32_t d[32];
+                    uint32_t m;
+                    bool uni = true;
+                    int dummy[32];
+                    if (fast) {
+                        tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
+                        m = survivors32<true>(d, cim1, dummy, P.neg1);
+                        if (bypass) m = 0xFFFFFFFFu;
+                    } else {
                         const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
                         const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
-                        rm = low_mask(kh) & ~low_mask(kl);
+                        const uint32_t rm = low_mask(kh) & ~low_mask(kl);
                         if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
-                    }
-                    uint32_t d[32];
-                    tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
-                    const uint32_t sz0 = cz[cl], sz1 = cz[cl + 31];
-                    const bool uni = sz0 == sz1;
-                    uint32_t m;
-                    if (uni) {
-                        if (sz0 != last_sz) {
-                            last_sz = sz0;
-                            const int T = __ldg(P.maxham + si + sz0);
-                            cim1 = pc - T - 1;
-                            cim1_2 = pc2 - T - 1;
+                        tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
+                        const uint32_t sz0 = cz[cl];
+                        uni = sz0 == cz[cl + 31];
+                        if (uni) {
+                            if (sz0 != last_sz) {
+                                last_sz = sz0;
+                                const int T = __ldg(P.maxham + si + sz0);
+                                cim1 = pc - T - 1;
+                                cim1_2 = pc2 - T - 1;
+                            }
+                            m = survivors32<true>(d, cim1, dummy, P.neg1);
+                        } else {
+                            m = survivors_mixed(d, pc, P.maxham, si, cz + cl);
                         }
-                        int dummy[32];
-                        m = survivors32<true>(d, cim1, dummy, P.neg1);
-                    } else {
-                        m = survivors_mixed(d, pc, P.maxham, si, cz + cl);
+                        m = bypass ? rm : (m & rm);
                     }
-                    m = bypass ? rm : (m & rm);
                     cnt += __popc(m);
+                    if (!__any_sync(0xFFFFFFFFu, m != 0)) continue;
                     uint32_t e = m;
                     if constexpr (K2 > 0) {
-                        if (__any_sync(0xFFFFFFFFu, m != 0)) {
-                            tmem_ld32(tmem_base + lane_base + 2 * NT + as * NT + cl, d);
-                            int dummy[32];
-                            e = m & (uni ? survivors32<true>(d, cim1_2, dummy, P.neg1)
-                                         : survivors_mixed(d, pc2, P.maxham, si, cz + cl));
-                        }
+                        tmem_ld32(tmem_base + lane_base + 2 * NT + as * NT + cl, d);
+                        e = m & (uni ? survivors32<true>(d, cim1_2, dummy, P.neg1)
+                                     : survivors_mixed(d, pc2, P.maxham, si, cz + cl));
                     } else if constexpr (W2 > 0) {
-                        if (__any_sync(0xFFFFFFFFu, m != 0)) {
-                            uint32_t mm = m;
-                            e = 0;
-                            while (mm) {
-                                const int k = __ffs(mm) - 1;
-                                mm &= mm - 1;
-                                const uint64_t* col = cb2 + (cl + k) * W2;
-                                int h = 0;
+                        uint32_t mm = m;
+                        e = 0;
+                        while (mm) {
+                            const int k = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const uint64_t* col = P.bits2 + static_cast<uint64_t>(gbase + k) * W2;
+                            int h = 0;
 #pragma unroll
-                                for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ col[w]);
-                                e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
-                            }
+                            for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ __ldg(col + w));
+                            e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
                         }
                     }
                     if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);

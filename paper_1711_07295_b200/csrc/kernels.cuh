@@ -215,10 +215,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep in hardware instead of spinning
         : "memory");
 }
 
@@ -622,7 +622,8 @@ struct VerifyParams {
     const uint64_t* offsets;
     const int32_t* minov;     // minov[|r|+|s|]
     const uint2* surv;
-    unsigned long long count;
+    const unsigned long long* count_ptr;  // survivors emitted by K2 (device memory)
+    unsigned long long count_cap;         // survivor buffer capacity
     unsigned long long* res_keys;  // (j << 32) | i
     uint32_t* res_ov;
     unsigned long long res_cap;
@@ -634,13 +635,14 @@ struct VerifyParams {
 // exact because the exit only fires on pairs that cannot reach minov.
 __global__ void verify_pairs(VerifyParams P) {
     const int lane = threadIdx.x & 31;
+    const unsigned long long count = min(*P.count_ptr, P.count_cap);
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
-    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < P.count;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < count;
          base += stride) {
         const unsigned long long k = base + threadIdx.x;
         bool matched = false;
         uint32_t j = 0, i = 0, ov = 0;
-        if (k < P.count) {
+        if (k < count) {
             const uint2 pr = P.surv[k];
             j = pr.x;
             i = pr.y;
@@ -665,7 +667,7 @@ __global__ void verify_pairs(VerifyParams P) {
         }
         // algorithmic traffic: both token lists plus the 16-byte result record
         unsigned long long vb = 0;
-        if (k < P.count) vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
+        if (k < count) vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
         if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);
