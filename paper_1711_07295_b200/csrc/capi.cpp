@@ -209,7 +209,9 @@ std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssj
             bounds[0] = row_begin;
             for (int g = 1; g < devices; ++g) {
                 const double target = pre.back() * g / devices;
-                bounds[g] = row_begin + (std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+                uint64_t b = row_begin + (std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+                b = row_begin + ((b - row_begin) & ~uint64_t(127));  // 128-row tile boundaries
+                bounds[g] = std::max(b, bounds[g - 1]);
             }
             bounds[devices] = row_end;
         }

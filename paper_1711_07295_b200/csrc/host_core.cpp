@@ -589,6 +589,12 @@ std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, 
         run += static_cast<double>(j0 < i ? i - j0 : 0) + 1.0;
         while (g < parts && run >= per * g) bounds[static_cast<size_t>(g++)] = i + 1;
     }
+    // shard starts on 128-row tile boundaries (the filter's row tile and the
+    // tensor-core operand layout want 8-aligned row blocks)
+    for (int k = 1; k < parts; ++k) {
+        uint64_t b = bounds[static_cast<size_t>(k)] & ~uint64_t(127);
+        bounds[static_cast<size_t>(k)] = std::max(b, bounds[static_cast<size_t>(k - 1)]);
+    }
     return bounds;
 }
 

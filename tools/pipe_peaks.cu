@@ -6,6 +6,7 @@
 //   usage: pipe_peaks [device]   -> one JSON line on stdout
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 
@@ -40,6 +41,95 @@ __global__ void lop3_loop(unsigned* out, unsigned seed) {
 #pragma unroll
     for (int k = 0; k < kChains; ++k) s ^= a[k];
     if (s == 0x12345678u) out[0] = s;
+}
+
+
+// ---- tcgen05 kind::i8 throughput: back-to-back M=128 x N=256 x K=32 MMAs
+// from shared memory into TMEM, one CTA per SM (the filter kernel's shape).
+__device__ __forceinline__ uint64_t pk_desc(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(128 >> 4) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    return d;
+}
+
+constexpr int kTcIters = 2048;  // groups of 8 MMAs
+
+__global__ void __launch_bounds__(128, 1) tc_i8_loop(unsigned* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];  // A 128x32 + B 256x32 bytes (zeros are fine)
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ uint32_t tbase;
+    const int warp = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < (128 + 256) * 32 / 4; k += blockDim.x) reinterpret_cast<uint32_t*>(sm)[k] = 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(&tbase))));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]))));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (threadIdx.x == 0) {
+        const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+        const uint32_t b0 = a0 + 128 * 32;
+        const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+        const uint64_t da = pk_desc(a0, 2 * 128), db = pk_desc(b0, 2 * 128);
+        uint32_t phase[2] = {0, 0};
+        for (int it = 0; it < kTcIters; ++it) {
+            const int b = it & 1;
+            if (it >= 2) {  // keep two groups in flight
+                const uint32_t ba = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
+                asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W;\n}\n"
+                             ::"r"(ba), "r"(phase[b]) : "memory");
+                phase[b] ^= 1;
+            }
+            for (int k = 0; k < 8; ++k)
+                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                             ::"r"(tbase + b * 256), "l"(da), "l"(db), "r"(idesc), "r"(k));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]))) : "memory");
+        }
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t ba = static_cast<uint32_t>(__cvta_generic_to_shared(&bar[b]));
+            asm volatile("{\n.reg .pred P1;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W2;\n}\n"
+                         ::"r"(ba), "r"(phase[b]) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+    if (threadIdx.x == 0 && out == nullptr) out[0] = 1;
+}
+
+double run_tc(int sms) {
+    const int smem = (128 + 256) * 32;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    unsigned* d;
+    cudaMalloc(&d, 64);
+    tc_i8_loop<<<sms, 128, smem>>>(d);
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        tc_i8_loop<<<sms, 128, smem>>>(d);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaFree(d);
+    const double ops = double(sms) * kTcIters * 8 * 128.0 * 256.0 * 32.0 * 2.0;
+    return ops / (best * 1e-3);
 }
 
 template <typename K>
@@ -77,10 +167,14 @@ int main(int argc, char** argv) {
     cudaMalloc(&d, 64);
     const double popc = run(popc_loop, sms, d);
     const double lop3 = run(lop3_loop, sms, d);
+    const double tci8 = run_tc(sms);
+    cudaError_t err = cudaGetLastError();
     const double clk = clk_khz * 1e3;
-    std::printf("{\"popc_ops_per_s\": %.6e, \"lop3_ops_per_s\": %.6e, \"sms\": %d, \"max_clock_hz\": %.6e, "
-                "\"popc_per_clk_per_sm_at_max\": %.3f, \"lop3_per_clk_per_sm_at_max\": %.3f}\n",
-                popc, lop3, sms, clk, popc / (sms * clk), lop3 / (sms * clk));
+    std::printf("{\"popc_ops_per_s\": %.6e, \"lop3_ops_per_s\": %.6e, \"tc_i8_ops_per_s\": %.6e, \"sms\": %d, "
+                "\"max_clock_hz\": %.6e, \"popc_per_clk_per_sm_at_max\": %.3f, \"lop3_per_clk_per_sm_at_max\": %.3f, "
+                "\"tc_i8_ops_per_clk_per_sm_at_max\": %.1f, \"error\": \"%s\"}\n",
+                popc, lop3, tci8, sms, clk, popc / (sms * clk), lop3 / (sms * clk), tci8 / (sms * clk),
+                err == cudaSuccess ? "" : cudaGetErrorString(err));
     cudaFree(d);
     return 0;
 }
