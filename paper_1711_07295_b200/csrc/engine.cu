@@ -95,12 +95,19 @@ struct Timer {  // device-time spans on one stream
     }
 };
 
+bool narrow_tokens(const Collection& c) { return !c.tokens.empty() && c.universe <= 65536; }
+
 void register_host(const Collection& c) {
-    // Page-lock the canonical arrays once so every upload is a pinned DMA.
+    // Page-lock the arrays that are uploaded so every upload is a pinned DMA;
+    // tokens of a universe <= 65536 travel as a 16-bit copy built once here.
     if (c.host_registered) return;
-    if (!c.tokens.empty())
+    if (narrow_tokens(c)) {
+        c.tokens16.assign(c.tokens.begin(), c.tokens.end());
+        cudaHostRegister(c.tokens16.data(), c.tokens16.size() * sizeof(uint16_t), cudaHostRegisterDefault);
+    } else if (!c.tokens.empty()) {
         cudaHostRegister(const_cast<uint32_t*>(c.tokens.data()), c.tokens.size() * sizeof(uint32_t),
                          cudaHostRegisterDefault);
+    }
     cudaHostRegister(const_cast<uint64_t*>(c.offsets.data()), c.offsets.size() * sizeof(uint64_t),
                      cudaHostRegisterDefault);
     cudaGetLastError();  // registration is an optimisation; ignore failures
@@ -172,6 +179,16 @@ __global__ void sizes_from_offsets(const uint64_t* off, uint32_t* sizes, size_t 
     else if (r < n + kPadRows) sizes[r] = n ? static_cast<uint32_t>(off[n] - off[n - 1]) : 0u;
 }
 
+__global__ void widen_tokens(const uint16_t* in, uint32_t* out, size_t n) {
+    size_t k = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) * 4;
+    if (k + 3 < n) {
+        const ushort4 v = *reinterpret_cast<const ushort4*>(in + k);
+        *reinterpret_cast<uint4*>(out + k) = make_uint4(v.x, v.y, v.z, v.w);
+    } else {
+        for (; k < n; ++k) out[k] = in[k];
+    }
+}
+
 std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
                                       uint64_t& launches, bool resident = false) {
     register_host(c);
@@ -190,12 +207,26 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     }
     rep->device = device;
     rep->n = n;
-    if (!c.tokens.empty())
+    uint64_t tok_h2d = 0;
+    if (narrow_tokens(c)) {
+        // 16-bit upload, widened on the device
+        uint16_t* t16 = nullptr;
+        const size_t T = c.tokens.size();
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&t16), T * sizeof(uint16_t), stream));
+        CK(cudaMemcpyAsync(t16, c.tokens16.data(), T * sizeof(uint16_t), cudaMemcpyHostToDevice, stream));
+        widen_tokens<<<static_cast<unsigned>((T + 1023) / 1024), 256, 0, stream>>>(t16, rep->tokens, T);
+        ++launches;
+        CK(cudaGetLastError());
+        CK(cudaFreeAsync(t16, stream));
+        tok_h2d = T * sizeof(uint16_t);
+    } else if (!c.tokens.empty()) {
         CK(cudaMemcpyAsync(rep->tokens, c.tokens.data(), c.tokens.size() * sizeof(uint32_t),
                            cudaMemcpyHostToDevice, stream));
+        tok_h2d = c.tokens.size() * sizeof(uint32_t);
+    }
     CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                        stream));
-    rep->bytes = c.tokens.size() * sizeof(uint32_t) + (n + 1) * sizeof(uint64_t);
+    rep->bytes = tok_h2d + (n + 1) * sizeof(uint64_t);
     h2d += rep->bytes;
     const size_t tot = n + kPadRows;
     sizes_from_offsets<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(rep->offsets, rep->sizes, n);
@@ -489,7 +520,8 @@ void engine_unpin(const Collection& c, int device) {
 
 void engine_release_host(const Collection& c) {
     if (!c.host_registered) return;
-    if (!c.tokens.empty()) cudaHostUnregister(const_cast<uint32_t*>(c.tokens.data()));
+    if (narrow_tokens(c)) cudaHostUnregister(c.tokens16.data());
+    else if (!c.tokens.empty()) cudaHostUnregister(const_cast<uint32_t*>(c.tokens.data()));
     cudaHostUnregister(const_cast<uint64_t*>(c.offsets.data()));
     cudaGetLastError();
     c.host_registered = false;

@@ -265,6 +265,10 @@ void canonicalize(Collection& c, std::vector<uint32_t>&& raw, const std::vector<
         std::memcpy(c.tokens.data() + c.offsets[k], raw.data() + off[r], len[r] * sizeof(uint32_t));
         c.max_size = std::max(c.max_size, len[r]);
     }
+    // size index of the sorted collection (the length filter's window starts)
+    c.first_ge.assign(static_cast<size_t>(c.max_size) + 2, static_cast<uint32_t>(n));
+    for (size_t k = n; k-- > 0;) c.first_ge[c.rec_size(k)] = static_cast<uint32_t>(k);
+    for (size_t s = c.max_size + 1; s-- > 0;) c.first_ge[s] = std::min(c.first_ge[s], c.first_ge[s + 1]);
 }
 
 Collection::~Collection() = default;
@@ -550,20 +554,25 @@ JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size
                              static_cast<__int128>(plan.p) + plan.q);
         plan.minov[S] = static_cast<int32_t>(std::max<int64_t>(1, v));
     }
-    // first index per size, then j0 per size (reference src/parallel_join.cpp:65-70)
-    std::vector<uint32_t> first_ge(static_cast<size_t>(ms) + 2, static_cast<uint32_t>(n));
-    for (size_t r = n; r-- > 0;) first_ge[c.rec_size(r)] = static_cast<uint32_t>(r);
-    for (size_t s = ms + 1; s-- > 0;) first_ge[s] = std::min(first_ge[s], first_ge[s + 1]);
+    // j0 per size from the collection's size index (reference src/parallel_join.cpp:65-70)
+    const std::vector<uint32_t>& first_ge = c.first_ge;
     plan.window_start.resize(static_cast<size_t>(ms) + 1);
     for (size_t s = 0; s <= ms; ++s) {
         int64_t lo = ceil_div(static_cast<__int128>(plan.p) * static_cast<int64_t>(s), plan.q);
         plan.window_start[s] = lo > static_cast<int64_t>(ms) ? static_cast<uint32_t>(n)
                                                              : first_ge[static_cast<size_t>(lo)];
     }
+    // sum over rows of (i - j0(i)), one arithmetic series per size class
     uint64_t w = 0;
-    for (size_t i = plan.row_begin; i < plan.row_end; ++i) {
-        uint32_t j0 = window_start_of(c, plan, i);
-        if (j0 < i) w += i - j0;
+    for (size_t s = 0; s <= ms; ++s) {
+        const uint64_t a = std::max<uint64_t>(first_ge[s], plan.row_begin);
+        const uint64_t b = std::min<uint64_t>(first_ge[s + 1], plan.row_end);
+        if (a >= b) continue;
+        const uint64_t j0 = plan.naive ? 0 : plan.window_start[s];
+        const uint64_t from = std::max(a, j0 + 1);  // rows with a non-empty window
+        if (from >= b) continue;
+        const uint64_t cnt = b - from;
+        w += cnt * (from - j0) + cnt * (cnt - 1) / 2;
     }
     plan.window_pairs = w;
     return plan;

@@ -83,6 +83,7 @@ struct Collection {
     std::vector<uint64_t> offsets{0};
     uint64_t universe = 0;   // token_frequency.size() of the reference
     uint32_t max_size = 0;
+    std::vector<uint32_t> first_ge;  // first record index with size >= s, s in [0, max_size + 1]
 
     size_t size() const { return offsets.size() - 1; }
     uint32_t rec_size(size_t r) const { return static_cast<uint32_t>(offsets[r + 1] - offsets[r]); }
@@ -93,6 +94,8 @@ struct Collection {
     mutable std::mutex dev_mu;
     mutable std::shared_ptr<DeviceReplica> pinned[16];
     mutable bool host_registered = false;
+    // 16-bit copy of the tokens (universe <= 65536), page-locked: halves every upload
+    mutable std::vector<uint16_t> tokens16;
     ~Collection();
 };
 
