@@ -422,8 +422,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                     int dummy[32];
                     if (fast) {
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
-                        m = survivors32<true>(d, cim1, dummy, P.neg1);
-                        if (bypass) m = 0xFFFFFFFFu;
+                        // any survivor in the group <=> max_k D_k > cim1: 16 three-input
+                        // maxima (VIMNMX3) decide most groups without building the mask
+                        int mx = __vimax3_s32(static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]));
+#pragma unroll
+                        for (int k = 3; k < 31; k += 2)
+                            mx = __vimax3_s32(mx, static_cast<int>(d[k]), static_cast<int>(d[k + 1]));
+                        mx = max(mx, static_cast<int>(d[31]));
+                        if (!__any_sync(0xFFFFFFFFu, bypass || mx > cim1)) continue;
+                        m = bypass ? 0xFFFFFFFFu : survivors32<true>(d, cim1, dummy, P.neg1);
                     } else {
                         const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
                         const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
