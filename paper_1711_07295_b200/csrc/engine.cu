@@ -124,19 +124,19 @@ struct SketchSet {
     int method = -1, width = 0, hash = 0, words2 = 0;
     uint64_t* bits = nullptr;
     uint64_t* bits2 = nullptr;
-    uint8_t *opA = nullptr, *opB = nullptr, *opA2 = nullptr, *opB2 = nullptr;
+    uint8_t *opA_i8 = nullptr, *opB_i8 = nullptr;  // level-1 int8 operands
+    uint8_t *opA_f4 = nullptr, *opB_f4 = nullptr;  // level-1 fp4 operands
+    uint8_t *opA2 = nullptr, *opB2 = nullptr;      // level-2 int8 operands
     bool owned = false;  // cudaMalloc'd (persistent) rather than arena memory
     ~SketchSet() {
         if (!owned) return;
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
-        cudaFree(bits);
-        cudaFree(bits2);
-        cudaFree(opA);
-        cudaFree(opB);
-        cudaFree(opA2);
-        cudaFree(opB2);
+        for (void* p : {static_cast<void*>(bits), static_cast<void*>(bits2), static_cast<void*>(opA_i8),
+                        static_cast<void*>(opB_i8), static_cast<void*>(opA_f4), static_cast<void*>(opB_f4),
+                        static_cast<void*>(opA2), static_cast<void*>(opB2)})
+            cudaFree(p);
         cudaSetDevice(cur);
     }
 };
@@ -305,34 +305,46 @@ size_t filter_smem(int words, int words2) {
 struct TcKernel {
     void (*fn)(dev::TcParams);
     int smem;
+    int threads;
 };
 
-template <int KA, int K2, int W2, int NS, int NT>
+template <int KIND, int KA, int K2, int W2, int NS, int NT>
 TcKernel tc_kernel() {
-    return TcKernel{dev::filter_tc_kernel<KA, K2, W2, NS, NT>, dev::TcLayout<KA, K2, W2, NS, NT>::kBytes};
+    using L = dev::TcLayout<KIND, KA, K2, W2, NS, NT>;
+    return TcKernel{dev::filter_tc_kernel<KIND, KA, K2, W2, NS, NT>, L::kBytes, L::kThreads};
 }
 
-// Tensor-core filter instantiations: level-1 width b = 64*words (K = b + 32),
-// level 2 as a second GEMM on 256-bit Xor sketches (l2gemm, 128-column
-// tiles) or a POPC check of level-1 survivors (256-column tiles).
-TcKernel tc_select(int words, bool l2gemm) {
+// Tensor-core filter instantiations: level-1 width b = 64*words.
+//   fp4:  kind::mxf4, K = b + 64 e2m1 elements ((b+64)/2 bytes), 192-column tiles
+//   i8:   kind::i8, K = b + 32 bytes, 256-column tiles; with the level-2
+//         GEMM on 256-bit Xor sketches (l2gemm), 128-column tiles
+TcKernel tc_select(int words, bool l2gemm, bool fp4) {
     if (l2gemm) {
         switch (words) {
-            case 1: return tc_kernel<96, 288, 4, 3, 128>();
-            case 2: return tc_kernel<160, 288, 4, 2, 128>();
+            case 1: return tc_kernel<dev::kKindI8, 96, 288, 4, 3, 128>();
+            case 2: return tc_kernel<dev::kKindI8, 160, 288, 4, 2, 128>();
+        }
+    } else if (fp4) {
+        switch (words) {
+            case 1: return tc_kernel<dev::kKindF4, 64, 0, 4, 6, 192>();
+            case 2: return tc_kernel<dev::kKindF4, 96, 0, 4, 6, 192>();
+            case 3: return tc_kernel<dev::kKindF4, 128, 0, 8, 5, 192>();
+            case 4: return tc_kernel<dev::kKindF4, 160, 0, 8, 5, 192>();
         }
     } else {
         switch (words) {
-            case 1: return tc_kernel<96, 0, 4, 4, 256>();
-            case 2: return tc_kernel<160, 0, 4, 4, 256>();
-            case 3: return tc_kernel<224, 0, 8, 2, 256>();
-            case 4: return tc_kernel<288, 0, 8, 3, 128>();
+            case 1: return tc_kernel<dev::kKindI8, 96, 0, 4, 4, 256>();
+            case 2: return tc_kernel<dev::kKindI8, 160, 0, 4, 4, 256>();
+            case 3: return tc_kernel<dev::kKindI8, 224, 0, 8, 2, 256>();
+            case 4: return tc_kernel<dev::kKindI8, 288, 0, 8, 3, 128>();
         }
     }
     throw DeviceError("no tensor-core filter instantiation for this width");
 }
 
-void launch_expand(const uint64_t* bits, int words, uint8_t* opA, uint8_t* opB, uint32_t rows, cudaStream_t s,
+size_t operand_bytes(int words, bool fp4) { return fp4 ? 32 * words + 32 : 64 * words + 32; }
+
+void launch_expand(const uint64_t* bits, int words, uint8_t* opA, uint8_t* opB, uint32_t rows, bool fp4, cudaStream_t s,
                    uint64_t& launches) {
     dev::ExpandParams E{};
     E.bits = bits;
@@ -340,7 +352,8 @@ void launch_expand(const uint64_t* bits, int words, uint8_t* opA, uint8_t* opB, 
     E.opB = opB;
     E.rows = rows;
     E.words = words;
-    E.K = 64 * words + 32;
+    E.fp4 = fp4 ? 1 : 0;
+    E.K = static_cast<int>(operand_bytes(words, fp4));
     const uint64_t threads = static_cast<uint64_t>(rows) * (E.K / 16);
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
     ++launches;
@@ -607,18 +620,28 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             l2gemm = static_cast<double>(cx) < 1.25 * static_cast<double>(c.median_size());
         }
     }
+    const char* kenv = std::getenv("SSJB_TC_KIND");
+    const bool fp4 = use_tc && !l2gemm && !(kenv && std::string(kenv) == "i8");
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
-    const size_t KA = 64 * W + 32, K2b = 64 * W2 + 32;
+    const size_t KA = operand_bytes(W, fp4), K2b = 64 * W2 + 32;
     const bool resident = rep->stream == nullptr;
     std::shared_ptr<SketchSet> sk;
+    // resident replicas build sketches/operands once, under the collection lock
+    std::unique_lock<std::mutex> cache_lock(c.dev_mu, std::defer_lock);
     if (resident) {
-        std::lock_guard<std::mutex> lk(c.dev_mu);
+        cache_lock.lock();
         sk = rep->sketches;
     }
+    auto get = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (resident) CK(cudaMalloc(&p, bytes));
+        else p = A.alloc<uint8_t>(bytes);
+        return p;
+    };
     const int mcode = enabled ? static_cast<int>(plan.bitmap.method) : -2;
-    const bool hit = sk && sk->method == mcode && sk->width == width && sk->hash == plan.bitmap.hash &&
-                     sk->words2 == W2 && (!use_tc || sk->opA) && (!l2gemm || sk->opA2);
-    if (!hit && enabled) {
+    bool built = false;
+    if (enabled && !(sk && sk->method == mcode && sk->width == width && sk->hash == plan.bitmap.hash &&
+                     sk->words2 == W2)) {
         auto fresh = std::make_shared<SketchSet>();
         fresh->device = device;
         fresh->method = mcode;
@@ -626,12 +649,6 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         fresh->hash = plan.bitmap.hash;
         fresh->words2 = W2;
         fresh->owned = resident;
-        auto get = [&](size_t bytes) -> void* {
-            void* p = nullptr;
-            if (resident) CK(cudaMalloc(&p, bytes));
-            else p = A.alloc<uint8_t>(bytes);
-            return p;
-        };
         fresh->bits = static_cast<uint64_t*>(get((n + kPadRows + 8) * W * 8));
         CK(cudaMemsetAsync(fresh->bits + n * W, 0, (kPadRows + 8) * W * 8, s));
         launch_build(*rep, fresh->bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
@@ -640,27 +657,38 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             CK(cudaMemsetAsync(fresh->bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
             launch_build(*rep, fresh->bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
         }
-        if (use_tc) {
-            fresh->opA = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-            fresh->opB = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-            launch_expand(fresh->bits, W, fresh->opA, fresh->opB, n_pad, s, st.launches);
-            if (W2 == 4) {  // level-2 GEMM operands (cheap; kept with the set)
-                fresh->opA2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
-                fresh->opB2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
-                launch_expand(fresh->bits2, W2, fresh->opA2, fresh->opB2, n_pad, s, st.launches);
-            }
-        }
-        if (resident) {
-            CK(cudaStreamSynchronize(s));  // publish only finished sketches
-            std::lock_guard<std::mutex> lk(c.dev_mu);
-            rep->sketches = fresh;
-        }
         sk = fresh;
+        built = true;
+    }
+    if (use_tc && fp4 && !sk->opA_f4) {
+        sk->opA_f4 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+        sk->opB_f4 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+        launch_expand(sk->bits, W, sk->opA_f4, sk->opB_f4, n_pad, true, s, st.launches);
+        built = true;
+    }
+    if (use_tc && !fp4 && !sk->opA_i8) {
+        sk->opA_i8 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+        sk->opB_i8 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
+        launch_expand(sk->bits, W, sk->opA_i8, sk->opB_i8, n_pad, false, s, st.launches);
+        built = true;
+    }
+    if (l2gemm && !sk->opA2) {
+        sk->opA2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
+        sk->opB2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
+        launch_expand(sk->bits2, W2, sk->opA2, sk->opB2, n_pad, false, s, st.launches);
+        built = true;
+    }
+    if (resident) {
+        if (built) {
+            CK(cudaStreamSynchronize(s));  // publish only finished sketches
+            rep->sketches = sk;
+        }
+        cache_lock.unlock();
     }
     uint64_t* d_bits = enabled ? sk->bits : A.alloc<uint64_t>((n + kPadRows + 8) * W);
     uint64_t* d_bits2 = enabled && W2 ? sk->bits2 : nullptr;
-    uint8_t* d_opA = use_tc ? sk->opA : nullptr;
-    uint8_t* d_opB = use_tc ? sk->opB : nullptr;
+    uint8_t* d_opA = !use_tc ? nullptr : (fp4 ? sk->opA_f4 : sk->opA_i8);
+    uint8_t* d_opB = !use_tc ? nullptr : (fp4 ? sk->opB_f4 : sk->opB_i8);
     uint8_t* d_opA2 = l2gemm ? sk->opA2 : nullptr;
     uint8_t* d_opB2 = l2gemm ? sk->opB2 : nullptr;
     cudaEvent_t e_build = T.mark();
@@ -723,7 +751,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     dev::TcParams TP{};
     TcKernel tck{nullptr, 0};
     if (use_tc) {
-        tck = tc_select(W, l2gemm);
+        tck = tc_select(W, l2gemm, fp4);
         CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
         TP.opA = d_opA;
         TP.opB = d_opB;
@@ -747,7 +775,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.cutoff = FP.cutoff;
         TP.neg1 = -1;
         TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
-        st.filter_kernel = l2gemm ? 2 : 1;
+        st.filter_kernel = l2gemm ? 2 : (fp4 ? 3 : 1);
     }
 
     dev::VerifyParams VP{};
@@ -809,7 +837,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             TP.item_end = ie;
             TP.tile_begin = tb;
             const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms));
-            tck.fn<<<static_cast<unsigned>(grid), dev::kTcThreads, tck.smem, s>>>(TP);
+            tck.fn<<<static_cast<unsigned>(grid), tck.threads, tck.smem, s>>>(TP);
         } else {
             const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms) * per_sm);
             ffn<<<static_cast<unsigned>(grid), dev::kRowTile, fsmem, s>>>(FP);

@@ -30,9 +30,9 @@
 namespace ssjb {
 namespace dev {
 
-constexpr int kTcEpiWarps = 16;   // 4 per TMEM lane quarter
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
 constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
+constexpr int kKindI8 = 0;         // tcgen05 kind::i8, s32 accumulators
+constexpr int kKindF4 = 1;         // tcgen05 kind::mxf4 (packed e2m1, unit block scales), f32 accumulators
 
 struct TcParams {
     const uint8_t* opA;        // expanded level-1 rows, core layout, n_pad x KA
@@ -87,6 +87,25 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t da, uint64_t db,
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// kind::mxf4.block_scale.block32: A/B packed e2m1 (MXF4 format 1), ue8m0 scales
+// (bit 23) read from TMEM -- all 1.0 here -- f32 accumulate, K = 64 per instruction.
+template <int NT>
+__device__ __forceinline__ void umma_f4(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc, uint32_t sfa,
+                                        uint32_t sfb) {
+    constexpr uint32_t idesc = (1u << 7) | (1u << 10) | ((NT >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
+}
+
+__device__ __forceinline__ void tmem_fill32(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(v));
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -110,29 +129,64 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // (8 columns each) keep the ALU pipe fed; the subtraction is an IMAD on the
 // FMA pipe (neg1 == -1 arrives as a kernel parameter so ptxas keeps it there).
 // Result: bit k = column k.
-template <bool kUniform>
+template <bool kUniform, int KIND = kKindI8>
 __device__ __forceinline__ uint32_t survivors32(const uint32_t (&d)[32], int cim1, const int (&cims)[32], int neg1) {
     uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    const float cf = static_cast<float>(cim1);
+    const float nf = static_cast<float>(neg1);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int c0 = kUniform ? cim1 : cims[j], c1 = kUniform ? cim1 : cims[8 + j];
-        const int c2 = kUniform ? cim1 : cims[16 + j], c3 = kUniform ? cim1 : cims[24 + j];
-        m0 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[j]) * neg1 + c0), m0, 1);
-        m1 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[8 + j]) * neg1 + c1), m1, 1);
-        m2 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[16 + j]) * neg1 + c2), m2, 1);
-        m3 = __funnelshift_l(static_cast<uint32_t>(static_cast<int>(d[24 + j]) * neg1 + c3), m3, 1);
+        uint32_t v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int kk = 8 * c + j;
+            if constexpr (KIND == kKindI8) {
+                const int cc = kUniform ? cim1 : cims[kk];
+                v[c] = static_cast<uint32_t>(static_cast<int>(d[kk]) * neg1 + cc);
+            } else {  // exact small integers in f32: FFMA keeps the sign semantics (x - x = +0)
+                const float cc = kUniform ? cf : static_cast<float>(cims[kk]);
+                v[c] = __float_as_uint(__fmaf_rn(__uint_as_float(d[kk]), nf, cc));
+            }
+        }
+        m0 = __funnelshift_l(v[0], m0, 1);
+        m1 = __funnelshift_l(v[1], m1, 1);
+        m2 = __funnelshift_l(v[2], m2, 1);
+        m3 = __funnelshift_l(v[3], m3, 1);
     }
     // m_c bit (7-j) = column 8c+j  ->  bit 31-k = column k  ->  brev
     return __brev((m0 << 24) | (m1 << 16) | (m2 << 8) | m3);
 }
 
+// Accumulator value as an exact integer (s32, or an integral f32).
+template <int KIND>
+__device__ __forceinline__ int acc_int(uint32_t d) {
+    if constexpr (KIND == kKindI8) return static_cast<int>(d);
+    else return static_cast<int>(__uint_as_float(d));
+}
+
+// max_k D_k > cim1 for 32 accumulators, 16 three-input maxima.  For f32
+// accumulators the bit patterns are compared as signed integers: that order
+// is exact among non-negative values and puts every negative value below
+// them, so the test is exact whenever cim1 >= 0 (the caller treats cim1 < 0
+// as "maybe").
+template <int KIND>
+__device__ __forceinline__ bool any_above(const uint32_t (&d)[32], int cim1) {
+    int mx = __vimax3_s32(static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]));
+#pragma unroll
+    for (int k = 3; k < 31; k += 2) mx = __vimax3_s32(mx, static_cast<int>(d[k]), static_cast<int>(d[k + 1]));
+    mx = max(mx, static_cast<int>(d[31]));
+    if constexpr (KIND == kKindI8) return mx > cim1;
+    else return cim1 < 0 || mx > __float_as_int(static_cast<float>(cim1) + 0.5f);
+}
+
 // Non-uniform group (column sizes change inside it): per-column threshold.
+template <int KIND = kKindI8>
 __device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int base, const int32_t* maxham,
                                                     uint32_t si, const uint32_t* cz) {
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k)
-        m |= ((base - __ldg(maxham + si + cz[k]) - 1 - static_cast<int>(d[k])) < 0 ? 1u : 0u) << k;
+        m |= ((base - __ldg(maxham + si + cz[k]) - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
     return m;
 }
 
@@ -185,27 +239,35 @@ struct TcItem {
     uint32_t tile, c0, c1, ntiles, done;
 };
 
-// KA: level-1 operand bytes per row; K2: level-2 GEMM operand bytes (0: none);
-// W2: level-2 Xor sketch words for the POPC check (used when K2 == 0);
-// NS: B stages; NT: columns per MMA tile (accumulator slots of NT columns).
-template <int KA, int K2, int W2, int NS, int NT>
+// KIND: operand kind; KA: level-1 operand bytes per row; K2: level-2 GEMM
+// operand bytes (0: none); W2: level-2 Xor sketch words for the POPC check
+// (used when K2 == 0); NS: B stages; NT: columns per MMA tile.
+template <int KIND, int KA, int K2, int W2, int NS, int NT>
 struct TcLayout {
+    static constexpr int kWords = KIND == kKindI8 ? (KA - 32) / 64 : (KA - 32) / 32;  // level-1 sketch words
+    static constexpr int kEpiWarps = NT == 192 ? 12 : 16;      // 3 or 4 per TMEM lane quarter
+    static constexpr int kThreads = 64 + 32 * kEpiWarps;
+    static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
     static constexpr int kA = 128 * (KA + K2);                 // one A slot
     static constexpr int kBop = NT * (KA + K2);                // B operands per stage
     static constexpr int kBsk = 0;  // level-2 column sketches are read from L2 for survivors only
     static constexpr int kBsz = NT * 4;                        // sizes
     static constexpr int kB = kBop + kBsk + kBsz;
     static constexpr int kAslots = K2 ? 1 : 2;
-    static constexpr int kQueue = kTcEpiWarps * kTcQueue * 8;
+    static constexpr int kQueue = kEpiWarps * kTcQueue * 8;
     static constexpr int kBytes = kAslots * kA + NS * kB + kQueue;
-    static constexpr int kColsPerWarp = NT / 4;                // 4 epilogue warps per lane quarter
-    static constexpr uint32_t kTmemCols = K2 ? 4 * NT : 2 * NT;
-    static_assert(kTmemCols <= 512, "TMEM");
+    static constexpr uint32_t kAccCols = K2 ? 4 * NT : 2 * NT;
+    static constexpr uint32_t kSfCol = kAccCols;              // fp4: 32 columns of A scales, then B scales
+    static constexpr uint32_t kTmemCols = KIND == kKindF4 ? 512 : (kAccCols <= 256 ? 256 : 512);
+    static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
+    static_assert(KIND == kKindI8 || kAccCols + 128 <= 512, "TMEM: accumulators + scale factors");
+    static_assert(kAccCols <= 512, "TMEM");
 };
 
-template <int KA, int K2, int W2, int NS, int NT>
-__global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
-    using L = TcLayout<KA, K2, W2, NS, NT>;
+template <int KIND, int KA, int K2, int W2, int NS, int NT>
+__global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads), 1) filter_tc_kernel(TcParams P) {
+    using L = TcLayout<KIND, KA, K2, W2, NS, NT>;
+    constexpr int kTcEpiWarps = L::kEpiWarps;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;                                   // [2][kA]
     uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
@@ -216,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kTmemCols = L::kTmemCols < 32 ? 32 : L::kTmemCols;  // 2 slots x (L1 [+ L2]) x NT
+    constexpr uint32_t kTmemCols = L::kTmemCols;  // 2 slots x (L1 [+ L2]) x NT (+ fp4 scale factors)
 
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -242,6 +304,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem_base = tmem_base_sh;
+    if constexpr (KIND == kKindF4) {
+        // unit block scales (ue8m0 127 = 1.0) for every A and B scale slot the MMA may read
+        if (warp >= 2 && warp < 6) {
+            const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+#pragma unroll
+            for (int c = 0; c < 128; c += 32) tmem_fill32(tmem_base + lanes + L::kSfCol + c, 0x7F7F7F7Fu);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
@@ -319,9 +393,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
 #pragma unroll
-                    for (int s = 0; s < KA / 32; ++s)
-                        umma_i8<NT>(d1, umma_desc(a0 + s * 256, (KA / 16) * 128),
-                                    umma_desc(b0 + s * 256, (KA / 16) * 128), s > 0);
+                    for (int s = 0; s < KA / 32; ++s) {
+                        const uint64_t da = umma_desc(a0 + s * 256, (KA / 16) * 128);
+                        const uint64_t db = umma_desc(b0 + s * 256, (KA / 16) * 128);
+                        if constexpr (KIND == kKindI8)
+                            umma_i8<NT>(d1, da, db, s > 0);
+                        else
+                            umma_f4<NT>(d1, da, db, s > 0, tmem_base + L::kSfCol, tmem_base + L::kSfCol + 32);
+                    }
                     if constexpr (K2 > 0) {
                         const uint32_t d2 = tmem_base + 2 * NT + as * NT;
 #pragma unroll
@@ -368,7 +447,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                 j0 = P.wstart[si];
                 bypass = static_cast<int64_t>(si) > P.cutoff;
 #pragma unroll
-                for (int w = 0; w < KA / 64; ++w) pc += __popcll(P.bits[static_cast<uint64_t>(i) * (KA / 64) + w]);
+                for (int w = 0; w < L::kWords; ++w) pc += __popcll(P.bits[static_cast<uint64_t>(i) * L::kWords + w]);
                 if constexpr (W2 > 0) {
 #pragma unroll
                     for (int w = 0; w < W2; ++w) mine2[w] = P.bits2[static_cast<uint64_t>(i) * W2 + w];
@@ -424,13 +503,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
                         // any survivor in the group <=> max_k D_k > cim1: 16 three-input
                         // maxima (VIMNMX3) decide most groups without building the mask
-                        int mx = __vimax3_s32(static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]));
-#pragma unroll
-                        for (int k = 3; k < 31; k += 2)
-                            mx = __vimax3_s32(mx, static_cast<int>(d[k]), static_cast<int>(d[k + 1]));
-                        mx = max(mx, static_cast<int>(d[31]));
-                        if (!__any_sync(0xFFFFFFFFu, bypass || mx > cim1)) continue;
-                        m = bypass ? 0xFFFFFFFFu : survivors32<true>(d, cim1, dummy, P.neg1);
+                        if (!__any_sync(0xFFFFFFFFu, bypass || any_above<KIND>(d, cim1))) continue;
+                        m = bypass ? 0xFFFFFFFFu : survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                     } else {
                         const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
                         const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
@@ -446,9 +520,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                                 cim1 = pc - T - 1;
                                 cim1_2 = pc2 - T - 1;
                             }
-                            m = survivors32<true>(d, cim1, dummy, P.neg1);
+                            m = survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                         } else {
-                            m = survivors_mixed(d, pc, P.maxham, si, cz + cl);
+                            m = survivors_mixed<KIND>(d, pc, P.maxham, si, cz + cl);
                         }
                         m = bypass ? rm : (m & rm);
                     }
@@ -457,8 +531,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
                     uint32_t e = m;
                     if constexpr (K2 > 0) {
                         tmem_ld32(tmem_base + lane_base + 2 * NT + as * NT + cl, d);
-                        e = m & (uni ? survivors32<true>(d, cim1_2, dummy, P.neg1)
-                                     : survivors_mixed(d, pc2, P.maxham, si, cz + cl));
+                        e = m & (uni ? survivors32<true, KIND>(d, cim1_2, dummy, P.neg1)
+                                     : survivors_mixed<KIND>(d, pc2, P.maxham, si, cz + cl));
                     } else if constexpr (W2 > 0) {
                         uint32_t mm = m;
                         e = 0;
@@ -494,14 +568,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) filter_tc_kernel(TcParams P) {
 
 // Expanded GEMM operands in the core-matrix layout (see the header comment).
 // One thread per (row, 16-byte K chunk).
+//   int8 (K = b + 32 bytes):  A = bit (u8), B = 2*bit (s8); extension
+//     A = 1,1  B = -ceil(pc/2), -floor(pc/2)
+//   fp4  (K = b + 64 e2m1 elements, packed two per byte, low nibble first):
+//     A = 1.0*bit, B = 2.0*bit; extension A = 1.0 everywhere,
+//     B = -6 (x floor(pc/6)) then the remainder as one or two of -1..-4 -- an
+//     exact small-integer sum -pc_j in f32 accumulation.
 struct ExpandParams {
     const uint64_t* bits;  // n_pad x W sketches
     uint8_t* opA;
     uint8_t* opB;
     uint32_t rows;         // n_pad (multiple of 8)
     int words;             // W
-    int K;                 // bytes per row = 64 W + 32
+    int K;                 // bytes per row
+    int fp4;
 };
+
+__device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -4, -6
+    switch (v) {
+        case 1: return 0xAu;
+        case 2: return 0xCu;
+        case 3: return 0xDu;
+        case 4: return 0xEu;
+        default: return 0xFu;
+    }
+}
 
 __global__ void expand_operands(ExpandParams P) {
     const int KC = P.K / 16;
@@ -511,21 +602,49 @@ __global__ void expand_operands(ExpandParams P) {
     const int c = static_cast<int>(idx % KC);
     uint32_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
     const int bitsn = 64 * P.words;
-    if (16 * c < bitsn) {
-        const uint64_t w = P.bits[static_cast<uint64_t>(r) * P.words + (16 * c) / 64];
-        const uint32_t bits16 = static_cast<uint32_t>(w >> ((16 * c) % 64)) & 0xFFFFu;
+    const uint64_t* row = P.bits + static_cast<uint64_t>(r) * P.words;
+    if (!P.fp4) {
+        if (16 * c < bitsn) {
+            const uint32_t bits16 = static_cast<uint32_t>(row[(16 * c) / 64] >> ((16 * c) % 64)) & 0xFFFFu;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const uint32_t bit = (bits16 >> k) & 1u;
-            a[k >> 2] |= bit << (8 * (k & 3));
-            b[k >> 2] |= (bit * 2u) << (8 * (k & 3));
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t bit = (bits16 >> k) & 1u;
+                a[k >> 2] |= bit << (8 * (k & 3));
+                b[k >> 2] |= (bit * 2u) << (8 * (k & 3));
+            }
+        } else if (16 * c == bitsn) {
+            int pcnt = 0;
+            for (int w = 0; w < P.words; ++w) pcnt += __popcll(row[w]);
+            const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
+            a[0] = 0x0101u;
+            b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) |
+                   (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
         }
-    } else if (16 * c == bitsn) {
-        int pcnt = 0;
-        for (int w = 0; w < P.words; ++w) pcnt += __popcll(P.bits[static_cast<uint64_t>(r) * P.words + w]);
-        const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
-        a[0] = 0x0101u;
-        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) | (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
+    } else {
+        const int e0 = 32 * c;  // first element of this chunk
+        if (e0 < bitsn) {
+            const uint32_t bits32 = static_cast<uint32_t>(row[e0 / 64] >> (e0 % 64));
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t bit = (bits32 >> k) & 1u;
+                a[k >> 3] |= (bit * 0x2u) << (4 * (k & 7));
+                b[k >> 3] |= (bit * 0x4u) << (4 * (k & 7));
+            }
+        } else {
+            int pcnt = 0;
+            for (int w = 0; w < P.words; ++w) pcnt += __popcll(row[w]);
+            const int sixes = pcnt / 6, rem = pcnt % 6;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int x = e0 - bitsn + k;  // extension element index
+                uint32_t code = 0;
+                if (x < sixes) code = 0xFu;
+                else if (x == sixes && rem) code = e2m1_neg(rem == 5 ? 3 : rem);
+                else if (x == sixes + 1 && rem == 5) code = e2m1_neg(2);
+                a[k >> 3] |= 0x2u << (4 * (k & 7));
+                b[k >> 3] |= code << (4 * (k & 7));
+            }
+        }
     }
     const uint64_t off = ((static_cast<uint64_t>(r / 8) * KC + c) * 8 + (r % 8)) * 16;
     *reinterpret_cast<uint4*>(P.opA + off) = make_uint4(a[0], a[1], a[2], a[3]);

@@ -54,18 +54,19 @@ def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
         assert sha(store) == e["sha256"], e
 
 
-FILTERS = ["tc", "popc", "tc-l2gemm"]
+FILTERS = ["tc-fp4", "tc-i8", "popc", "tc-l2gemm"]
 
 
 def set_filter(monkeypatch, flavour):
     monkeypatch.setenv("SSJB_FILTER", "popc" if flavour == "popc" else "tc")
     monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour == "tc-l2gemm" else "0")
+    monkeypatch.setenv("SSJB_TC_KIND", "i8" if flavour == "tc-i8" else "fp4")
 
 
 @pytest.mark.parametrize("flavour", FILTERS)
 def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
-    """Every reference fixture, through each filter kernel (tcgen05 GEMM, POPC,
-    tcgen05 with the level-2 GEMM)."""
+    """Every reference fixture, through each filter kernel (tcgen05 fp4 and int8
+    GEMMs, POPC, tcgen05 with the level-2 GEMM)."""
     set_filter(monkeypatch, flavour)
     for e in golden["joins"]:
         rep = S.join(colls(e["collection"]), options_of(lib, e))
