@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -124,19 +125,21 @@ struct SketchSet {
     int method = -1, width = 0, hash = 0, words2 = 0;
     uint64_t* bits = nullptr;
     uint64_t* bits2 = nullptr;
-    uint8_t *opA_i8 = nullptr, *opB_i8 = nullptr;  // level-1 int8 operands
-    uint8_t *opA_f4 = nullptr, *opB_f4 = nullptr;  // level-1 fp4 operands
-    uint8_t *opA2 = nullptr, *opB2 = nullptr;      // level-2 int8 operands
+    // expanded tcgen05 operand arrays (A, B) per variant: 0 int8, 1 int8 + level-2, 2 fp4
+    uint8_t* opA[3] = {nullptr, nullptr, nullptr};
+    uint8_t* opB[3] = {nullptr, nullptr, nullptr};
     bool owned = false;  // cudaMalloc'd (persistent) rather than arena memory
     ~SketchSet() {
         if (!owned) return;
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(device);
-        for (void* p : {static_cast<void*>(bits), static_cast<void*>(bits2), static_cast<void*>(opA_i8),
-                        static_cast<void*>(opB_i8), static_cast<void*>(opA_f4), static_cast<void*>(opB_f4),
-                        static_cast<void*>(opA2), static_cast<void*>(opB2)})
-            cudaFree(p);
+        cudaFree(bits);
+        cudaFree(bits2);
+        for (int v = 0; v < 3; ++v) {
+            cudaFree(opA[v]);
+            cudaFree(opB[v]);
+        }
         cudaSetDevice(cur);
     }
 };
@@ -319,22 +322,36 @@ TcKernel tc_kernel() {
 //   i8:   kind::i8, K = b + 32 bytes, 256-column tiles; with the level-2
 //         GEMM on 256-bit Xor sketches (l2gemm), 128-column tiles
 TcKernel tc_select(int words, bool l2gemm, bool fp4) {
+    const char* nenv = std::getenv("SSJB_TC_N");  // tile width override (experiments)
+    const int nt = nenv && *nenv ? std::atoi(nenv) : 0;
     if (l2gemm) {
         switch (words) {
             case 1: return tc_kernel<dev::kKindI8, 96, 288, 4, 3, 128>();
             case 2: return tc_kernel<dev::kKindI8, 160, 288, 4, 2, 128>();
         }
     } else if (fp4) {
+        if (nt == 128) {
+            switch (words) {
+                case 1: return tc_kernel<dev::kKindF4, 64, 0, 4, 8, 128>();
+                case 2: return tc_kernel<dev::kKindF4, 96, 0, 4, 12, 128>();
+            }
+        }
         switch (words) {
-            case 1: return tc_kernel<dev::kKindF4, 64, 0, 4, 6, 192>();
-            case 2: return tc_kernel<dev::kKindF4, 96, 0, 4, 6, 192>();
+            case 1: return tc_kernel<dev::kKindF4, 64, 0, 4, 12, 192>();
+            case 2: return tc_kernel<dev::kKindF4, 96, 0, 4, 8, 192>();
             case 3: return tc_kernel<dev::kKindF4, 128, 0, 8, 5, 192>();
-            case 4: return tc_kernel<dev::kKindF4, 160, 0, 8, 5, 192>();
+            case 4: return tc_kernel<dev::kKindF4, 160, 0, 8, 4, 192>();
         }
     } else {
+        if (nt == 128) {
+            switch (words) {
+                case 1: return tc_kernel<dev::kKindI8, 96, 0, 4, 8, 128>();
+                case 2: return tc_kernel<dev::kKindI8, 160, 0, 4, 6, 128>();
+            }
+        }
         switch (words) {
             case 1: return tc_kernel<dev::kKindI8, 96, 0, 4, 4, 256>();
-            case 2: return tc_kernel<dev::kKindI8, 160, 0, 4, 4, 256>();
+            case 2: return tc_kernel<dev::kKindI8, 160, 0, 4, 3, 256>();
             case 3: return tc_kernel<dev::kKindI8, 224, 0, 8, 2, 256>();
             case 4: return tc_kernel<dev::kKindI8, 288, 0, 8, 3, 128>();
         }
@@ -344,17 +361,27 @@ TcKernel tc_select(int words, bool l2gemm, bool fp4) {
 
 size_t operand_bytes(int words, bool fp4) { return fp4 ? 32 * words + 32 : 64 * words + 32; }
 
-void launch_expand(const uint64_t* bits, int words, uint8_t* opA, uint8_t* opB, uint32_t rows, bool fp4, cudaStream_t s,
-                   uint64_t& launches) {
+// Operand row bytes of a variant: level 1 | level 2 (int8, 256-bit sketch) | 16-byte size chunk.
+size_t operand_row(int words, int variant) {
+    return operand_bytes(words, variant == 2) + (variant == 1 ? 64 * 4 + 32 : 0) + 16;
+}
+
+void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int words2, const uint32_t* sizes,
+                   uint8_t* opA, uint8_t* opB, uint32_t rows, int variant, cudaStream_t s, uint64_t& launches) {
     dev::ExpandParams E{};
     E.bits = bits;
+    E.bits2 = bits2;
+    E.sizes = sizes;
     E.opA = opA;
     E.opB = opB;
     E.rows = rows;
     E.words = words;
-    E.fp4 = fp4 ? 1 : 0;
-    E.K = static_cast<int>(operand_bytes(words, fp4));
-    const uint64_t threads = static_cast<uint64_t>(rows) * (E.K / 16);
+    E.words2 = variant == 1 ? words2 : 0;
+    E.fp4 = variant == 2 ? 1 : 0;
+    E.K1 = static_cast<int>(operand_bytes(words, variant == 2));
+    E.K2 = variant == 1 ? 64 * words2 + 32 : 0;
+    const int kct = (E.K1 + E.K2) / 16 + 1;
+    const uint64_t threads = static_cast<uint64_t>(rows) * kct;
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
     ++launches;
     CK(cudaGetLastError());
@@ -477,6 +504,7 @@ struct Tiling {
     uint32_t ntiles = 0;
     std::vector<uint64_t> item_base;  // ntiles + 1
     std::vector<uint32_t> col_lo;     // ntiles
+    std::vector<uint32_t> item_tile;  // tile of each work item
 };
 
 Tiling make_tiling(const Collection& c, const JoinPlan& plan) {
@@ -495,6 +523,10 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan) {
         if (rl > lo && j0 < rl) items = (rl - lo + dev::kColChunk - 1) / dev::kColChunk;
         t.item_base[k + 1] = t.item_base[k] + items;
     }
+    t.item_tile.resize(t.item_base.back());
+    for (uint32_t k = 0; k < t.ntiles; ++k)
+        std::fill(t.item_tile.begin() + static_cast<ptrdiff_t>(t.item_base[k]),
+                  t.item_tile.begin() + static_cast<ptrdiff_t>(t.item_base[k + 1]), k);
     return t;
 }
 
@@ -593,11 +625,14 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     Tiling tl = make_tiling(c, plan);
     uint64_t* d_item_base = A.alloc<uint64_t>(tl.item_base.size());
     uint32_t* d_col_lo = A.alloc<uint32_t>(tl.col_lo.size());
+    uint32_t* d_item_tile = A.alloc<uint32_t>(tl.item_tile.size());
     CK(cudaMemcpyAsync(d_maxham, maxham.data(), maxham.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_minov, plan.minov.data(), plan.minov.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_wstart, plan.window_start.data(), plan.window_start.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_item_base, tl.item_base.data(), tl.item_base.size() * 8, cudaMemcpyHostToDevice, s));
     if (tl.ntiles) CK(cudaMemcpyAsync(d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!tl.item_tile.empty())
+        CK(cudaMemcpyAsync(d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4, cudaMemcpyHostToDevice, s));
     st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4 + tl.item_base.size() * 8 + tl.col_lo.size() * 4;
     cudaEvent_t e_up = T.mark();
 
@@ -621,9 +656,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
     }
     const char* kenv = std::getenv("SSJB_TC_KIND");
-    const bool fp4 = use_tc && !l2gemm && !(kenv && std::string(kenv) == "i8");
+    const bool fp4 = use_tc && !l2gemm && kenv && std::string(kenv) == "fp4";  // int8 by default
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
-    const size_t KA = operand_bytes(W, fp4), K2b = 64 * W2 + 32;
     const bool resident = rep->stream == nullptr;
     std::shared_ptr<SketchSet> sk;
     // resident replicas build sketches/operands once, under the collection lock
@@ -660,22 +694,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         sk = fresh;
         built = true;
     }
-    if (use_tc && fp4 && !sk->opA_f4) {
-        sk->opA_f4 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-        sk->opB_f4 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-        launch_expand(sk->bits, W, sk->opA_f4, sk->opB_f4, n_pad, true, s, st.launches);
-        built = true;
-    }
-    if (use_tc && !fp4 && !sk->opA_i8) {
-        sk->opA_i8 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-        sk->opB_i8 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * KA));
-        launch_expand(sk->bits, W, sk->opA_i8, sk->opB_i8, n_pad, false, s, st.launches);
-        built = true;
-    }
-    if (l2gemm && !sk->opA2) {
-        sk->opA2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
-        sk->opB2 = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * K2b));
-        launch_expand(sk->bits2, W2, sk->opA2, sk->opB2, n_pad, false, s, st.launches);
+    const int variant = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : 0));
+    if (variant >= 0 && !sk->opA[variant]) {
+        const size_t rowb = operand_row(W, variant);
+        sk->opA[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
+        sk->opB[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
+        launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, sk->opA[variant], sk->opB[variant], n_pad, variant, s,
+                      st.launches);
         built = true;
     }
     if (resident) {
@@ -687,10 +712,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     }
     uint64_t* d_bits = enabled ? sk->bits : A.alloc<uint64_t>((n + kPadRows + 8) * W);
     uint64_t* d_bits2 = enabled && W2 ? sk->bits2 : nullptr;
-    uint8_t* d_opA = !use_tc ? nullptr : (fp4 ? sk->opA_f4 : sk->opA_i8);
-    uint8_t* d_opB = !use_tc ? nullptr : (fp4 ? sk->opB_f4 : sk->opB_i8);
-    uint8_t* d_opA2 = l2gemm ? sk->opA2 : nullptr;
-    uint8_t* d_opB2 = l2gemm ? sk->opB2 : nullptr;
+    uint8_t* d_opA = variant >= 0 ? sk->opA[variant] : nullptr;
+    uint8_t* d_opB = variant >= 0 ? sk->opB[variant] : nullptr;
     cudaEvent_t e_build = T.mark();
 
     // buffers
@@ -755,14 +778,14 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
         TP.opA = d_opA;
         TP.opB = d_opB;
-        TP.opA2 = d_opA2;
-        TP.opB2 = d_opB2;
         TP.bits = d_bits;
         TP.bits2 = d_bits2;
         TP.sizes = rep->sizes;
         TP.maxham = d_maxham;
+        TP.maxham_len = static_cast<int>(maxham.size());
         TP.wstart = d_wstart;
         TP.item_base = d_item_base;
+        TP.item_tile = d_item_tile;
         TP.tile_col_lo = d_col_lo;
         TP.surv = d_surv;
         TP.rowcnt = d_rowcnt;
@@ -775,6 +798,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.cutoff = FP.cutoff;
         TP.neg1 = -1;
         TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
+        if (TP.debug & 2) {
+            TP.trace = A.alloc<unsigned long long>(2048 + 2 * 8192);
+            CK(cudaMemsetAsync(TP.trace, 0, (2048 + 2 * 8192) * 8, s));
+        }
         st.filter_kernel = l2gemm ? 2 : (fp4 ? 3 : 1);
     }
 
@@ -1012,6 +1039,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         out.pairs = std::move(merged);
     }
 
+    if (use_tc && TP.trace) {
+        std::vector<unsigned long long> tr(2048 + 2 * 8192);
+        CK(cudaMemcpy(tr.data(), TP.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen("gpurun_out/tc_trace.txt", "a")) {
+            for (int k = 0; k < 512; ++k) {
+                std::fprintf(f, "%d %llu %llu %llu", k, tr[k * 4], tr[k * 4 + 1], tr[k * 4 + 2]);
+                for (int w = 0; w < 16; ++w) std::fprintf(f, " %llu", tr[2048 + k * 16 + w]);
+                for (int w = 0; w < 16; ++w) std::fprintf(f, " %llu", tr[2048 + 8192 + k * 16 + w]);
+                std::fprintf(f, "\n");
+            }
+            std::fprintf(f, "---\n");
+            std::fclose(f);
+        }
+    }
     out.candidates = plan.window_pairs;
     out.bitmap_tested = h_ctl.tested;
     out.pruned_bitmap = h_ctl.pruned;

@@ -25,26 +25,29 @@
 // L2G) or a POPC check of the level-1 survivors against staged sketches.
 #pragma once
 
+#include <climits>
+
 #include "kernels.cuh"
 
 namespace ssjb {
 namespace dev {
 
 constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
+constexpr int kTcLut = 1536;       // shared-memory copy of maxham[] (entries)
 constexpr int kKindI8 = 0;         // tcgen05 kind::i8, s32 accumulators
 constexpr int kKindF4 = 1;         // tcgen05 kind::mxf4 (packed e2m1, unit block scales), f32 accumulators
 
 struct TcParams {
-    const uint8_t* opA;        // expanded level-1 rows, core layout, n_pad x KA
-    const uint8_t* opB;        // expanded level-1 columns (s8), n_pad x KA
-    const uint8_t* opA2;       // level-2 GEMM operands (L2G), n_pad x K2
-    const uint8_t* opB2;
+    const uint8_t* opA;        // expanded rows, core layout, n_pad x (KA [+ K2] + 16): L1 | L2 | size
+    const uint8_t* opB;        // expanded columns, same layout (B encoding)
     const uint64_t* bits;      // level-1 sketches (row popcounts)
     const uint64_t* bits2;     // level-2 Xor sketches (rows; staged columns for the POPC check)
     const uint32_t* sizes;
     const int32_t* maxham;
+    int maxham_len;
     const uint32_t* wstart;
     const uint64_t* item_base;
+    const uint32_t* item_tile;   // tile of each work item
     const uint32_t* tile_col_lo;
     uint2* surv;
     uint32_t* rowcnt;
@@ -57,6 +60,7 @@ struct TcParams {
     int64_t cutoff;
     int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
     int debug;                 // bit 0: skip the epilogue math (pipeline probe)
+    unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,6 +69,36 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+// Spin without a suspend hint (single-lane producer / MMA roles: wake-up
+// latency is on the critical path there).
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo) {
@@ -176,17 +210,24 @@ __device__ __forceinline__ bool any_above(const uint32_t (&d)[32], int cim1) {
     for (int k = 3; k < 31; k += 2) mx = __vimax3_s32(mx, static_cast<int>(d[k]), static_cast<int>(d[k + 1]));
     mx = max(mx, static_cast<int>(d[31]));
     if constexpr (KIND == kKindI8) return mx > cim1;
-    else return cim1 < 0 || mx > __float_as_int(static_cast<float>(cim1) + 0.5f);
+    else return mx > cim1;  // caller passes the bit pattern of cim1 + 0.5f, or INT_MIN when cim1 < 0
+}
+
+// Column sizes live in the last 16-byte chunk of every operand row (one
+// bulk copy per tile carries operands and sizes); KCT = chunks per row.
+template <int KCT>
+__device__ __forceinline__ uint32_t stage_size(const uint8_t* stage, int col) {
+    return *reinterpret_cast<const uint32_t*>(stage + ((col >> 3) * KCT + (KCT - 1)) * 128 + (col & 7) * 16);
 }
 
 // Non-uniform group (column sizes change inside it): per-column threshold.
-template <int KIND = kKindI8>
+template <int KIND, int KCT>
 __device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int base, const int32_t* maxham,
-                                                    uint32_t si, const uint32_t* cz) {
+                                                    uint32_t si, const uint8_t* stage, int cl) {
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k)
-        m |= ((base - __ldg(maxham + si + cz[k]) - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
+        m |= ((base - maxham[si + stage_size<KCT>(stage, cl + k)] - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
     return m;
 }
 
@@ -248,20 +289,26 @@ struct TcLayout {
     static constexpr int kEpiWarps = NT == 192 ? 12 : 16;      // 3 or 4 per TMEM lane quarter
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
-    static constexpr int kA = 128 * (KA + K2);                 // one A slot
-    static constexpr int kBop = NT * (KA + K2);                // B operands per stage
-    static constexpr int kBsk = 0;  // level-2 column sketches are read from L2 for survivors only
-    static constexpr int kBsz = NT * 4;                        // sizes
-    static constexpr int kB = kBop + kBsk + kBsz;
+    static constexpr int kRow = KA + K2 + 16;                  // operand row: L1 | L2 | size chunk
+    static constexpr int kKCT = kRow / 16;                     // 16-byte chunks per row
+    static constexpr int kSbo = kKCT * 128;                    // stride between 8-row core groups
+    static constexpr int kA = 128 * kRow;                      // one A slot
+    static constexpr int kB = NT * kRow;                       // one B stage: a single bulk copy
     static constexpr int kAslots = K2 ? 1 : 2;
     static constexpr int kQueue = kEpiWarps * kTcQueue * 8;
     static constexpr int kBytes = kAslots * kA + NS * kB + kQueue;
-    static constexpr uint32_t kAccCols = K2 ? 4 * NT : 2 * NT;
+    // accumulator slots in flight: as many NT-column slots (x2 with the level-2
+    // GEMM) as TMEM holds next to the fp4 scale factors, at most 4
+    static constexpr int kAccSlots = (((KIND == kKindF4 ? 384 : 512) / (NT * (K2 ? 2 : 1))) < 4)
+                                         ? ((KIND == kKindF4 ? 384 : 512) / (NT * (K2 ? 2 : 1))) : 4;
+    static constexpr uint32_t kAccCols = (K2 ? 2 : 1) * kAccSlots * NT;
+    static constexpr uint32_t kL2Col = kAccSlots * NT;        // level-2 accumulators follow level 1
     static constexpr uint32_t kSfCol = kAccCols;              // fp4: 32 columns of A scales, then B scales
     static constexpr uint32_t kTmemCols = KIND == kKindF4 ? 512 : (kAccCols <= 256 ? 256 : 512);
     static_assert(kColsPerWarp % 32 == 0, "epilogue column split");
+    static_assert(kBytes + 1024 + 4 * kTcLut + 512 <= 232448, "shared memory per CTA");
     static_assert(KIND == kKindI8 || kAccCols + 128 <= 512, "TMEM: accumulators + scale factors");
-    static_assert(kAccCols <= 512, "TMEM");
+    static_assert(kAccCols <= 512 && kAccSlots >= 2, "TMEM");
 };
 
 template <int KIND, int KA, int K2, int W2, int NS, int NT>
@@ -273,9 +320,10 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
     uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
     uint2* sQ = reinterpret_cast<uint2*>(sB + NS * L::kB);  // [8][kTcQueue]
     __shared__ __align__(8) uint64_t item_full[2], item_empty[2], a_full[2], a_empty[2];
-    __shared__ __align__(8) uint64_t b_full[NS], b_empty[NS], acc_full[2], acc_empty[2];
+    __shared__ __align__(8) uint64_t b_full[NS], b_empty[NS], acc_full[L::kAccSlots], acc_empty[L::kAccSlots];
     __shared__ TcItem items[2];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int32_t s_maxham[kTcLut];  // maxham[] when it fits (2*max_size + 1 <= kTcLut)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t kTmemCols = L::kTmemCols;  // 2 slots x (L1 [+ L2]) x NT (+ fp4 scale factors)
@@ -285,12 +333,18 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                      "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    const bool lut_smem = P.maxham_len <= kTcLut;
+    if (lut_smem)
+        for (int k = threadIdx.x; k < P.maxham_len; k += blockDim.x) s_maxham[k] = P.maxham[k];
+    const int32_t* maxham = lut_smem ? s_maxham : P.maxham;
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; ++s) {
             mbar_init(&item_full[s], 1);
             mbar_init(&item_empty[s], 1 + kTcEpiWarps);
             mbar_init(&a_full[s], 1);
             mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < L::kAccSlots; ++s) {
             mbar_init(&acc_full[s], 1);
             mbar_init(&acc_empty[s], kTcEpiWarps);
         }
@@ -321,10 +375,14 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             uint32_t iseq = 0, tseq = 0;
+            // the next work item is claimed and looked up while the current one's
+            // column tiles are still streaming (hides the atomic + table latency)
+            unsigned long long nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+            uint32_t nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
             for (;;) {
                 const int slot = iseq & 1;
-                mbar_wait(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
-                const unsigned long long it = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                mbar_spin(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
+                const unsigned long long it = nxt;
                 TcItem info{};
                 info.item = it;
                 if (it >= P.item_end) {
@@ -333,12 +391,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     mbar_arrive(&item_full[slot]);
                     break;
                 }
-                uint32_t lo = P.tile_begin, hi = P.ntiles;
-                while (hi - lo > 1) {
-                    uint32_t mid = (lo + hi) >> 1;
-                    if (P.item_base[mid] <= it) lo = mid; else hi = mid;
-                }
-                const uint32_t tile = lo;
+                const uint32_t tile = nxt_tile;
                 const uint32_t chunk = static_cast<uint32_t>(it - P.item_base[tile]);
                 const uint32_t row0 = P.row_begin + tile * kRowTile;
                 const uint32_t rows_end = min(row0 + kRowTile, P.row_end);
@@ -350,23 +403,26 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 items[slot] = info;
                 // row operand (A): 128 rows, contiguous in the core layout
                 const int aslot = iseq % L::kAslots;
-                mbar_wait(&a_empty[aslot], ((iseq / L::kAslots) & 1) ^ 1);
+                mbar_spin(&a_empty[aslot], ((iseq / L::kAslots) & 1) ^ 1);
                 mbar_expect_tx(&a_full[aslot], L::kA);
-                tma_load_1d(sA + aslot * L::kA, P.opA + static_cast<uint64_t>(row0) * KA, 128 * KA, &a_full[aslot]);
-                if constexpr (K2 > 0)
-                    tma_load_1d(sA + aslot * L::kA + 128 * KA, P.opA2 + static_cast<uint64_t>(row0) * K2, 128 * K2,
-                                &a_full[aslot]);
+                tma_load_1d(sA + aslot * L::kA, P.opA + static_cast<uint64_t>(row0) * L::kRow, L::kA, &a_full[aslot]);
                 mbar_arrive(&item_full[slot]);
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
-                    mbar_wait(&b_empty[st], ((tseq / NS) & 1) ^ 1);
+                    mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     uint8_t* dst = sB + st * L::kB;
                     mbar_expect_tx(&b_full[st], L::kB);
-                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * KA, NT * KA, &b_full[st]);
-                    if constexpr (K2 > 0)
-                        tma_load_1d(dst + NT * KA, P.opB2 + static_cast<uint64_t>(col) * K2, NT * K2, &b_full[st]);
-                    tma_load_1d(dst + L::kBop + L::kBsk, P.sizes + col, L::kBsz, &b_full[st]);
+                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
+                    if (t == 0) {
+                        nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                        nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+                    }
+                }
+                if (info.ntiles == 0) {
+                    nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                    nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
                 }
                 ++iseq;
             }
@@ -377,36 +433,38 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             uint32_t iseq = 0, tseq = 0, aseq = 0;
             for (;;) {
                 const int slot = iseq & 1;
-                mbar_wait(&item_full[slot], (iseq >> 1) & 1);
+                mbar_spin(&item_full[slot], (iseq >> 1) & 1);
                 const TcItem info = items[slot];
                 mbar_arrive(&item_empty[slot]);
                 if (info.done) break;
                 const int aslot = iseq % L::kAslots;
-                mbar_wait(&a_full[aslot], (iseq / L::kAslots) & 1);
+                mbar_spin(&a_full[aslot], (iseq / L::kAslots) & 1);
                 const uint32_t a0 = smem_u32(sA + aslot * L::kA);
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
                     const int st = tseq % NS;
-                    const int as = aseq & 1;
-                    mbar_wait(&b_full[st], (tseq / NS) & 1);
-                    mbar_wait(&acc_empty[as], ((aseq >> 1) & 1) ^ 1);
+                    const int as = aseq % L::kAccSlots;
+                    mbar_spin(&b_full[st], (tseq / NS) & 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
+                    mbar_spin(&acc_empty[as], ((aseq / L::kAccSlots) & 1) ^ 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
 #pragma unroll
                     for (int s = 0; s < KA / 32; ++s) {
-                        const uint64_t da = umma_desc(a0 + s * 256, (KA / 16) * 128);
-                        const uint64_t db = umma_desc(b0 + s * 256, (KA / 16) * 128);
+                        const uint64_t da = umma_desc(a0 + s * 256, L::kSbo);
+                        const uint64_t db = umma_desc(b0 + s * 256, L::kSbo);
                         if constexpr (KIND == kKindI8)
                             umma_i8<NT>(d1, da, db, s > 0);
                         else
                             umma_f4<NT>(d1, da, db, s > 0, tmem_base + L::kSfCol, tmem_base + L::kSfCol + 32);
                     }
                     if constexpr (K2 > 0) {
-                        const uint32_t d2 = tmem_base + 2 * NT + as * NT;
+                        const uint32_t d2 = tmem_base + L::kL2Col + as * NT;
 #pragma unroll
                         for (int s = 0; s < K2 / 32; ++s)
-                            umma_i8<NT>(d2, umma_desc(a0 + 128 * KA + s * 256, (K2 / 16) * 128),
-                                        umma_desc(b0 + NT * KA + s * 256, (K2 / 16) * 128), s > 0);
+                            umma_i8<NT>(d2, umma_desc(a0 + KA * 8 + s * 256, L::kSbo),
+                                        umma_desc(b0 + KA * 8 + s * 256, L::kSbo), s > 0);
                     }
                     umma_commit(&b_empty[st]);
                     umma_commit(&acc_full[as]);
@@ -424,7 +482,11 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         uint2* q = sQ + ew * kTcQueue;
         int qlen = 0;
-        uint32_t iseq = 0, tseq = 0, aseq = 0;
+        uint32_t iseq = 0;
+        uint32_t st_idx = 0, st_phase = 0, acc_idx = 0, acc_phase = 0;  // ring positions
+        uint32_t tile_seq = 0;
+        const uint32_t bfull_u32 = smem_u32(&b_full[0]), bempty_u32 = smem_u32(&b_empty[0]);
+        const uint32_t accfull_u32 = smem_u32(&acc_full[0]), accempty_u32 = smem_u32(&acc_empty[0]);
         for (;;) {
             const int slot = iseq & 1;
             mbar_wait(&item_full[slot], (iseq >> 1) & 1);
@@ -469,30 +531,31 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             }
             uint32_t cnt = 0;
             uint32_t last_sz = 0xFFFFFFFFu;  // cim1 cache: sizes are sorted, so it rarely changes
-            int cim1 = 0, cim1_2 = 0;
-            for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
-                const int st = tseq % NS;
-                const int as = aseq & 1;
-                mbar_wait(&b_full[st], (tseq / NS) & 1);
-                mbar_wait(&acc_full[as], (aseq >> 1) & 1);
+            int cim1 = 0, cim1_2 = 0, cim1_key = 0;
+            for (uint32_t t = 0; t < info.ntiles; ++t) {
+                const int st = static_cast<int>(st_idx), as = static_cast<int>(acc_idx);
+                mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
+                mbar_wait_u32(accfull_u32 + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512) P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
+                ++tile_seq;
                 const uint8_t* stage = sB + st * L::kB;
-                const uint32_t* cz = reinterpret_cast<const uint32_t*>(stage + L::kBop + L::kBsk);
                 const int cw = part * L::kColsPerWarp;               // this warp's first column
                 const uint32_t wbase = info.c0 + t * NT + cw;
-                const uint32_t szw0 = cz[cw], szw1 = cz[cw + L::kColsPerWarp - 1];
+                const uint32_t szw0 = stage_size<L::kKCT>(stage, cw);
+                const uint32_t szw1 = stage_size<L::kKCT>(stage, cw + L::kColsPerWarp - 1);
                 // fast path: every group of this warp's range is inside all 32
                 // windows and of one column size (the bulk of the pair space)
                 const bool fast = szw0 == szw1 && wbase >= lo_max && wbase + L::kColsPerWarp <= hi_min;
                 if (fast && szw0 != last_sz) {
                     last_sz = szw0;
-                    const int T = __ldg(P.maxham + si + szw0);
+                    const int T = maxham[si + szw0];
                     cim1 = pc - T - 1;
                     cim1_2 = pc2 - T - 1;
+                    cim1_key = cim1 < 0 ? INT_MIN : __float_as_int(static_cast<float>(cim1) + 0.5f);
                 }
 #pragma unroll 1
-                for (int g = 0; g < L::kColsPerWarp / 32; ++g) {
-                    if (P.debug & 1) break;
+                for (int g = 0; g < ((P.debug & 1) ? 0 : L::kColsPerWarp / 32); ++g) {
                     const int cl = cw + g * 32;  // column within the tile
                     const uint32_t gbase = wbase + g * 32;
                     uint32_t d[32];
@@ -503,7 +566,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
                         // any survivor in the group <=> max_k D_k > cim1: 16 three-input
                         // maxima (VIMNMX3) decide most groups without building the mask
-                        if (!__any_sync(0xFFFFFFFFu, bypass || any_above<KIND>(d, cim1))) continue;
+                        if (!__any_sync(0xFFFFFFFFu, bypass || any_above<KIND>(d, KIND == kKindI8 ? cim1 : cim1_key))) continue;
                         m = bypass ? 0xFFFFFFFFu : survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                     } else {
                         const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
@@ -511,18 +574,19 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         const uint32_t rm = low_mask(kh) & ~low_mask(kl);
                         if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
-                        const uint32_t sz0 = cz[cl];
-                        uni = sz0 == cz[cl + 31];
+                        const uint32_t sz0 = stage_size<L::kKCT>(stage, cl);
+                        uni = sz0 == stage_size<L::kKCT>(stage, cl + 31);
                         if (uni) {
                             if (sz0 != last_sz) {
                                 last_sz = sz0;
-                                const int T = __ldg(P.maxham + si + sz0);
+                                const int T = maxham[si + sz0];
                                 cim1 = pc - T - 1;
                                 cim1_2 = pc2 - T - 1;
+                                cim1_key = cim1 < 0 ? INT_MIN : __float_as_int(static_cast<float>(cim1) + 0.5f);
                             }
                             m = survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                         } else {
-                            m = survivors_mixed<KIND>(d, pc, P.maxham, si, cz + cl);
+                            m = survivors_mixed<KIND, L::kKCT>(d, pc, maxham, si, stage, cl);
                         }
                         m = bypass ? rm : (m & rm);
                     }
@@ -530,9 +594,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (!__any_sync(0xFFFFFFFFu, m != 0)) continue;
                     uint32_t e = m;
                     if constexpr (K2 > 0) {
-                        tmem_ld32(tmem_base + lane_base + 2 * NT + as * NT + cl, d);
+                        tmem_ld32(tmem_base + lane_base + L::kL2Col + as * NT + cl, d);
                         e = m & (uni ? survivors32<true, KIND>(d, cim1_2, dummy, P.neg1)
-                                     : survivors_mixed<KIND>(d, pc2, P.maxham, si, cz + cl));
+                                     : survivors_mixed<KIND, L::kKCT>(d, pc2, maxham, si, stage, cl));
                     } else if constexpr (W2 > 0) {
                         uint32_t mm = m;
                         e = 0;
@@ -543,7 +607,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                             int h = 0;
 #pragma unroll
                             for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ __ldg(col + w));
-                            e |= (h <= __ldg(P.maxham + si + cz[cl + k]) ? 1u : 0u) << k;
+                            e |= (h <= maxham[si + stage_size<L::kKCT>(stage, cl + k)] ? 1u : 0u) << k;
                         }
                     }
                     if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
@@ -551,8 +615,17 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&acc_empty[as]);
-                    mbar_arrive(&b_empty[st]);
+                    if (P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
+                    mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
+                    mbar_arrive_u32(bempty_u32 + 8 * st_idx);
+                }
+                if (++st_idx == NS) {
+                    st_idx = 0;
+                    st_phase ^= 1u;
+                }
+                if (++acc_idx == L::kAccSlots) {
+                    acc_idx = 0;
+                    acc_phase ^= 1u;
                 }
             }
             if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
@@ -575,13 +648,16 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
 //     B = -6 (x floor(pc/6)) then the remainder as one or two of -1..-4 -- an
 //     exact small-integer sum -pc_j in f32 accumulation.
 struct ExpandParams {
-    const uint64_t* bits;  // n_pad x W sketches
+    const uint64_t* bits;   // level-1 sketches, n_pad x W
+    const uint64_t* bits2;  // level-2 Xor sketches (with_l2), n_pad x W2
+    const uint32_t* sizes;  // |r| (padded)
     uint8_t* opA;
     uint8_t* opB;
-    uint32_t rows;         // n_pad (multiple of 8)
-    int words;             // W
-    int K;                 // bytes per row
-    int fp4;
+    uint32_t rows;          // n_pad (multiple of 8)
+    int words, words2;
+    int K1;                 // level-1 bytes per row
+    int K2;                 // level-2 bytes per row (0: none)
+    int fp4;                // level-1 encoding
 };
 
 __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -4, -6
@@ -594,59 +670,72 @@ __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -
     }
 }
 
-__global__ void expand_operands(ExpandParams P) {
-    const int KC = P.K / 16;
-    const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<uint64_t>(P.rows) * KC) return;
-    const uint32_t r = static_cast<uint32_t>(idx / KC);
-    const int c = static_cast<int>(idx % KC);
-    uint32_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
-    const int bitsn = 64 * P.words;
-    const uint64_t* row = P.bits + static_cast<uint64_t>(r) * P.words;
-    if (!P.fp4) {
-        if (16 * c < bitsn) {
-            const uint32_t bits16 = static_cast<uint32_t>(row[(16 * c) / 64] >> ((16 * c) % 64)) & 0xFFFFu;
+// int8 segment chunk c (16 bytes = 16 elements) of a sketch with `words` words
+__device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c, uint32_t (&a)[4], uint32_t (&b)[4]) {
+    const int bitsn = 64 * words;
+    if (16 * c < bitsn) {
+        const uint32_t bits16 = static_cast<uint32_t>(row[(16 * c) / 64] >> ((16 * c) % 64)) & 0xFFFFu;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const uint32_t bit = (bits16 >> k) & 1u;
-                a[k >> 2] |= bit << (8 * (k & 3));
-                b[k >> 2] |= (bit * 2u) << (8 * (k & 3));
-            }
-        } else if (16 * c == bitsn) {
-            int pcnt = 0;
-            for (int w = 0; w < P.words; ++w) pcnt += __popcll(row[w]);
-            const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
-            a[0] = 0x0101u;
-            b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) |
-                   (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t bit = (bits16 >> k) & 1u;
+            a[k >> 2] |= bit << (8 * (k & 3));
+            b[k >> 2] |= (bit * 2u) << (8 * (k & 3));
+        }
+    } else if (16 * c == bitsn) {
+        int pcnt = 0;
+        for (int w = 0; w < words; ++w) pcnt += __popcll(row[w]);
+        const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
+        a[0] = 0x0101u;
+        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) | (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
+    }
+}
+
+// fp4 segment chunk c (16 bytes = 32 e2m1 elements)
+__device__ __forceinline__ void expand_f4(const uint64_t* row, int words, int c, uint32_t (&a)[4], uint32_t (&b)[4]) {
+    const int bitsn = 64 * words;
+    const int e0 = 32 * c;
+    if (e0 < bitsn) {
+        const uint32_t bits32 = static_cast<uint32_t>(row[e0 / 64] >> (e0 % 64));
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t bit = (bits32 >> k) & 1u;
+            a[k >> 3] |= (bit * 0x2u) << (4 * (k & 7));
+            b[k >> 3] |= (bit * 0x4u) << (4 * (k & 7));
         }
     } else {
-        const int e0 = 32 * c;  // first element of this chunk
-        if (e0 < bitsn) {
-            const uint32_t bits32 = static_cast<uint32_t>(row[e0 / 64] >> (e0 % 64));
+        int pcnt = 0;
+        for (int w = 0; w < words; ++w) pcnt += __popcll(row[w]);
+        const int sixes = pcnt / 6, rem = pcnt % 6;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const uint32_t bit = (bits32 >> k) & 1u;
-                a[k >> 3] |= (bit * 0x2u) << (4 * (k & 7));
-                b[k >> 3] |= (bit * 0x4u) << (4 * (k & 7));
-            }
-        } else {
-            int pcnt = 0;
-            for (int w = 0; w < P.words; ++w) pcnt += __popcll(row[w]);
-            const int sixes = pcnt / 6, rem = pcnt % 6;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int x = e0 - bitsn + k;  // extension element index
-                uint32_t code = 0;
-                if (x < sixes) code = 0xFu;
-                else if (x == sixes && rem) code = e2m1_neg(rem == 5 ? 3 : rem);
-                else if (x == sixes + 1 && rem == 5) code = e2m1_neg(2);
-                a[k >> 3] |= 0x2u << (4 * (k & 7));
-                b[k >> 3] |= code << (4 * (k & 7));
-            }
+        for (int k = 0; k < 32; ++k) {
+            const int x = e0 - bitsn + k;  // extension element index
+            uint32_t code = 0;
+            if (x < sixes) code = 0xFu;
+            else if (x == sixes && rem) code = e2m1_neg(rem == 5 ? 3 : rem);
+            else if (x == sixes + 1 && rem == 5) code = e2m1_neg(2);
+            a[k >> 3] |= 0x2u << (4 * (k & 7));
+            b[k >> 3] |= code << (4 * (k & 7));
         }
     }
-    const uint64_t off = ((static_cast<uint64_t>(r / 8) * KC + c) * 8 + (r % 8)) * 16;
+}
+
+__global__ void expand_operands(ExpandParams P) {
+    const int KCT = (P.K1 + P.K2) / 16 + 1;
+    const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<uint64_t>(P.rows) * KCT) return;
+    const uint32_t r = static_cast<uint32_t>(idx / KCT);
+    const int c = static_cast<int>(idx % KCT);
+    uint32_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
+    if (c < P.K1 / 16) {
+        const uint64_t* row = P.bits + static_cast<uint64_t>(r) * P.words;
+        if (P.fp4) expand_f4(row, P.words, c, a, b);
+        else expand_i8(row, P.words, c, a, b);
+    } else if (c < (P.K1 + P.K2) / 16) {
+        expand_i8(P.bits2 + static_cast<uint64_t>(r) * P.words2, P.words2, c - P.K1 / 16, a, b);
+    } else {
+        a[0] = b[0] = P.sizes[r];  // the size chunk
+    }
+    const uint64_t off = ((static_cast<uint64_t>(r / 8) * KCT + c) * 8 + (r % 8)) * 16;
     *reinterpret_cast<uint4*>(P.opA + off) = make_uint4(a[0], a[1], a[2], a[3]);
     *reinterpret_cast<uint4*>(P.opB + off) = make_uint4(b[0], b[1], b[2], b[3]);
 }

@@ -56,12 +56,12 @@ __device__ __forceinline__ uint64_t pk_desc(uint32_t saddr, uint32_t sbo) {
 
 constexpr int kTcIters = 2048;  // groups of 8 MMAs
 
-__global__ void __launch_bounds__(128, 1) tc_i8_loop(unsigned* out) {
-    extern __shared__ __align__(1024) uint8_t sm[];  // A 128x32 + B 256x32 bytes (zeros are fine)
+__global__ void __launch_bounds__(128, 1) tc_i8_loop(unsigned* out, uint32_t sbo, uint32_t lbo, uint32_t bofs) {
+    extern __shared__ __align__(1024) uint8_t sm[];  // A and B tiles (zeros are fine)
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t tbase;
     const int warp = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < (128 + 256) * 32 / 4; k += blockDim.x) reinterpret_cast<uint32_t*>(sm)[k] = 0;
+    for (int k = threadIdx.x; k < 200 * 1024 / 4; k += blockDim.x) reinterpret_cast<uint32_t*>(sm)[k] = 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
             static_cast<uint32_t>(__cvta_generic_to_shared(&tbase))));
@@ -78,9 +78,11 @@ __global__ void __launch_bounds__(128, 1) tc_i8_loop(unsigned* out) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (threadIdx.x == 0) {
         const uint32_t a0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
-        const uint32_t b0 = a0 + 128 * 32;
+        const uint32_t b0 = a0 + bofs;
         const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
-        const uint64_t da = pk_desc(a0, 2 * 128), db = pk_desc(b0, 2 * 128);
+        uint64_t da = pk_desc(a0, sbo), db = pk_desc(b0, sbo);
+        da = (da & ~(uint64_t(0x3FFF) << 16)) | (uint64_t((lbo >> 4) & 0x3FFF) << 16);
+        db = (db & ~(uint64_t(0x3FFF) << 16)) | (uint64_t((lbo >> 4) & 0x3FFF) << 16);
         uint32_t phase[2] = {0, 0};
         for (int it = 0; it < kTcIters; ++it) {
             const int b = it & 1;
@@ -108,19 +110,20 @@ __global__ void __launch_bounds__(128, 1) tc_i8_loop(unsigned* out) {
     if (threadIdx.x == 0 && out == nullptr) out[0] = 1;
 }
 
-double run_tc(int sms) {
-    const int smem = (128 + 256) * 32;
+double run_tc(int sms, uint32_t sbo = 256, uint32_t lbo = 128, uint32_t bofs = 128 * 32) {
+    const int smem = 200 * 1024;
+    cudaFuncSetAttribute(tc_i8_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     unsigned* d;
     cudaMalloc(&d, 64);
-    tc_i8_loop<<<sms, 128, smem>>>(d);
+    tc_i8_loop<<<sms, 128, smem>>>(d, sbo, lbo, bofs);
     cudaDeviceSynchronize();
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(e0);
-        tc_i8_loop<<<sms, 128, smem>>>(d);
+        tc_i8_loop<<<sms, 128, smem>>>(d, sbo, lbo, bofs);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -168,6 +171,13 @@ int main(int argc, char** argv) {
     const double popc = run(popc_loop, sms, d);
     const double lop3 = run(lop3_loop, sms, d);
     const double tci8 = run_tc(sms);
+    if (argc > 2) {  // layout sweep: SBO / LBO effect on tcgen05 operand reads
+        const uint32_t sbos[] = {256, 640, 1408, 1536, 2048, 2816};
+        for (uint32_t sb : sbos)
+            std::printf("sbo=%u lbo=128: %.0f TOPS\n", sb, run_tc(sms, sb, 128, 16 * sb) / 1e12);
+        std::printf("sbo=128 lbo=2048 (chunk-major): %.0f TOPS\n", run_tc(sms, 128, 2048, 65536) / 1e12);
+        std::printf("sbo=128 lbo=4096 (chunk-major): %.0f TOPS\n", run_tc(sms, 128, 4096, 65536) / 1e12);
+    }
     cudaError_t err = cudaGetLastError();
     const double clk = clk_khz * 1e3;
     std::printf("{\"popc_ops_per_s\": %.6e, \"lop3_ops_per_s\": %.6e, \"tc_i8_ops_per_s\": %.6e, \"sms\": %d, "
