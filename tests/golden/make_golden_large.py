@@ -33,7 +33,8 @@ def main(prefixes):
     if os.path.exists(OUT):
         for line in open(OUT):
             done.add(json.loads(line)["case"])
-    cases = [("C1", lambda: D.c1(ref), (9, 10), 64)]
+    cases = [("C1", lambda: D.c1(ref), (9, 10), 64),
+             ("C3", lambda: D.c3(ref), (1, 2), 64)]
     for bits in (128, 256):
         for tau in reversed(D.C2_TAUS):
             cases.append((f"C2_b{bits}_{tau[0]}_{tau[1]}", None, tau, bits))
@@ -47,12 +48,15 @@ def main(prefixes):
             if c2 is None:
                 c2 = D.c2(ref)
             coll = c2
-        opts = S.par_bitmap_options(ref, threshold=tau, method=capi.SSJ_BITMAP_XOR, bits=bits,
+        method = capi.SSJ_BITMAP_NEXT if name == "C3" else capi.SSJ_BITMAP_XOR
+        opts = S.par_bitmap_options(ref, threshold=tau, method=method, bits=bits,
                                     cutoff_mode=capi.SSJ_CUTOFF_OFF, workers=os.cpu_count() or 8)
+        t, o = coll.csr()
         t0 = time.time()
         rep = S.join(coll, opts)
         wall = time.time() - t0
-        entry = dict(case=name, tau=list(tau), bits=bits, counters=rep.counters,
+        entry = dict(case=name, tau=list(tau), bits=bits, method=method, counters=rep.counters,
+                     collection_sha256=hashlib.sha256(t.tobytes() + o.tobytes()).hexdigest(),
                      saturated_records=rep.saturated_records, pair_count=int(len(rep.pairs)),
                      pairs_sha256=hashlib.sha256(rep.pairs.tobytes()).hexdigest(),
                      ref_total_s=rep.timings["total_s"], ref_wall_s=wall, workers=opts.workers)

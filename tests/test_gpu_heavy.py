@@ -1,0 +1,136 @@
+"""Full-size parity for the heavy-tailed BASELINE configs (C3 KOSARAK-shaped,
+C4 ORKUT-shaped, C5 AOL-shaped; paper_1711_07295_b200/datasets.py).
+
+The CPU oracle cannot finish these joins in test time (C4: 4.7e11 window
+pairs, C5: 1.2e13), so each config is pinned three ways:
+  * against the reference's own full-size run where one is committed
+    (tests/golden/large.jsonl, C3: the unmodified reference, 8 threads);
+  * row-block samples: ssjb_join_rows over blocks spread across the
+    collection vs the oracle on the same rows -- same pairs, same counters
+    (reference src/parallel_join.cpp:61-136 is row-local, so a row block of
+    the full collection is an exact sub-problem);
+  * size-independent properties of the full join: candidates == the
+    length-window sum, candidates == pruned_bitmap + verified, pairs strictly
+    sorted with id_r < id_s, a sample of pairs re-verified exactly on the host,
+    the full result restricted to each sampled block == that block's result,
+    and a 2-way row partition adds up to the full run.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR
+from paper_1711_07295_b200 import datasets as D
+from paper_1711_07295_b200 import ssjoin as S
+
+pytestmark = pytest.mark.gpu
+
+COUNTERS = ("candidates", "pruned_bitmap", "bitmap_tested", "verified", "matched")
+
+CONFIGS = {
+    "C3": (D.c3, D.c3_options, {}),
+    "C4": (D.c4, D.c4_options, {}),
+    "C4_b128": (D.c4, D.c4_options, {"bits": 128}),
+    "C5": (D.c5, D.c5_options, {}),
+}
+
+_COLL = {}
+
+
+def collection(lib, name):
+    key = CONFIGS[name][0]
+    if key not in _COLL:
+        _COLL.clear()  # one big collection in host memory at a time
+        c = key(lib)
+        _COLL[key] = (c, *c.csr())
+    return _COLL[key]
+
+
+def golden_large(case):
+    path = os.path.join(GOLDEN_DIR, "large.jsonl")
+    if os.path.exists(path):
+        for line in open(path):
+            e = json.loads(line)
+            if e["case"] == case:
+                return e
+    return None
+
+
+def blocks(n, count=6, rows=48):
+    starts = [int((k + 0.5) * n / count) for k in range(count)] + [n - rows]
+    return [(s, min(n, s + rows)) for s in starts]
+
+
+def host_overlap(t, o, a, b):
+    x = t[int(o[a]):int(o[a + 1])]
+    y = t[int(o[b]):int(o[b + 1])]
+    return len(np.intersect1d(x, y, assume_unique=True))
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_heavy_config(lib, oracle, name):
+    coll, t, o = collection(lib, name)
+    _, mkopts, kw = CONFIGS[name]
+    opts = mkopts(lib, **kw)
+    p, q = opts.threshold_num, opts.threshold_den
+    n = len(o) - 1
+    rep = S.join(coll, opts)
+    c = rep.counters
+    pairs = rep.pairs
+
+    # reference's own full-size run, where committed
+    g = golden_large(name)
+    if g is not None:
+        assert g["collection_sha256"] == hashlib.sha256(t.tobytes() + o.tobytes()).hexdigest(), \
+            "generated collection differs from the one the fixture was made on"
+        assert len(pairs) == g["pair_count"]
+        assert hashlib.sha256(pairs.tobytes()).hexdigest() == g["pairs_sha256"]
+        for k in COUNTERS:
+            assert c[k] == g["counters"][k], k
+        assert rep.saturated_records == g["saturated_records"]
+
+    # size-independent properties
+    assert c["candidates"] == D.window_pairs(o, p, q)
+    assert c["candidates"] == c["pruned_bitmap"] + c["verified"]
+    assert c["matched"] == len(pairs)
+    key = pairs["id_r"].astype(np.uint64) << np.uint64(32) | pairs["id_s"].astype(np.uint64)
+    assert (pairs["id_r"] < pairs["id_s"]).all()
+    assert (key[1:] > key[:-1]).all()
+    rng = np.random.default_rng(11)
+    sizes = np.diff(o.astype(np.int64))
+    for k in rng.choice(len(pairs), size=min(len(pairs), 3000), replace=False) if len(pairs) else []:
+        a, b, ov = int(pairs["id_r"][k]), int(pairs["id_s"][k]), int(pairs["overlap"][k])
+        assert ov == host_overlap(t, o, a, b)
+        assert ov * (p + q) >= p * (sizes[a] + sizes[b])  # Jaccard >= p/q in overlap space
+
+    # row-block samples vs the oracle on the same rows
+    for r0, r1 in blocks(n):
+        want, cnt = oracle.par_bitmap_join(t, o, p, q, True, opts.bitmap_method, opts.bitmap_bits,
+                                           opts.bitmap_hash, oracle.INT64_MAX,
+                                           opts.buffer_capacity, r0, r1)
+        blk = S.join_rows(coll, opts, r0, r1)
+        assert len(blk.pairs) == len(want) and (blk.pairs == want).all(), (r0, r1)
+        for k in COUNTERS:
+            assert blk.counters[k] == cnt[k], (r0, r1, k)
+        assert blk.saturated_records == cnt["saturated_records"], (r0, r1)
+        sel = (pairs["id_s"] >= r0) & (pairs["id_s"] < r1)
+        mine = np.sort(pairs[sel], order=["id_r", "id_s"])
+        assert len(mine) == len(want) and (mine == want).all(), (r0, r1)
+
+    # 2-way row partition adds up to the full run
+    bounds = S.partition_rows(coll, opts, 2)
+    parts = [S.join_rows(coll, opts, int(bounds[k]), int(bounds[k + 1])) for k in range(2)]
+    merged = np.concatenate([x.pairs for x in parts])
+    assert len(merged) == len(pairs)
+    mkey = merged["id_r"].astype(np.uint64) << np.uint64(32) | merged["id_s"].astype(np.uint64)
+    order = np.argsort(mkey, kind="stable")
+    assert (mkey[order] == key).all()
+    assert (merged["overlap"][order] == pairs["overlap"]).all()
+    for k in COUNTERS:
+        assert sum(x.counters[k] for x in parts) == c[k], k
+    assert sum(x.saturated_records for x in parts) == rep.saturated_records
+    print(f"{name}: n={n} window={c['candidates']:.3e} verified={c['verified']} matched={c['matched']} "
+          f"saturated={rep.saturated_records} total_s={rep.timings['total_s']:.3f}")
