@@ -15,7 +15,8 @@ import subprocess
 from . import capi
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libssjoin.so")
+# SSJB_LIB points experiments at another build of the same library (A/B timing)
+LIB_PATH = os.environ.get("SSJB_LIB") or os.path.join(PKG_DIR, "lib", "libssjoin.so")
 CSRC_DIR = os.path.join(PKG_DIR, "csrc")
 
 _lib = None

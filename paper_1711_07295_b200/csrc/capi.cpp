@@ -23,7 +23,7 @@ struct ssj_collection {
 };
 
 struct ssj_report {
-    std::vector<ssj_pair> pairs;
+    ssjb::PairVec pairs;  // same 16-byte layout as ssj_pair
     ssj_counters counters{};
     ssj_timings timings{};
     uint64_t saturated = 0;
@@ -133,15 +133,14 @@ int configured_devices() {
 void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double total_s) {
     size_t total = 0;
     for (auto& p : parts) total += p.pairs.size();
-    rep.pairs.resize(total);
     if (parts.size() == 1) {
-        std::memcpy(rep.pairs.data(), parts[0].pairs.data(), total * sizeof(ssj_pair));
+        rep.pairs = std::move(parts[0].pairs);
     } else {
         // shards own disjoint id_s ranges; k-way merge by (id_r, id_s)
-        std::vector<ssjb::PairOut> merged;
+        ssjb::PairVec merged;
         merged.reserve(total);
         for (auto& p : parts) {
-            std::vector<ssjb::PairOut> tmp;
+            ssjb::PairVec tmp;
             tmp.reserve(merged.size() + p.pairs.size());
             std::merge(merged.begin(), merged.end(), p.pairs.begin(), p.pairs.end(), std::back_inserter(tmp),
                        [](const ssjb::PairOut& x, const ssjb::PairOut& y) {
@@ -149,7 +148,7 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
                        });
             merged.swap(tmp);
         }
-        std::memcpy(rep.pairs.data(), merged.data(), total * sizeof(ssj_pair));
+        rep.pairs = std::move(merged);
     }
     ssj_counters& c = rep.counters;
     std::memset(&c, 0, sizeof c);
@@ -359,7 +358,9 @@ SSJB_API ssj_status ssj_resolve_bitmap(const ssj_collection* coll, const ssj_joi
 }
 
 SSJB_API size_t ssj_report_pair_count(const ssj_report* report) { return report ? report->pairs.size() : 0; }
-SSJB_API const ssj_pair* ssj_report_pairs(const ssj_report* report) { return report ? report->pairs.data() : nullptr; }
+SSJB_API const ssj_pair* ssj_report_pairs(const ssj_report* report) {
+    return report ? reinterpret_cast<const ssj_pair*>(report->pairs.data()) : nullptr;
+}
 SSJB_API void ssj_report_counters(const ssj_report* report, ssj_counters* out) {
     if (report == nullptr || out == nullptr) return;
     *out = report->counters;

@@ -12,11 +12,13 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
 #include "kernels.cuh"
 #include "filter_tc.cuh"
+#include "filter_tc2.cuh"
 
 namespace ssjb {
 
@@ -125,9 +127,10 @@ struct SketchSet {
     int method = -1, width = 0, hash = 0, words2 = 0;
     uint64_t* bits = nullptr;
     uint64_t* bits2 = nullptr;
-    // expanded tcgen05 operand arrays (A, B) per variant: 0 int8, 1 int8 + level-2, 2 fp4
-    uint8_t* opA[3] = {nullptr, nullptr, nullptr};
-    uint8_t* opB[3] = {nullptr, nullptr, nullptr};
+    // expanded tcgen05 operand arrays (A, B) per variant: 0 int8, 1 int8 + level-2,
+    // 2 fp4, 3 int8 without the size chunk (CTA-pair kernel)
+    uint8_t* opA[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint8_t* opB[4] = {nullptr, nullptr, nullptr, nullptr};
     bool owned = false;  // cudaMalloc'd (persistent) rather than arena memory
     ~SketchSet() {
         if (!owned) return;
@@ -136,7 +139,7 @@ struct SketchSet {
         cudaSetDevice(device);
         cudaFree(bits);
         cudaFree(bits2);
-        for (int v = 0; v < 3; ++v) {
+        for (int v = 0; v < 4; ++v) {
             cudaFree(opA[v]);
             cudaFree(opB[v]);
         }
@@ -151,6 +154,7 @@ struct DeviceReplica {
     uint64_t* offsets = nullptr;
     uint32_t* sizes = nullptr;
     size_t n = 0;
+    uint64_t tokens_total = 0;
     uint64_t bytes = 0;
     cudaStream_t stream = nullptr;  // set for per-join replicas: stream-ordered alloc/free
     std::shared_ptr<SketchSet> sketches;  // resident replicas only
@@ -210,6 +214,7 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     }
     rep->device = device;
     rep->n = n;
+    rep->tokens_total = c.tokens.size();
     uint64_t tok_h2d = 0;
     if (narrow_tokens(c)) {
         // 16-bit upload, widened on the device
@@ -359,11 +364,26 @@ TcKernel tc_select(int words, bool l2gemm, bool fp4) {
     throw DeviceError("no tensor-core filter instantiation for this width");
 }
 
+// CTA-pair int8 filter (filter_tc2.cuh): level-1 width b = 64 * words <= 128.
+template <int KA, int NS>
+TcKernel tc2_kernel() {
+    using L = dev::Tc2Layout<KA, NS>;
+    return TcKernel{dev::filter_tc2_kernel<KA, NS>, L::kBytes, L::kThreads};
+}
+
+TcKernel tc2_select(int words) {
+    switch (words) {
+        case 1: return tc2_kernel<96, 8>();
+        case 2: return tc2_kernel<160, 6>();
+    }
+    throw DeviceError("no CTA-pair filter instantiation for this width");
+}
+
 size_t operand_bytes(int words, bool fp4) { return fp4 ? 32 * words + 32 : 64 * words + 32; }
 
 // Operand row bytes of a variant: level 1 | level 2 (int8, 256-bit sketch) | 16-byte size chunk.
 size_t operand_row(int words, int variant) {
-    return operand_bytes(words, variant == 2) + (variant == 1 ? 64 * 4 + 32 : 0) + 16;
+    return operand_bytes(words, variant == 2) + (variant == 1 ? 64 * 4 + 32 : 0) + (variant == 3 ? 0 : 16);
 }
 
 void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int words2, const uint32_t* sizes,
@@ -380,7 +400,8 @@ void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int w
     E.fp4 = variant == 2 ? 1 : 0;
     E.K1 = static_cast<int>(operand_bytes(words, variant == 2));
     E.K2 = variant == 1 ? 64 * words2 + 32 : 0;
-    const int kct = (E.K1 + E.K2) / 16 + 1;
+    E.with_size = variant == 3 ? 0 : 1;
+    const int kct = (E.K1 + E.K2) / 16 + E.with_size;
     const uint64_t threads = static_cast<uint64_t>(rows) * kct;
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
     ++launches;
@@ -406,6 +427,66 @@ void launch_build(const DeviceReplica& rep, uint64_t* bits, Method method, int w
     CK(cudaGetLastError());
 }
 
+using BuildFn2 = void (*)(dev::BuildParams2);
+
+// Set/Xor sketches (and the level-2 Xor sketch in the same token pass) with
+// several lanes per record; null when the shape has no instantiation.
+BuildFn2 build_sub_fn(int words, int words2) {
+#define SSJB_SUB(W)                                      \
+    case W:                                              \
+        switch (words2) {                                \
+            case 0: return dev::build_sketches_sub<W, 0>; \
+            case 4: return dev::build_sketches_sub<W, 4>; \
+            case 8: return dev::build_sketches_sub<W, 8>; \
+        }                                                \
+        break;
+    switch (words) {
+        SSJB_SUB(1)
+        SSJB_SUB(2)
+        SSJB_SUB(3)
+        SSJB_SUB(4)
+        SSJB_SUB(5)
+        SSJB_SUB(6)
+        SSJB_SUB(7)
+        SSJB_SUB(8)
+    }
+#undef SSJB_SUB
+    return nullptr;
+}
+
+// Level-1 Set/Xor sketch (+ level-2 Xor sketch when bits2) in one launch.
+// Returns false when the method/width needs the one-thread-per-record kernel.
+bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2, Method method, int width,
+                      int width2, int hash, cudaStream_t s, uint64_t& launches) {
+    if (method != Method::Set && method != Method::Xor) return false;
+    BuildFn2 fn = build_sub_fn(width / 64, bits2 ? width2 / 64 : 0);
+    if (!fn) return false;
+    if (rep.n == 0) return true;
+    dev::BuildParams2 P{};
+    P.tokens = rep.tokens;
+    P.offsets = rep.offsets;
+    P.bits = bits;
+    P.bits2 = bits2;
+    P.n = static_cast<uint32_t>(rep.n);
+    P.width = static_cast<uint32_t>(width);
+    P.width2 = static_cast<uint32_t>(width2);
+    P.method = method == Method::Set ? 0 : 1;
+    P.hash_mult = hash == 1 ? 1 : 0;
+    P.pow2 = (width & (width - 1)) == 0;
+    P.pow2_2 = (width2 & (width2 - 1)) == 0;
+    // about 8 tokens per lane: lanes per record = next power of two of mean/8
+    const double mean = static_cast<double>(rep.tokens_total) / static_cast<double>(rep.n);
+    int lg = 0;
+    while (lg < 5 && (1 << lg) * 8.0 < mean) ++lg;
+    P.lpr_log2 = lg;
+    const uint64_t threads = static_cast<uint64_t>(rep.n) << lg;
+    const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+    fn<<<grid, 256, 0, s>>>(P);
+    ++launches;
+    CK(cudaGetLastError());
+    return true;
+}
+
 // Sort keys/vals in place by key bits [0, 32+bits) skipping constant bytes;
 // returns the buffer holding the result (a or b).
 struct SortBufs {
@@ -419,6 +500,59 @@ struct SortBufs {
 };
 
 constexpr uint32_t kSmallSort = 4096;
+
+// Sorted (j << 32 | i, overlap) results -> ssj_pair records (id_r, id_s, i64).
+__global__ void pack_pairs(const unsigned long long* keys, const uint32_t* ov, PairOut* out, uint64_t count) {
+    const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (k >= count) return;
+    const unsigned long long key = keys[k];
+    out[k] = PairOut{static_cast<uint32_t>(key >> 32), static_cast<uint32_t>(key & 0xFFFFFFFFu),
+                     static_cast<int64_t>(ov[k])};
+}
+
+// Device -> pageable host copy of a large buffer: double-buffered through
+// pinned staging chunks, the host side copied out by several threads while the
+// next chunk is in flight (a plain cudaMemcpy to pageable memory runs at a
+// fraction of the link rate).
+void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t kChunk = size_t(64) << 20;
+    if (bytes <= kChunk) {
+        if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    static thread_local uint8_t* stage[2] = {nullptr, nullptr};
+    static thread_local cudaEvent_t ev[2];
+    if (!stage[0]) {
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk));
+            CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+        }
+    }
+    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t k) {
+        const size_t off = k * kChunk, len = std::min(kChunk, bytes - off);
+        CK(cudaMemcpyAsync(stage[k & 1], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[k & 1], s));
+    };
+    const unsigned nthreads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    issue(0);
+    for (size_t k = 0; k < nchunks; ++k) {
+        if (k + 1 < nchunks) issue(k + 1);
+        CK(cudaEventSynchronize(ev[k & 1]));
+        const size_t off = k * kChunk, len = std::min(kChunk, bytes - off);
+        const size_t piece = (len + nthreads - 1) / nthreads;
+        const uint8_t* buf = stage[k & 1];  // (thread_local: resolve here, not in the workers)
+        uint8_t* out = static_cast<uint8_t*>(dst) + off;
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < nthreads; ++t) {
+            const size_t a = std::min(len, t * piece), b = std::min(len, a + piece);
+            if (a < b) th.emplace_back([=]() { std::memcpy(out + a, buf + a, b - a); });
+        }
+        std::memcpy(out, buf, std::min(len, piece));
+        for (auto& x : th) x.join();
+    }
+}
 
 // Single-CTA bitonic sort of up to 4096 (key, value) pairs; the count comes
 // from device memory so it runs in the same stream-ordered chain as the
@@ -501,21 +635,23 @@ bool sort_results(SortBufs& B, unsigned long long n, int idbits, cudaStream_t s,
 }
 
 struct Tiling {
+    uint32_t tile_rows = dev::kRowTile;  // rows per work item
     uint32_t ntiles = 0;
     std::vector<uint64_t> item_base;  // ntiles + 1
     std::vector<uint32_t> col_lo;     // ntiles
     std::vector<uint32_t> item_tile;  // tile of each work item
 };
 
-Tiling make_tiling(const Collection& c, const JoinPlan& plan) {
+Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows) {
     Tiling t;
+    t.tile_rows = tile_rows;
     const size_t rows = plan.row_end - plan.row_begin;
-    t.ntiles = static_cast<uint32_t>((rows + dev::kRowTile - 1) / dev::kRowTile);
+    t.ntiles = static_cast<uint32_t>((rows + tile_rows - 1) / tile_rows);
     t.item_base.assign(t.ntiles + 1, 0);
     t.col_lo.assign(t.ntiles, 0);
     for (uint32_t k = 0; k < t.ntiles; ++k) {
-        const size_t r0 = plan.row_begin + static_cast<size_t>(k) * dev::kRowTile;
-        const size_t rl = std::min(r0 + dev::kRowTile, plan.row_end) - 1;  // last row
+        const size_t r0 = plan.row_begin + static_cast<size_t>(k) * tile_rows;
+        const size_t rl = std::min<size_t>(r0 + tile_rows, plan.row_end) - 1;  // last row
         const uint32_t j0 = window_start_of(c, plan, r0);                   // smallest j0 of the tile
         const uint32_t lo = j0 & ~31u;
         t.col_lo[k] = lo;
@@ -583,7 +719,8 @@ void engine_build_bitmaps(const Collection& c, Method method, int width, int has
         Arena A(s);
         const int W = width / 64;
         uint64_t* bits = A.alloc<uint64_t>((c.size() + kPadRows) * W);
-        launch_build(*rep, bits, method, width, hash, s, launches);
+        if (!launch_build_sub(*rep, bits, nullptr, method, width, 0, hash, s, launches))
+            launch_build(*rep, bits, method, width, hash, s, launches);
         if (c.size())
             CK(cudaMemcpyAsync(out_host, bits, c.size() * W * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -622,19 +759,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_wstart = A.alloc<uint32_t>(plan.window_start.size());
     std::vector<int32_t> maxham(plan.minov.size());
     for (size_t S = 0; S < maxham.size(); ++S) maxham[S] = static_cast<int32_t>(S) - 2 * plan.minov[S];
-    Tiling tl = make_tiling(c, plan);
-    uint64_t* d_item_base = A.alloc<uint64_t>(tl.item_base.size());
-    uint32_t* d_col_lo = A.alloc<uint32_t>(tl.col_lo.size());
-    uint32_t* d_item_tile = A.alloc<uint32_t>(tl.item_tile.size());
     CK(cudaMemcpyAsync(d_maxham, maxham.data(), maxham.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_minov, plan.minov.data(), plan.minov.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(d_wstart, plan.window_start.data(), plan.window_start.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_item_base, tl.item_base.data(), tl.item_base.size() * 8, cudaMemcpyHostToDevice, s));
-    if (tl.ntiles) CK(cudaMemcpyAsync(d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4, cudaMemcpyHostToDevice, s));
-    if (!tl.item_tile.empty())
-        CK(cudaMemcpyAsync(d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4, cudaMemcpyHostToDevice, s));
-    st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4 + tl.item_base.size() * 8 + tl.col_lo.size() * 4;
-    cudaEvent_t e_up = T.mark();
+    st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4;
 
     // K1: sketches (+ level-2 Xor sketches), reused from a resident replica's cache
     const int W2 = enabled ? level2_words(W) : 0;
@@ -643,8 +771,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     const bool tc_ok = enabled && W <= 4 && plan.row_begin % 8 == 0;
     const bool use_tc = tc_ok && !(fenv && std::string(fenv) == "popc");
     bool l2gemm = false;
+    bool l2_auto = false;  // may switch to the level-2 GEMM when level-1 survivors overflow
     if (use_tc && W <= 2 && W2 == 4) {
         const char* genv = std::getenv("SSJB_L2GEMM");
+        l2_auto = !(genv && *genv);
         if (genv && *genv) {
             l2gemm = std::atoi(genv) != 0;
         } else {
@@ -656,7 +786,34 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
     }
     const char* kenv = std::getenv("SSJB_TC_KIND");
-    const bool fp4 = use_tc && !l2gemm && kenv && std::string(kenv) == "fp4";  // int8 by default
+    // operand kind: fp4 (packed e2m1) halves the operand bytes and doubles the
+    // MMA rate per element, which wins for b >= 192 (C2 b=256 sweep: 7.96 vs
+    // 10.0 ms); at b <= 128 the int8 kernel's 256-column tiles are faster
+    // (C2 b=128: 9.0 vs 22.5 ms).  SSJB_TC_KIND=i8|fp4 overrides.
+    const bool fp4 = use_tc && !l2gemm &&
+                     (kenv && *kenv ? std::string(kenv) == "fp4" : W >= 3);
+    // int8 level-1-only filter on a CTA pair (M = 256): experimental, SSJB_TC2=1
+    const bool use_tc2 = use_tc && !l2gemm && !fp4 && W <= 2 && env_u64("SSJB_TC2", 0) != 0;
+
+    // work items: (row tile, 4096-column chunk); the pair kernel takes 256-row tiles
+    Tiling tl;
+    uint64_t* d_item_base = nullptr;
+    uint32_t* d_col_lo = nullptr;
+    uint32_t* d_item_tile = nullptr;
+    auto set_tiling = [&](uint32_t tile_rows) {
+        tl = make_tiling(c, plan, tile_rows);
+        d_item_base = A.alloc<uint64_t>(tl.item_base.size());
+        d_col_lo = A.alloc<uint32_t>(tl.col_lo.size());
+        d_item_tile = A.alloc<uint32_t>(tl.item_tile.size());
+        CK(cudaMemcpyAsync(d_item_base, tl.item_base.data(), tl.item_base.size() * 8, cudaMemcpyHostToDevice, s));
+        if (tl.ntiles)
+            CK(cudaMemcpyAsync(d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4, cudaMemcpyHostToDevice, s));
+        if (!tl.item_tile.empty())
+            CK(cudaMemcpyAsync(d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4, cudaMemcpyHostToDevice, s));
+        st.h2d_bytes += tl.item_base.size() * 8 + tl.col_lo.size() * 4 + tl.item_tile.size() * 4;
+    };
+    set_tiling(use_tc2 ? 2 * dev::kRowTile : dev::kRowTile);
+    cudaEvent_t e_up = T.mark();
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
     const bool resident = rep->stream == nullptr;
     std::shared_ptr<SketchSet> sk;
@@ -685,16 +842,22 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         fresh->owned = resident;
         fresh->bits = static_cast<uint64_t*>(get((n + kPadRows + 8) * W * 8));
         CK(cudaMemsetAsync(fresh->bits + n * W, 0, (kPadRows + 8) * W * 8, s));
-        launch_build(*rep, fresh->bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
         if (W2) {
             fresh->bits2 = static_cast<uint64_t*>(get((n + kPadRows + 8) * W2 * 8));
             CK(cudaMemsetAsync(fresh->bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
-            launch_build(*rep, fresh->bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
+        }
+        // one token pass for both sketches where the sub-warp builder applies
+        if (!launch_build_sub(*rep, fresh->bits, fresh->bits2, plan.bitmap.method, width, 64 * W2,
+                              plan.bitmap.hash, s, st.launches)) {
+            launch_build(*rep, fresh->bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
+            if (W2 && !launch_build_sub(*rep, fresh->bits2, nullptr, Method::Xor, 64 * W2, 0, plan.bitmap.hash, s,
+                                        st.launches))
+                launch_build(*rep, fresh->bits2, Method::Xor, 64 * W2, plan.bitmap.hash, s, st.launches);
         }
         sk = fresh;
         built = true;
     }
-    const int variant = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : 0));
+    const int variant = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : (use_tc2 ? 3 : 0)));
     if (variant >= 0 && !sk->opA[variant]) {
         const size_t rowb = operand_row(W, variant);
         sk->opA[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
@@ -717,16 +880,26 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     cudaEvent_t e_build = T.mark();
 
     // buffers
-    const uint64_t surv_cap = std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << 27), 1u << 20);
+    // buffer sizing: survivors (8 B) and result sort buffers (24 B); a batch's
+    // results must fit the result buffer, so res_cap >= surv_cap.  With the HBM
+    // of a B200 free, larger buffers mean fewer filter batches / result runs.
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t big = free_b >= (size_t(64) << 30) ? 1 : 0;
+    const uint64_t surv_cap =
+        std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
     const uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
     uint2* d_surv = A.alloc<uint2>(surv_cap);
     uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
     // per-(item,row) survivor counts let the saturation rescan touch one chunk per row
-    const uint64_t n_items = tl.item_base.back();
-    const bool keep_item_counts = !naive && n_items * dev::kRowTile * 4 <= (uint64_t(1) << 30);
-    uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * dev::kRowTile) : nullptr;
+    uint64_t n_items = tl.item_base.back();
+    const uint64_t ic_bytes = n_items * tl.tile_rows * 4;
+    const bool keep_item_counts =
+        !naive && (ic_bytes <= (uint64_t(1) << 30) ||
+                   (ic_bytes <= (uint64_t(16) << 30) && static_cast<double>(ic_bytes) <= 0.3 * double(free_b)));
+    uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * tl.tile_rows) : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
     SB.ka = A.alloc<unsigned long long>(res_cap);
@@ -773,8 +946,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 
     dev::TcParams TP{};
     TcKernel tck{nullptr, 0};
+    bool tc2_active = use_tc2;
     if (use_tc) {
-        tck = tc_select(W, l2gemm, fp4);
+        tck = use_tc2 ? tc2_select(W) : tc_select(W, l2gemm, fp4);
         CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
         TP.opA = d_opA;
         TP.opB = d_opB;
@@ -814,15 +988,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     VP.res_ov = SB.va;
     VP.res_cap = res_cap;
     VP.ctl = d_ctl;
+    if (W2 && !naive) {  // level-2 re-test of level-1 survivors before the merge
+        VP.bits2 = d_bits2;
+        VP.maxham = d_maxham;
+        VP.w2 = W2;
+    }
 
-    std::vector<std::vector<PairOut>> runs;
+    std::vector<PairVec> runs;
     uint64_t res_count = 0;
     int idbits = 1;
     while ((uint64_t(1) << idbits) < n + 1) ++idbits;
     SB.count = &d_ctl->results;
 
     auto take_run = [&](const unsigned long long* keys, const uint32_t* ov, uint64_t count) {
-        std::vector<PairOut> run(count);
+        PairVec run(count);
         for (uint64_t k = 0; k < count; ++k)
             run[k] = PairOut{static_cast<uint32_t>(keys[k] >> 32), static_cast<uint32_t>(keys[k] & 0xFFFFFFFFu),
                              static_cast<int64_t>(ov[k])};
@@ -830,31 +1009,35 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     };
 
     auto flush_results = [&](uint64_t count) {
-        // K4 on the current result buffer, then download one sorted run
+        // K4 on the current result buffer, packed to ssj_pair records on the
+        // device, then one (staged) download of the sorted run
         cudaEvent_t a = T.mark();
         bool inb = sort_results(SB, count, idbits, s, st.launches);
-        cudaEvent_t b = T.mark();
-        std::vector<unsigned long long> keys(count);
-        std::vector<uint32_t> ov(count);
+        PairOut* packed = count ? A.alloc<PairOut>(count) : nullptr;
         if (count) {
-            CK(cudaMemcpyAsync(keys.data(), inb ? SB.kb : SB.ka, count * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaMemcpyAsync(ov.data(), inb ? SB.vb : SB.va, count * 4, cudaMemcpyDeviceToHost, s));
+            pack_pairs<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(inb ? SB.kb : SB.ka,
+                                                                              inb ? SB.vb : SB.va, packed, count);
+            ++st.launches;
+            CK(cudaGetLastError());
         }
+        cudaEvent_t b = T.mark();
+        PairVec run(count);
+        d2h_staged(run.data(), packed, count * sizeof(PairOut), s);
         cudaEvent_t d = T.mark();
         CK(cudaStreamSynchronize(s));
-        st.d2h_bytes += count * 12;
+        st.d2h_bytes += count * sizeof(PairOut);
         st.ms_sort += Timer::ms(a, b);
         st.ms_download += Timer::ms(b, d);
-        take_run(keys.data(), ov.data(), count);
+        runs.push_back(std::move(run));
         CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
     };
 
-    const uint64_t total_items = tl.item_base.back();
+    uint64_t total_items = tl.item_base.back();
     auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb) {
         CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
         CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
         if (d_item_counts && ie > ib)
-            CK(cudaMemsetAsync(d_item_counts + ib * dev::kRowTile, 0, (ie - ib) * dev::kRowTile * 4, s));
+            CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (ie - ib) * tl.tile_rows * 4, s));
         if (ie <= ib) return;
         FP.item_begin = ib;
         FP.item_end = ie;
@@ -863,8 +1046,14 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             TP.item_begin = ib;
             TP.item_end = ie;
             TP.tile_begin = tb;
-            const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms));
-            tck.fn<<<static_cast<unsigned>(grid), tck.threads, tck.smem, s>>>(TP);
+            if (tc2_active) {
+                // one CTA pair per TPC, the pair sharing each work item
+                const uint64_t pairs = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms / 2));
+                tck.fn<<<static_cast<unsigned>(2 * pairs), tck.threads, tck.smem, s>>>(TP);
+            } else {
+                const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms));
+                tck.fn<<<static_cast<unsigned>(grid), tck.threads, tck.smem, s>>>(TP);
+            }
         } else {
             const uint64_t grid = std::min<uint64_t>(ie - ib, static_cast<uint64_t>(sms) * per_sm);
             ffn<<<static_cast<unsigned>(grid), dev::kRowTile, fsmem, s>>>(FP);
@@ -876,7 +1065,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         // survivor count read on the device: no host round trip between K2 and K3
         VP.count_ptr = &d_ctl->survivors;
         VP.count_cap = surv_cap;
-        dev::verify_pairs<<<static_cast<unsigned>(sms) * 8, 256, 0, s>>>(VP);
+        const unsigned vgrid = static_cast<unsigned>(sms) * 8;
+        if (VP.w2 == 4) dev::verify_pairs<4><<<vgrid, 256, 0, s>>>(VP);
+        else if (VP.w2 == 8) dev::verify_pairs<8><<<vgrid, 256, 0, s>>>(VP);
+        else dev::verify_pairs<0><<<vgrid, 256, 0, s>>>(VP);
         ++st.launches;
         CK(cudaGetLastError());
     };
@@ -890,6 +1082,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.wstart = d_wstart;
             RP.rowcnt = d_rowcnt;
             RP.item_counts = d_item_counts;
+            RP.tile_rows = tl.tile_rows;
             RP.item_base = d_item_base;
             RP.tile_col_lo = d_col_lo;
             RP.jstar = d_jstar;
@@ -963,6 +1156,37 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             // survivor buffer overflow: discard and redo in batches
             CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4ull, s));
             CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
+            if (l2_auto && use_tc && !l2gemm && !fp4) {
+                // level-1 survivors overflow: the b-bit sketch is saturated for this
+                // collection, so re-test level 1 and level 2 together in the GEMM and
+                // emit only level-2 survivors (operands built for this join only)
+                const size_t rowb = operand_row(W, 1);
+                uint8_t* a1 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * rowb);
+                uint8_t* b1 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * rowb);
+                launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, a1, b1, n_pad, 1, s, st.launches);
+                l2gemm = true;
+                if (tc2_active) {
+                    // the single-CTA kernels take 128-row work items
+                    tc2_active = false;
+                    set_tiling(dev::kRowTile);
+                    total_items = n_items = tl.item_base.back();
+                    TP.item_base = d_item_base;
+                    TP.item_tile = d_item_tile;
+                    TP.tile_col_lo = d_col_lo;
+                    TP.ntiles = tl.ntiles;
+                    if (d_item_counts && n_items * tl.tile_rows * 4 <= ic_bytes) {
+                        TP.item_counts = d_item_counts;  // same buffer, fewer/equal bytes
+                    } else {
+                        d_item_counts = nullptr;
+                        TP.item_counts = nullptr;
+                    }
+                }
+                tck = tc_select(W, true, false);
+                CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
+                TP.opA = a1;
+                TP.opB = b1;
+                st.filter_kernel = 2;
+            }
         }
     }
 
@@ -977,7 +1201,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                                                       tl.item_base.begin() - 1);
             const uint32_t te = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ie - 1) -
                                                       tl.item_base.begin() - 1);
-            const uint32_t rb = tb * dev::kRowTile, re = std::min<uint32_t>(rows, (te + 1) * dev::kRowTile);
+            const uint32_t rb = tb * tl.tile_rows, re = std::min<uint32_t>(rows, (te + 1) * tl.tile_rows);
             CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
             cudaEvent_t a = T.mark();
             launch_filter(ib, ie, tb);
@@ -1027,9 +1251,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     if (runs.size() == 1) {
         out.pairs = std::move(runs[0]);
     } else {
-        std::vector<PairOut> merged;
+        PairVec merged;
         for (auto& r : runs) {
-            std::vector<PairOut> tmp(merged.size() + r.size());
+            PairVec tmp(merged.size() + r.size());
             std::merge(merged.begin(), merged.end(), r.begin(), r.end(), tmp.begin(),
                        [](const PairOut& x, const PairOut& y) {
                            return x.id_r != y.id_r ? x.id_r < y.id_r : x.id_s < y.id_s;

@@ -8,6 +8,8 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "host_core.hpp"
@@ -21,6 +23,28 @@ struct PairOut {  // layout of ssj_pair (reference include/ssjoin.h:125-129)
 };
 static_assert(sizeof(PairOut) == 16, "ssj_pair layout");
 
+// Allocator that leaves trivially-constructible elements uninitialised: result
+// vectors of 1e8+ pairs are filled by device copies, not zeroed first.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+using PairVec = std::vector<PairOut, DefaultInitAlloc<PairOut>>;
+
 struct EngineStats {
     uint64_t window_pairs = 0, survivors = 0, batches = 0, launches = 0;
     uint64_t h2d_bytes = 0, d2h_bytes = 0, verify_bytes = 0;
@@ -30,7 +54,7 @@ struct EngineStats {
 };
 
 struct EngineResult {
-    std::vector<PairOut> pairs;  // sorted by (id_r, id_s)
+    PairVec pairs;  // sorted by (id_r, id_s)
     uint64_t candidates = 0, bitmap_tested = 0, pruned_bitmap = 0, verified = 0, matched = 0;
     uint64_t saturated = 0;
     double index_s = 0, candidates_s = 0, verify_s = 0;

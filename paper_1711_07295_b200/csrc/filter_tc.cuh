@@ -158,6 +158,90 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 64 accumulator columns in one load: the low 16 bits of columns 2k, 2k+1 in
+// register k (tcgen05.ld .pack::16b).  Exact for the int8 filter: every
+// accumulator lies in [-2b, 2b] and b <= 256.
+__device__ __forceinline__ void tmem_ld64_pack16(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+          "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+          "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// max over 64 packed s16 accumulators > c (two independent VIMNMX3.S16x2 chains)
+__device__ __forceinline__ bool any_above16(const uint32_t (&d)[32], int c) {
+    uint32_t a = __vimax3_s16x2(d[0], d[1], d[2]);
+    uint32_t b = __vimax3_s16x2(d[3], d[4], d[5]);
+#pragma unroll
+    for (int k = 6; k < 30; k += 4) {
+        a = __vimax3_s16x2(a, d[k], d[k + 1]);
+        b = __vimax3_s16x2(b, d[k + 2], d[k + 3]);
+    }
+    a = __vimax3_s16x2(a, b, __vimax3_s16x2(d[30], d[31], d[31]));
+    const int hi = static_cast<int>(a) >> 16;
+    const int lo = static_cast<int>(static_cast<int16_t>(a & 0xFFFFu));
+    return max(hi, lo) > c;
+}
+
+// 32 accumulator columns packed into 16 registers, no wait (pair with tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld32_pack16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// max over 32 packed s16 accumulators > c
+__device__ __forceinline__ bool any_above16_32(const uint32_t (&d)[16], int c) {
+    uint32_t a = __vimax3_s16x2(d[0], d[1], d[2]);
+    uint32_t b = __vimax3_s16x2(d[3], d[4], d[5]);
+    a = __vimax3_s16x2(a, d[6], d[7]);
+    b = __vimax3_s16x2(b, d[8], d[9]);
+    a = __vimax3_s16x2(a, d[10], d[11]);
+    b = __vimax3_s16x2(b, d[12], d[13]);
+    a = __vimax3_s16x2(a, b, __vimax3_s16x2(d[14], d[15], d[15]));
+    const int hi = static_cast<int>(a) >> 16;
+    const int lo = static_cast<int>(static_cast<int16_t>(a & 0xFFFFu));
+    return max(hi, lo) > c;
+}
+
+// survivor mask of 32 packed columns: bit k set iff accumulator k > c (c >= -32768)
+__device__ __forceinline__ uint32_t mask16_32(const uint32_t (&d)[16], int c) {
+    const uint32_t c2 = (static_cast<uint32_t>(c) & 0xFFFFu) * 0x10001u;
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t v = __vcmpgts2(d[k], c2);
+        x |= ((v & 1u) | ((v >> 30) & 2u)) << (2 * k);
+    }
+    return x;
+}
+
+// survivor masks of the two 32-column groups of a packed 64-column load:
+// bit k of m[g] = column 32g + k, set iff its accumulator > c (c >= -32768)
+__device__ __forceinline__ void masks16(const uint32_t (&d)[32], int c, uint32_t& m0, uint32_t& m1) {
+    const uint32_t c2 = (static_cast<uint32_t>(c) & 0xFFFFu) * 0x10001u;
+    uint32_t x0 = 0, x1 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t v0 = __vcmpgts2(d[k], c2);       // 0xFFFF per half that survives
+        const uint32_t v1 = __vcmpgts2(d[16 + k], c2);
+        x0 |= ((v0 & 1u) | ((v0 >> 30) & 2u)) << (2 * k);
+        x1 |= ((v1 & 1u) | ((v1 >> 30) & 2u)) << (2 * k);
+    }
+    m0 = x0;
+    m1 = x1;
+}
+
 // Survivor mask of 32 accumulator columns: column k survives iff
 // cim1_k - D_k < 0 (sign bit set).  Four independent funnel-shift chains
 // (8 columns each) keep the ALU pipe fed; the subtraction is an IMAD on the
@@ -510,7 +594,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 bypass = static_cast<int64_t>(si) > P.cutoff;
 #pragma unroll
                 for (int w = 0; w < L::kWords; ++w) pc += __popcll(P.bits[static_cast<uint64_t>(i) * L::kWords + w]);
-                if constexpr (W2 > 0) {
+                if constexpr (K2 > 0) {
 #pragma unroll
                     for (int w = 0; w < W2; ++w) mine2[w] = P.bits2[static_cast<uint64_t>(i) * W2 + w];
                 }
@@ -554,8 +638,119 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     cim1_2 = pc2 - T - 1;
                     cim1_key = cim1 < 0 ? INT_MIN : __float_as_int(static_cast<float>(cim1) + 0.5f);
                 }
+                // per-group tail: counts, level-2 check, emission (m = level-1 survivors)
+                auto finish = [&](int cl, uint32_t gbase, uint32_t m, bool uni) {
+                    cnt += __popc(m);
+                    if (!__any_sync(0xFFFFFFFFu, m != 0)) return;
+                    uint32_t e = m;
+                    if constexpr (K2 > 0) {
+                        uint32_t d2[32];
+                        int dummy2[32];
+                        tmem_ld32(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
+                        e = m & (uni ? survivors32<true, KIND>(d2, cim1_2, dummy2, P.neg1)
+                                     : survivors_mixed<KIND, L::kKCT>(d2, pc2, maxham, si, stage, cl));
+                    }
+                    // (without the level-2 GEMM, level-1 survivors are emitted and
+                    // verify_pairs re-tests them against the level-2 sketch first)
+                    if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
+                };
+                bool groups_done = (P.debug & 1) != 0;
+                if constexpr (KIND == kKindI8 && L::kColsPerWarp == 64) {
+                    // interior fast path: the warp's 64 columns in ONE packed TMEM
+                    // load (one load latency per tile instead of two)
+                    if (fast && !groups_done) {
+                        groups_done = true;
+                        uint32_t d[32];
+                        tmem_ld64_pack16(tmem_base + lane_base + as * NT + cw, d);
+                        const int c16 = max(cim1, -32768);
+                        if (__any_sync(0xFFFFFFFFu, bypass || any_above16(d, c16))) {
+                            uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
+                            if (!bypass) masks16(d, c16, m0, m1);
+                            finish(cw, wbase, m0, true);
+                            finish(cw + 32, wbase + 32, m1, true);
+                        }
+                    }
+                }
+                if constexpr (KIND == kKindI8 && K2 > 0) {
+                    // level-2 GEMM variant, interior fast path (one 32-column group per
+                    // warp): both accumulators as packed s16 in one load latency
+                    if (fast && !groups_done) {
+                        groups_done = true;
+                        uint32_t d[16], d2[16];
+                        tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cw, d);
+                        tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cw, d2);
+                        tmem_wait_ld();
+                        const int c16 = max(cim1, -32768);
+                        if (__any_sync(0xFFFFFFFFu, bypass || any_above16_32(d, c16))) {
+                            const uint32_t m = bypass ? 0xFFFFFFFFu : mask16_32(d, c16);
+                            cnt += __popc(m);
+                            if (__any_sync(0xFFFFFFFFu, m != 0)) {
+                                const uint32_t e = m & mask16_32(d2, max(cim1_2, -32768));
+                                if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, wbase, i, q, qlen, P, lane);
+                            }
+                        }
+                    }
+                }
+                if constexpr (KIND == kKindI8 && K2 == 0) {
+                    // int8 groups of 32 columns: level-1 accumulators
+                    // as packed s16 in one load latency.  Thresholds per run of equal
+                    // column size (sizes are sorted, so a group holds 1-3 runs): a
+                    // ballot over the lanes' column sizes gives each run's columns.
 #pragma unroll 1
-                for (int g = 0; g < ((P.debug & 1) ? 0 : L::kColsPerWarp / 32); ++g) {
+                    for (int g = 0; g < (groups_done ? 0 : L::kColsPerWarp / 32); ++g) {
+                        const int cl = cw + g * 32;
+                        const uint32_t gbase = wbase + g * 32;
+                        uint32_t rm = 0xFFFFFFFFu;
+                        if (!fast) {
+                            const int kl = static_cast<int>(lo_i) - static_cast<int>(gbase);
+                            const int kh = static_cast<int>(hi_i) - static_cast<int>(gbase);
+                            rm = low_mask(kh) & ~low_mask(kl);
+                            if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
+                        }
+                        uint32_t d[16], d2[16];
+                        tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cl, d);
+                        if constexpr (K2 > 0) tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
+                        const uint32_t colsz = fast ? 0u : stage_size<L::kKCT>(stage, cl + lane);
+                        tmem_wait_ld();
+                        // lowest threshold over the group's size runs (pre-test)
+                        int cmin = cim1;
+                        if (!fast) {
+                            cmin = INT_MAX;
+                            uint32_t rem = 0xFFFFFFFFu;
+                            while (rem) {
+                                const uint32_t sz = __shfl_sync(0xFFFFFFFFu, colsz, __ffs(rem) - 1);
+                                rem &= ~__ballot_sync(0xFFFFFFFFu, colsz == sz);
+                                cmin = min(cmin, pc - maxham[si + sz] - 1);
+                            }
+                        }
+                        if (!__any_sync(0xFFFFFFFFu, bypass || (rm != 0 && any_above16_32(d, max(cmin, -32768)))))
+                            continue;
+                        uint32_t m = 0xFFFFFFFFu, e2 = 0xFFFFFFFFu;
+                        if (fast) {
+                            if (!bypass) m = mask16_32(d, max(cim1, -32768));
+                            if constexpr (K2 > 0) e2 = mask16_32(d2, max(cim1_2, -32768));
+                        } else {
+                            uint32_t mm = 0, ee = 0, rem = 0xFFFFFFFFu;
+                            while (rem) {
+                                const uint32_t sz = __shfl_sync(0xFFFFFFFFu, colsz, __ffs(rem) - 1);
+                                const uint32_t sel = __ballot_sync(0xFFFFFFFFu, colsz == sz);
+                                rem &= ~sel;
+                                const int T = maxham[si + sz];
+                                mm |= mask16_32(d, max(pc - T - 1, -32768)) & sel;
+                                if constexpr (K2 > 0) ee |= mask16_32(d2, max(pc2 - T - 1, -32768)) & sel;
+                            }
+                            if (!bypass) m = mm;
+                            if constexpr (K2 > 0) e2 = ee;
+                        }
+                        m &= rm;
+                        cnt += __popc(m);
+                        const uint32_t e = m & e2;
+                        if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
+                    }
+                    groups_done = true;
+                }
+#pragma unroll 1
+                for (int g = 0; g < (groups_done ? 0 : L::kColsPerWarp / 32); ++g) {
                     const int cl = cw + g * 32;  // column within the tile
                     const uint32_t gbase = wbase + g * 32;
                     uint32_t d[32];
@@ -590,27 +785,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         }
                         m = bypass ? rm : (m & rm);
                     }
-                    cnt += __popc(m);
-                    if (!__any_sync(0xFFFFFFFFu, m != 0)) continue;
-                    uint32_t e = m;
-                    if constexpr (K2 > 0) {
-                        tmem_ld32(tmem_base + lane_base + L::kL2Col + as * NT + cl, d);
-                        e = m & (uni ? survivors32<true, KIND>(d, cim1_2, dummy, P.neg1)
-                                     : survivors_mixed<KIND, L::kKCT>(d, pc2, maxham, si, stage, cl));
-                    } else if constexpr (W2 > 0) {
-                        uint32_t mm = m;
-                        e = 0;
-                        while (mm) {
-                            const int k = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            const uint64_t* col = P.bits2 + static_cast<uint64_t>(gbase + k) * W2;
-                            int h = 0;
-#pragma unroll
-                            for (int w = 0; w < W2; ++w) h += __popcll(mine2[w] ^ __ldg(col + w));
-                            e |= (h <= maxham[si + stage_size<L::kKCT>(stage, cl + k)] ? 1u : 0u) << k;
-                        }
-                    }
-                    if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
+                    finish(cl, gbase, m, uni);
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
@@ -658,6 +833,7 @@ struct ExpandParams {
     int K1;                 // level-1 bytes per row
     int K2;                 // level-2 bytes per row (0: none)
     int fp4;                // level-1 encoding
+    int with_size;          // append the 16-byte size chunk (single-CTA kernels)
 };
 
 __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -4, -6
@@ -720,7 +896,7 @@ __device__ __forceinline__ void expand_f4(const uint64_t* row, int words, int c,
 }
 
 __global__ void expand_operands(ExpandParams P) {
-    const int KCT = (P.K1 + P.K2) / 16 + 1;
+    const int KCT = (P.K1 + P.K2) / 16 + P.with_size;
     const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<uint64_t>(P.rows) * KCT) return;
     const uint32_t r = static_cast<uint32_t>(idx / KCT);

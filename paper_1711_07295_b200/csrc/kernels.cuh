@@ -161,6 +161,80 @@ __global__ void __launch_bounds__(kBuildRecs) build_sketches(BuildParams P) {
     }
 }
 
+// Set / Xor sketches with LPR lanes per record (LPR = 1..32, a power of two):
+// lane k of a record's group folds tokens k, k+LPR, ... into register
+// sketches, then the group combines them with shuffles (OR for Set, XOR for
+// Xor -- both order-independent, reference src/bitmap.cpp:70-81).  Token loads
+// are coalesced across the group.  With W2 > 0 the same token pass also
+// builds the level-2 Xor sketch (64*W2 bits) into bits2.
+struct BuildParams2 {
+    const uint32_t* tokens;
+    const uint64_t* offsets;
+    uint64_t* bits;        // n * W words
+    uint64_t* bits2;       // n * W2 words (W2 > 0)
+    uint32_t n;
+    uint32_t width, width2;
+    int method;            // 0 Set, 1 Xor
+    int hash_mult;
+    int pow2, pow2_2;
+    int lpr_log2;          // log2(lanes per record)
+};
+
+template <int W, int W2>
+__global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
+    const int lpr = 1 << P.lpr_log2;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t r = gtid >> P.lpr_log2;
+    const int sub = static_cast<int>(gtid & (lpr - 1));
+    const bool live = r < P.n;
+    uint64_t row[W], row2[W2 > 0 ? W2 : 1];
+#pragma unroll
+    for (int w = 0; w < W; ++w) row[w] = 0;
+#pragma unroll
+    for (int w = 0; w < (W2 > 0 ? W2 : 1); ++w) row2[w] = 0;
+    if (live) {
+        const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
+        for (uint64_t k = b + sub; k < e; k += lpr) {
+            const uint32_t t = __ldg(P.tokens + k);
+            const uint32_t h = hash_token(t, P.width, P.hash_mult, P.pow2);
+            const uint64_t bit = 1ull << (h & 63);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint64_t m = (h >> 6) == uint32_t(w) ? bit : 0ull;
+                row[w] = P.method == 0 ? (row[w] | m) : (row[w] ^ m);
+            }
+            if constexpr (W2 > 0) {
+                const uint32_t h2 = hash_token(t, P.width2, P.hash_mult, P.pow2_2);
+                const uint64_t bit2 = 1ull << (h2 & 63);
+#pragma unroll
+                for (int w = 0; w < W2; ++w) row2[w] ^= (h2 >> 6) == uint32_t(w) ? bit2 : 0ull;
+            }
+        }
+    }
+    // group reduction (groups never straddle a warp: lpr divides 32)
+    for (int o = lpr >> 1; o > 0; o >>= 1) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, row[w], o);
+            row[w] = P.method == 0 ? (row[w] | v) : (row[w] ^ v);
+        }
+        if constexpr (W2 > 0) {
+#pragma unroll
+            for (int w = 0; w < W2; ++w) row2[w] ^= __shfl_xor_sync(0xFFFFFFFFu, row2[w], o);
+        }
+    }
+    if (!live) return;
+    // lanes of the group store disjoint words
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+        if (w % lpr == sub) P.bits[static_cast<uint64_t>(r) * W + w] = row[w];
+    if constexpr (W2 > 0) {
+#pragma unroll
+        for (int w = 0; w < W2; ++w)
+            if (w % lpr == sub) P.bits2[static_cast<uint64_t>(r) * W2 + w] = row2[w];
+    }
+}
+
 // ================================================================ K2: filter
 struct FilterParams {
     const uint64_t* bits;        // sketches, n * W words (padded by kColSub rows)
@@ -493,6 +567,7 @@ struct RescanParams {
     int64_t cutoff;
     int words;
     int bypass_all;
+    uint32_t tile_rows;           // rows per work item (128, or 256 for the CTA-pair filter)
 };
 
 // One warp per row whose survivor count reaches the capacity: locate the
@@ -514,10 +589,10 @@ __global__ void rescan_saturated(RescanParams P) {
         }
         uint32_t start = j0, stop = i, seen = 0;
         if (P.item_counts) {
-            const uint32_t tile = r / kRowTile, t = r % kRowTile;
+            const uint32_t tile = r / P.tile_rows, t = r % P.tile_rows;
             const uint64_t ib = P.item_base[tile], ie = P.item_base[tile + 1];
             for (uint64_t it = ib; it < ie; ++it) {
-                const uint32_t cc = P.item_counts[it * kRowTile + t];
+                const uint32_t cc = P.item_counts[it * P.tile_rows + t];
                 if (seen + cc >= P.capacity) {
                     const uint32_t c0 = P.tile_col_lo[tile] + static_cast<uint32_t>(it - ib) * kColChunk;
                     start = max(j0, c0);
@@ -628,11 +703,18 @@ struct VerifyParams {
     uint32_t* res_ov;
     unsigned long long res_cap;
     Control* ctl;
+    const uint64_t* bits2;    // level-2 Xor sketches (n x w2 words), or null
+    const int32_t* maxham;    // maxham[|r|+|s|] (with bits2)
+    int w2;
 };
 
 // One thread per surviving pair: branch-free sorted merge with the
 // reference's early exit (src/similarity.cpp:168-185).  A match's overlap is
 // exact because the exit only fires on pairs that cannot reach minov.
+// With bits2, a pair is first re-tested against the wider level-2 Xor sketch
+// (the same exact bound, reference src/bitmap.cpp:125-143, at 64*w2 bits):
+// level-1 survivors the wider sketch rejects cannot match and skip the merge.
+template <int W2>
 __global__ void verify_pairs(VerifyParams P) {
     const int lane = threadIdx.x & 31;
     const unsigned long long count = min(*P.count_ptr, P.count_cap);
@@ -640,7 +722,7 @@ __global__ void verify_pairs(VerifyParams P) {
     for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < count;
          base += stride) {
         const unsigned long long k = base + threadIdx.x;
-        bool matched = false;
+        bool matched = false, merged = false;
         uint32_t j = 0, i = 0, ov = 0;
         if (k < count) {
             const uint2 pr = P.surv[k];
@@ -654,6 +736,20 @@ __global__ void verify_pairs(VerifyParams P) {
             const uint32_t* B = P.tokens + bb;
             uint32_t ia = 0, ib = 0;
             int32_t o = 0;
+            bool l2_ok = true;
+            if constexpr (W2 > 0) {
+                const ulonglong2* sj = reinterpret_cast<const ulonglong2*>(P.bits2 + static_cast<uint64_t>(j) * W2);
+                const ulonglong2* si = reinterpret_cast<const ulonglong2*>(P.bits2 + static_cast<uint64_t>(i) * W2);
+                int h = 0;
+#pragma unroll
+                for (int w = 0; w < W2 / 2; ++w) {
+                    const ulonglong2 x = __ldg(sj + w), y = __ldg(si + w);
+                    h += __popcll(x.x ^ y.x) + __popcll(x.y ^ y.y);
+                }
+                l2_ok = h <= P.maxham[na + nb];
+                if (!l2_ok) ia = na;  // skip the merge
+            }
+            merged = l2_ok;
             while (ia < na && ib < nb) {
                 const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
                 if (o + rest < need) break;
@@ -667,7 +763,8 @@ __global__ void verify_pairs(VerifyParams P) {
         }
         // algorithmic traffic: both token lists plus the 16-byte result record
         unsigned long long vb = 0;
-        if (k < count) vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
+        if (merged)
+            vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
         if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);

@@ -191,12 +191,36 @@ class Report:
     extra: dict = field(default_factory=dict)
 
 
+class _ReportOwner:
+    """Frees an ``ssj_report`` when the last numpy view of its pairs is gone."""
+
+    def __init__(self, lib, handle):
+        self.lib, self.handle = lib, handle
+
+    def __del__(self):
+        try:
+            self.lib.ssj_report_free(self.handle)
+        except Exception:
+            pass
+
+
+_ZERO_COPY_PAIRS = 1 << 20  # larger results are viewed in place, not copied
+
+
 def _take_report(lib, handle) -> Report:
     n = int(lib.ssj_report_pair_count(handle))
+    owner = None
     if n:
         ptr = lib.ssj_report_pairs(handle)
-        raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), (n * 16,))
-        pairs = raw.view(PAIR_DTYPE).copy()
+        if n >= _ZERO_COPY_PAIRS:
+            # the report's own pair array (ssj_report_pairs, valid until
+            # ssj_report_free) becomes the numpy buffer; freed with the array
+            buf = (C.c_uint8 * (n * 16)).from_address(C.cast(ptr, C.c_void_p).value)
+            owner = buf._owner = _ReportOwner(lib, handle)
+            pairs = np.frombuffer(buf, dtype=PAIR_DTYPE)
+        else:
+            raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), (n * 16,))
+            pairs = raw.view(PAIR_DTYPE).copy()
     else:
         pairs = np.zeros(0, dtype=PAIR_DTYPE)
     cnt = capi.Counters()
@@ -212,7 +236,8 @@ def _take_report(lib, handle) -> Report:
         if lib.ssjb_report_stats(handle, C.byref(st)) == capi.SSJ_OK:
             rep.extra = {k: (float(getattr(st, k)) if isinstance(getattr(st, k), float)
                              else int(getattr(st, k))) for k, _ in capi.Stats._fields_}
-    lib.ssj_report_free(handle)
+    if owner is None:
+        lib.ssj_report_free(handle)
     return rep
 
 

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Iteration run: GPU parity, C2 per-tau phases (b=128 int8, b=256), one filter
-# trace, heavy-config phase breakdown.
+# trace, heavy-config phase breakdown, heavy parity (HEAVY_TESTS=1).
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_parity.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_parity.log
 timeout 300 python tools/c2_phases.py 128 3 > gpurun_out/phases128.jsonl 2>&1
@@ -19,3 +19,6 @@ for rep in range(2):
 print("filter_ms", r.extra["ms_filter"])
 PY
 timeout 900 python tools/heavy_phases.py ${HEAVY:-C3 C5 C4} > gpurun_out/heavy_phases.jsonl 2>&1
+if [ -n "$HEAVY_TESTS" ]; then
+timeout 1500 python -m pytest tests/test_gpu_heavy.py -x -q -s > gpurun_out/pytest_heavy.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_heavy.log
+fi
