@@ -77,13 +77,24 @@ struct Arena {
     }
 };
 
-struct Timer {  // device-time spans on one stream
+struct Timer {  // device-time spans on one stream; events recycled per host thread
     cudaStream_t stream;
     std::vector<cudaEvent_t> evs;
-    explicit Timer(cudaStream_t s) : stream(s) {}
+    int device = 0;
+    static std::vector<cudaEvent_t>& pool(int dev) {
+        static thread_local std::vector<cudaEvent_t> p[16];
+        return p[dev & 15];
+    }
+    explicit Timer(cudaStream_t s) : stream(s) { cudaGetDevice(&device); }
     cudaEvent_t mark() {
         cudaEvent_t e;
-        CK(cudaEventCreate(&e));
+        auto& p = pool(device);
+        if (!p.empty()) {
+            e = p.back();
+            p.pop_back();
+        } else {
+            CK(cudaEventCreate(&e));
+        }
         CK(cudaEventRecord(e, stream));
         evs.push_back(e);
         return e;
@@ -94,17 +105,75 @@ struct Timer {  // device-time spans on one stream
         return f;
     }
     ~Timer() {
-        for (auto e : evs) cudaEventDestroy(e);
+        auto& p = pool(device);  // per host thread and device
+        for (auto e : evs) p.push_back(e);
     }
 };
 
+// Dynamic shared-memory opt-in, once per kernel and device.
+void set_smem_once(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& d : done)
+        if (d.first.first == fn && d.first.second == dev && d.second >= bytes) return;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.push_back({{fn, dev}, bytes});
+}
+
 bool narrow_tokens(const Collection& c) { return !c.tokens.empty() && c.universe <= 65536; }
+
+// Builds the delta-coded token copy (see Collection::tokens8); true when it is
+// worth using (at most 80% of the 16-bit copy's bytes).
+bool build_delta8(const Collection& c) {
+    const size_t n = c.size(), T = c.tokens.size();
+    std::vector<uint8_t> bytes(T + n + 1);
+    std::vector<uint32_t> start(n + 1, 0);
+    std::vector<uint16_t> val;
+    for (size_t r = 0; r < n; ++r) {
+        start[r] = static_cast<uint32_t>(val.size());
+        const uint64_t t0 = c.offsets[r], t1 = c.offsets[r + 1];
+        uint8_t* b = bytes.data() + t0 + r;
+        if (t0 == t1) {
+            b[0] = 0;  // pad byte of an empty record
+            continue;
+        }
+        uint32_t prev = c.tokens[t0];
+        b[0] = static_cast<uint8_t>(prev & 0xFF);
+        b[1] = static_cast<uint8_t>(prev >> 8);
+        for (uint64_t t = t0 + 1; t < t1; ++t) {
+            const uint32_t v = c.tokens[t], d = v - prev;
+            if (d < 255) {
+                b[t - t0 + 1] = static_cast<uint8_t>(d);
+            } else {
+                b[t - t0 + 1] = 255;
+                val.push_back(static_cast<uint16_t>(v));
+            }
+            prev = v;
+        }
+    }
+    start[n] = static_cast<uint32_t>(val.size());
+    const double coded = double(bytes.size()) + 4.0 * double(start.size()) + 2.0 * double(val.size());
+    if (coded > 0.8 * 2.0 * double(T)) return false;
+    c.tokens8.swap(bytes);
+    c.exc_start.swap(start);
+    c.exc_val.swap(val);
+    return true;
+}
 
 void register_host(const Collection& c) {
     // Page-lock the arrays that are uploaded so every upload is a pinned DMA;
-    // tokens of a universe <= 65536 travel as a 16-bit copy built once here.
+    // tokens of a universe <= 65536 travel as a delta-coded byte stream (dense
+    // universes) or a 16-bit copy, built once here.
     if (c.host_registered) return;
-    if (narrow_tokens(c)) {
+    if (narrow_tokens(c) && c.universe <= 65535 && env_u64("SSJB_DELTA8", 1) != 0 && build_delta8(c)) {
+        c.use_delta8 = true;
+        cudaHostRegister(c.tokens8.data(), c.tokens8.size(), cudaHostRegisterDefault);
+        cudaHostRegister(c.exc_start.data(), c.exc_start.size() * 4, cudaHostRegisterDefault);
+        if (!c.exc_val.empty()) cudaHostRegister(c.exc_val.data(), c.exc_val.size() * 2, cudaHostRegisterDefault);
+    } else if (narrow_tokens(c)) {
         c.tokens16.assign(c.tokens.begin(), c.tokens.end());
         cudaHostRegister(c.tokens16.data(), c.tokens16.size() * sizeof(uint16_t), cudaHostRegisterDefault);
     } else if (!c.tokens.empty()) {
@@ -196,6 +265,60 @@ __global__ void widen_tokens(const uint16_t* in, uint32_t* out, size_t n) {
     }
 }
 
+// Delta-coded tokens (Collection::tokens8) -> u32 tokens of records [r0, r1),
+// one thread per record.
+__global__ void decode_delta8(const uint8_t* bytes, const uint64_t* offsets, const uint32_t* exc_start,
+                              const uint16_t* exc_val, uint32_t* out, uint32_t r0, uint32_t r1) {
+    const uint32_t r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= r1) return;
+    const uint64_t t0 = offsets[r], t1 = offsets[r + 1];
+    if (t0 == t1) return;
+    const uint8_t* b = bytes + t0 + r;
+    uint32_t v = static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[1]) << 8);
+    out[t0] = v;
+    uint32_t e = exc_start[r];
+    for (uint64_t t = t0 + 1; t < t1; ++t) {
+        const uint32_t d = b[t - t0 + 1];
+        if (d == 255) v = exc_val[e++];
+        else v += d;
+        out[t] = v;
+    }
+}
+
+struct Delta8Dev {
+    uint8_t* bytes = nullptr;
+    uint32_t* exc_start = nullptr;
+    uint16_t* exc_val = nullptr;
+};
+
+// Device buffers for the delta-coded stream; the exception lists are uploaded here.
+Delta8Dev alloc_delta8(const Collection& c, cudaStream_t stream, uint64_t& h2d) {
+    Delta8Dev d;
+    const size_t ne = c.exc_val.size();
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d.bytes), c.tokens8.size() + 16, stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d.exc_start), c.exc_start.size() * 4, stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&d.exc_val), std::max<size_t>(ne, 1) * 2, stream));
+    CK(cudaMemcpyAsync(d.exc_start, c.exc_start.data(), c.exc_start.size() * 4, cudaMemcpyHostToDevice, stream));
+    if (ne) CK(cudaMemcpyAsync(d.exc_val, c.exc_val.data(), ne * 2, cudaMemcpyHostToDevice, stream));
+    h2d += c.exc_start.size() * 4 + ne * 2;
+    return d;
+}
+
+void launch_decode(const Delta8Dev& d, const uint64_t* offsets, uint32_t* out, uint32_t r0, uint32_t r1,
+                   cudaStream_t stream, uint64_t& launches) {
+    if (r1 <= r0) return;
+    decode_delta8<<<(r1 - r0 + 127) / 128, 128, 0, stream>>>(d.bytes, offsets, d.exc_start, d.exc_val, out, r0, r1);
+    ++launches;
+    CK(cudaGetLastError());
+}
+
+void free_delta8(Delta8Dev& d, cudaStream_t stream) {
+    if (d.bytes) CK(cudaFreeAsync(d.bytes, stream));
+    if (d.exc_start) CK(cudaFreeAsync(d.exc_start, stream));
+    if (d.exc_val) CK(cudaFreeAsync(d.exc_val, stream));
+    d = Delta8Dev{};
+}
+
 std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStream_t stream, uint64_t& h2d,
                                       uint64_t& launches, bool resident = false) {
     register_host(c);
@@ -216,7 +339,16 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     rep->n = n;
     rep->tokens_total = c.tokens.size();
     uint64_t tok_h2d = 0;
-    if (narrow_tokens(c)) {
+    CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       stream));
+    if (c.use_delta8) {
+        // ~1 byte per token, decoded on the device
+        Delta8Dev d = alloc_delta8(c, stream, tok_h2d);
+        CK(cudaMemcpyAsync(d.bytes, c.tokens8.data(), c.tokens8.size(), cudaMemcpyHostToDevice, stream));
+        tok_h2d += c.tokens8.size();
+        launch_decode(d, rep->offsets, rep->tokens, 0, static_cast<uint32_t>(n), stream, launches);
+        free_delta8(d, stream);
+    } else if (narrow_tokens(c)) {
         // 16-bit upload, widened on the device
         uint16_t* t16 = nullptr;
         const size_t T = c.tokens.size();
@@ -232,8 +364,6 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
                            cudaMemcpyHostToDevice, stream));
         tok_h2d = c.tokens.size() * sizeof(uint32_t);
     }
-    CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                       stream));
     rep->bytes = tok_h2d + (n + 1) * sizeof(uint64_t);
     h2d += rep->bytes;
     const size_t tot = n + kPadRows;
@@ -251,6 +381,92 @@ std::shared_ptr<DeviceReplica> replica_for(const Collection& c, int device, cuda
         register_host(c);
     }
     return upload(c, device, stream, h2d, launches);
+}
+
+// Streamed ingest for a per-join replica: offsets and sizes are uploaded on
+// `stream` at once, the token array in row chunks (boundaries on multiples of
+// `align_rows`, balanced by tokens) on the copy stream `cs`, one event per chunk.
+// The join then builds sketches and filters chunk k while chunk k+1 is in
+// flight: the window of row i only reaches columns j < i, so a chunk's work
+// items never need rows of a later chunk.
+struct IngestChunk {
+    uint32_t r0 = 0, r1 = 0;
+    uint64_t t0 = 0, t1 = 0;
+    cudaEvent_t ev = nullptr;
+};
+
+std::shared_ptr<DeviceReplica> upload_streamed(const Collection& c, int device, cudaStream_t stream, cudaStream_t cs,
+                                               uint32_t align_rows, int nchunks, uint64_t& h2d, uint64_t& launches,
+                                               std::vector<IngestChunk>& chunks, uint16_t*& t16,
+                                               Delta8Dev& d8) {
+    {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        register_host(c);
+    }
+    auto rep = std::make_shared<DeviceReplica>();
+    const size_t n = c.size();
+    const size_t T = c.tokens.size();
+    const size_t tok_bytes = std::max<size_t>(T, 4) * sizeof(uint32_t) + 16;
+    rep->stream = stream;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->tokens), tok_bytes, stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->offsets), (n + 1) * sizeof(uint64_t), stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows) * sizeof(uint32_t), stream));
+    const bool delta8 = c.use_delta8;
+    const bool narrow = !delta8 && narrow_tokens(c);
+    t16 = nullptr;
+    uint64_t tok_h2d = 0;
+    if (delta8) d8 = alloc_delta8(c, stream, tok_h2d);
+    if (narrow) CK(cudaMallocAsync(reinterpret_cast<void**>(&t16), std::max<size_t>(T, 4) * 2 + 16, stream));
+    rep->device = device;
+    rep->n = n;
+    rep->tokens_total = T;
+    CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
+    sizes_from_offsets<<<static_cast<unsigned>((n + kPadRows + 255) / 256), 256, 0, stream>>>(rep->offsets,
+                                                                                              rep->sizes, n);
+    ++launches;
+    CK(cudaGetLastError());
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, stream));  // allocations done
+    CK(cudaStreamWaitEvent(cs, ready, 0));
+    CK(cudaEventDestroy(ready));
+    chunks.clear();
+    uint32_t r0 = 0;
+    for (int k = 1; k <= nchunks && r0 < n; ++k) {
+        uint32_t r1 = static_cast<uint32_t>(n);
+        if (k < nchunks) {
+            const uint64_t target = T * static_cast<uint64_t>(k) / nchunks;
+            const size_t r = std::lower_bound(c.offsets.begin(), c.offsets.end(), target) - c.offsets.begin();
+            r1 = static_cast<uint32_t>(std::min(n, (r + align_rows - 1) / align_rows * align_rows));
+            if (r1 <= r0) continue;
+        }
+        IngestChunk ch;
+        ch.r0 = r0;
+        ch.r1 = r1;
+        ch.t0 = c.offsets[r0];
+        ch.t1 = c.offsets[r1];
+        if (delta8) {
+            const uint64_t b0 = ch.t0 + r0, b1 = (r1 < n ? ch.t1 + r1 : c.tokens8.size());
+            if (b1 > b0)
+                CK(cudaMemcpyAsync(d8.bytes + b0, c.tokens8.data() + b0, b1 - b0, cudaMemcpyHostToDevice, cs));
+            tok_h2d += b1 - b0;
+        } else if (ch.t1 > ch.t0) {
+            tok_h2d += (ch.t1 - ch.t0) * (narrow ? 2 : 4);
+            if (narrow)
+                CK(cudaMemcpyAsync(t16 + ch.t0, c.tokens16.data() + ch.t0, (ch.t1 - ch.t0) * 2, cudaMemcpyHostToDevice,
+                                   cs));
+            else
+                CK(cudaMemcpyAsync(rep->tokens + ch.t0, c.tokens.data() + ch.t0, (ch.t1 - ch.t0) * 4,
+                                   cudaMemcpyHostToDevice, cs));
+        }
+        CK(cudaEventCreateWithFlags(&ch.ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ch.ev, cs));
+        chunks.push_back(ch);
+        r0 = r1;
+    }
+    rep->bytes = tok_h2d + (n + 1) * sizeof(uint64_t);
+    h2d += rep->bytes;
+    return rep;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -387,8 +603,11 @@ size_t operand_row(int words, int variant) {
 }
 
 void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int words2, const uint32_t* sizes,
-                   uint8_t* opA, uint8_t* opB, uint32_t rows, int variant, cudaStream_t s, uint64_t& launches) {
+                   uint8_t* opA, uint8_t* opB, uint32_t rows, int variant, cudaStream_t s, uint64_t& launches,
+                   uint32_t row0 = 0) {
+    if (rows <= row0) return;
     dev::ExpandParams E{};
+    E.row0 = row0;
     E.bits = bits;
     E.bits2 = bits2;
     E.sizes = sizes;
@@ -402,7 +621,7 @@ void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int w
     E.K2 = variant == 1 ? 64 * words2 + 32 : 0;
     E.with_size = variant == 3 ? 0 : 1;
     const int kct = (E.K1 + E.K2) / 16 + E.with_size;
-    const uint64_t threads = static_cast<uint64_t>(rows) * kct;
+    const uint64_t threads = static_cast<uint64_t>(rows - row0) * kct;
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
     ++launches;
     CK(cudaGetLastError());
@@ -457,17 +676,20 @@ BuildFn2 build_sub_fn(int words, int words2) {
 // Level-1 Set/Xor sketch (+ level-2 Xor sketch when bits2) in one launch.
 // Returns false when the method/width needs the one-thread-per-record kernel.
 bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2, Method method, int width,
-                      int width2, int hash, cudaStream_t s, uint64_t& launches) {
+                      int width2, int hash, cudaStream_t s, uint64_t& launches, uint32_t row0 = 0,
+                      uint32_t row1 = UINT32_MAX) {
     if (method != Method::Set && method != Method::Xor) return false;
     BuildFn2 fn = build_sub_fn(width / 64, bits2 ? width2 / 64 : 0);
     if (!fn) return false;
-    if (rep.n == 0) return true;
+    row1 = std::min<uint32_t>(row1, static_cast<uint32_t>(rep.n));
+    if (row1 <= row0) return true;
     dev::BuildParams2 P{};
+    P.row0 = row0;
     P.tokens = rep.tokens;
     P.offsets = rep.offsets;
     P.bits = bits;
     P.bits2 = bits2;
-    P.n = static_cast<uint32_t>(rep.n);
+    P.n = row1;
     P.width = static_cast<uint32_t>(width);
     P.width2 = static_cast<uint32_t>(width2);
     P.method = method == Method::Set ? 0 : 1;
@@ -479,7 +701,7 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
     int lg = 0;
     while (lg < 5 && (1 << lg) * 8.0 < mean) ++lg;
     P.lpr_log2 = lg;
-    const uint64_t threads = static_cast<uint64_t>(rep.n) << lg;
+    const uint64_t threads = static_cast<uint64_t>(row1 - row0) << lg;
     const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
     fn<<<grid, 256, 0, s>>>(P);
     ++launches;
@@ -701,7 +923,12 @@ void engine_unpin(const Collection& c, int device) {
 
 void engine_release_host(const Collection& c) {
     if (!c.host_registered) return;
-    if (narrow_tokens(c)) cudaHostUnregister(c.tokens16.data());
+    if (c.use_delta8) {
+        cudaHostUnregister(c.tokens8.data());
+        cudaHostUnregister(c.exc_start.data());
+        if (!c.exc_val.empty()) cudaHostUnregister(c.exc_val.data());
+    }
+    else if (narrow_tokens(c)) cudaHostUnregister(c.tokens16.data());
     else if (!c.tokens.empty()) cudaHostUnregister(const_cast<uint32_t*>(c.tokens.data()));
     cudaHostUnregister(const_cast<uint64_t*>(c.offsets.data()));
     cudaGetLastError();
@@ -752,7 +979,6 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     if (enabled && plan.bitmap.cutoff < 0) throw std::invalid_argument("bitmap cutoff must be >= 0");
 
     cudaEvent_t e0 = T.mark();
-    auto rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
     // plan tables
     int32_t* d_maxham = A.alloc<int32_t>(plan.minov.size());
     int32_t* d_minov = A.alloc<int32_t>(plan.minov.size());
@@ -792,7 +1018,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // (C2 b=128: 9.0 vs 22.5 ms).  SSJB_TC_KIND=i8|fp4 overrides.
     const bool fp4 = use_tc && !l2gemm &&
                      (kenv && *kenv ? std::string(kenv) == "fp4" : W >= 3);
-    // int8 level-1-only filter on a CTA pair (M = 256): experimental, SSJB_TC2=1
+    // int8 level-1-only filter on a CTA pair (M = 256): experimental, opt in with SSJB_TC2=1
     const bool use_tc2 = use_tc && !l2gemm && !fp4 && W <= 2 && env_u64("SSJB_TC2", 0) != 0;
 
     // work items: (row tile, 4096-column chunk); the pair kernel takes 256-row tiles
@@ -813,6 +1039,31 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         st.h2d_bytes += tl.item_base.size() * 8 + tl.col_lo.size() * 4 + tl.item_tile.size() * 4;
     };
     set_tiling(use_tc2 ? 2 * dev::kRowTile : dev::kRowTile);
+
+    // the collection on the device: a pinned replica, or uploaded for this join --
+    // streamed in row chunks (overlapping the first chunks' sketches and filter
+    // work with the rest of the transfer) when the whole self-join runs here
+    std::shared_ptr<DeviceReplica> rep;
+    {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        if (c.pinned[device & 15] && c.pinned[device & 15]->device == device) rep = c.pinned[device & 15];
+    }
+    std::vector<IngestChunk> ingest;
+    uint16_t* ingest_t16 = nullptr;
+    Delta8Dev ingest_d8;
+    const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
+    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n &&
+        n >= env_u64("SSJB_STREAM_MIN_ROWS", 65536) && n > 0 && env_u64("SSJB_STREAM", 1) != 0) {
+        static thread_local cudaStream_t copy_streams[16] = {};
+        if (!copy_streams[device & 15])
+            CK(cudaStreamCreateWithFlags(&copy_streams[device & 15], cudaStreamNonBlocking));
+        rep = upload_streamed(c, device, s, copy_streams[device & 15], tl.tile_rows,
+                              static_cast<int>(env_u64("SSJB_STREAM_CHUNKS", 4)), st.h2d_bytes, st.launches, ingest,
+                              ingest_t16, ingest_d8);
+    } else if (!rep) {
+        rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
+    }
+    const bool streamed = !ingest.empty();
     cudaEvent_t e_up = T.mark();
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
     const bool resident = rep->stream == nullptr;
@@ -847,8 +1098,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             CK(cudaMemsetAsync(fresh->bits2 + n * W2, 0, (kPadRows + 8) * W2 * 8, s));
         }
         // one token pass for both sketches where the sub-warp builder applies
-        if (!launch_build_sub(*rep, fresh->bits, fresh->bits2, plan.bitmap.method, width, 64 * W2,
-                              plan.bitmap.hash, s, st.launches)) {
+        // (streamed ingest: built chunk by chunk before each chunk's filter work)
+        if (streamed) {
+        } else if (!launch_build_sub(*rep, fresh->bits, fresh->bits2, plan.bitmap.method, width, 64 * W2,
+                                     plan.bitmap.hash, s, st.launches)) {
             launch_build(*rep, fresh->bits, plan.bitmap.method, width, plan.bitmap.hash, s, st.launches);
             if (W2 && !launch_build_sub(*rep, fresh->bits2, nullptr, Method::Xor, 64 * W2, 0, plan.bitmap.hash, s,
                                         st.launches))
@@ -862,8 +1115,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         const size_t rowb = operand_row(W, variant);
         sk->opA[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
         sk->opB[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
-        launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, sk->opA[variant], sk->opB[variant], n_pad, variant, s,
-                      st.launches);
+        if (streamed) {
+            // tiles near the diagonal load (masked) columns of the next chunk
+            // before it is expanded: keep them zero, i.e. size 0, a valid index
+            CK(cudaMemsetAsync(sk->opA[variant], 0, static_cast<size_t>(n_pad) * rowb, s));
+            CK(cudaMemsetAsync(sk->opB[variant], 0, static_cast<size_t>(n_pad) * rowb, s));
+        } else {
+            launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, sk->opA[variant], sk->opB[variant], n_pad, variant,
+                          s, st.launches);
+        }
         built = true;
     }
     if (resident) {
@@ -883,8 +1143,14 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // buffer sizing: survivors (8 B) and result sort buffers (24 B); a batch's
     // results must fit the result buffer, so res_cap >= surv_cap.  With the HBM
     // of a B200 free, larger buffers mean fewer filter batches / result runs.
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    // free HBM when this device was first used (one query per device and process)
+    static size_t free_at_first[16] = {};
+    static std::once_flag mem_once[16];
+    std::call_once(mem_once[device & 15], [device]() {
+        size_t f = 0, t = 0;
+        if (cudaMemGetInfo(&f, &t) == cudaSuccess) free_at_first[device & 15] = f;
+    });
+    const size_t free_b = free_at_first[device & 15];
     const uint64_t big = free_b >= (size_t(64) << 30) ? 1 : 0;
     const uint64_t surv_cap =
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
@@ -916,7 +1182,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // filter launch configuration
     const FilterFn ffn = filter_fn(W, W2);
     const size_t fsmem = filter_smem(W, W2);
-    CK(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+    set_smem_once(reinterpret_cast<const void*>(ffn), static_cast<int>(fsmem));
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffn, dev::kRowTile, fsmem));
@@ -949,7 +1215,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     bool tc2_active = use_tc2;
     if (use_tc) {
         tck = use_tc2 ? tc2_select(W) : tc_select(W, l2gemm, fp4);
-        CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
+        set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
         TP.opA = d_opA;
         TP.opB = d_opB;
         TP.bits = d_bits;
@@ -1033,8 +1299,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     };
 
     uint64_t total_items = tl.item_base.back();
-    auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb) {
-        CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
+    auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb, bool keep_survivors = false) {
+        if (!keep_survivors) CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
         CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
         if (d_item_counts && ie > ib)
             CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (ie - ib) * tl.tile_rows * 4, s));
@@ -1079,6 +1345,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.bits = d_bits;
             RP.sizes = rep->sizes;
             RP.maxham = d_maxham;
+            RP.maxham_len = static_cast<int>(maxham.size());
             RP.wstart = d_wstart;
             RP.rowcnt = d_rowcnt;
             RP.item_counts = d_item_counts;
@@ -1120,7 +1387,32 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     bool done = false;
     {
         cudaEvent_t a = T.mark();
-        launch_filter(0, total_items, 0);
+        if (streamed) {
+            const int variant_s = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : (use_tc2 ? 3 : 0)));
+            for (size_t k = 0; k < ingest.size(); ++k) {
+                const IngestChunk& ch = ingest[k];
+                CK(cudaStreamWaitEvent(s, ch.ev, 0));
+                if (ingest_d8.bytes) launch_decode(ingest_d8, rep->offsets, rep->tokens, ch.r0, ch.r1, s, st.launches);
+                if (ingest_t16 && ch.t1 > ch.t0) {
+                    const uint64_t w0 = ch.t0 & ~uint64_t(3);  // 8-byte aligned vector loads
+                    const uint64_t cnt = ch.t1 - w0;
+                    widen_tokens<<<static_cast<unsigned>((cnt + 1023) / 1024), 256, 0, s>>>(ingest_t16 + w0,
+                                                                                           rep->tokens + w0, cnt);
+                    ++st.launches;
+                    CK(cudaGetLastError());
+                }
+                launch_build_sub(*rep, sk->bits, sk->bits2, plan.bitmap.method, width, 64 * W2, plan.bitmap.hash, s,
+                                 st.launches, ch.r0, ch.r1);
+                const bool last = k + 1 == ingest.size();
+                launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, d_opA, d_opB, last ? n_pad : ch.r1, variant_s,
+                              s, st.launches, ch.r0);
+                const uint32_t ta = ch.r0 / tl.tile_rows;
+                const uint32_t tb2 = last ? tl.ntiles : ch.r1 / tl.tile_rows;
+                launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
+            }
+        } else {
+            launch_filter(0, total_items, 0);
+        }
         cudaEvent_t b = T.mark();
         launch_verify();
         cudaEvent_t c1 = T.mark();
@@ -1182,13 +1474,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                     }
                 }
                 tck = tc_select(W, true, false);
-                CK(cudaFuncSetAttribute(tck.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tck.smem));
+                set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
                 TP.opA = a1;
                 TP.opB = b1;
                 st.filter_kernel = 2;
             }
         }
     }
+
+    for (auto& ch : ingest) CK(cudaEventDestroy(ch.ev));
+    if (ingest_t16) CK(cudaFreeAsync(ingest_t16, s));
+    free_delta8(ingest_d8, s);
 
     if (!done) {
         // batches of work items sized so the survivors fit the buffer

@@ -671,26 +671,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         }
                     }
                 }
-                if constexpr (KIND == kKindI8 && K2 > 0) {
-                    // level-2 GEMM variant, interior fast path (one 32-column group per
-                    // warp): both accumulators as packed s16 in one load latency
-                    if (fast && !groups_done) {
-                        groups_done = true;
-                        uint32_t d[16], d2[16];
-                        tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cw, d);
-                        tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cw, d2);
-                        tmem_wait_ld();
-                        const int c16 = max(cim1, -32768);
-                        if (__any_sync(0xFFFFFFFFu, bypass || any_above16_32(d, c16))) {
-                            const uint32_t m = bypass ? 0xFFFFFFFFu : mask16_32(d, c16);
-                            cnt += __popc(m);
-                            if (__any_sync(0xFFFFFFFFu, m != 0)) {
-                                const uint32_t e = m & mask16_32(d2, max(cim1_2, -32768));
-                                if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, wbase, i, q, qlen, P, lane);
-                            }
-                        }
-                    }
-                }
+                // (the level-2 GEMM variant keeps the unpacked path below: it is bound
+                // by shared-memory operand traffic, and the packed s16 masks cost more
+                // ALU per group when most pairs survive level 1 -- 3.17 vs 2.68 ms, C2 tau=0.5)
                 if constexpr (KIND == kKindI8 && K2 == 0) {
                     // int8 groups of 32 columns: level-1 accumulators
                     // as packed s16 in one load latency.  Thresholds per run of equal
@@ -828,7 +811,8 @@ struct ExpandParams {
     const uint32_t* sizes;  // |r| (padded)
     uint8_t* opA;
     uint8_t* opB;
-    uint32_t rows;          // n_pad (multiple of 8)
+    uint32_t rows;          // rows [row0, rows) are expanded (n_pad: multiple of 8)
+    uint32_t row0;          // multiple of 8
     int words, words2;
     int K1;                 // level-1 bytes per row
     int K2;                 // level-2 bytes per row (0: none)
@@ -898,8 +882,8 @@ __device__ __forceinline__ void expand_f4(const uint64_t* row, int words, int c,
 __global__ void expand_operands(ExpandParams P) {
     const int KCT = (P.K1 + P.K2) / 16 + P.with_size;
     const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<uint64_t>(P.rows) * KCT) return;
-    const uint32_t r = static_cast<uint32_t>(idx / KCT);
+    if (idx >= static_cast<uint64_t>(P.rows - P.row0) * KCT) return;
+    const uint32_t r = P.row0 + static_cast<uint32_t>(idx / KCT);
     const int c = static_cast<int>(idx % KCT);
     uint32_t a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0};
     if (c < P.K1 / 16) {

@@ -43,6 +43,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Relaxed remote arrive: pure progress signals that publish no memory the
+// receiver reads through ordinary loads (the TMEM slot an epilogue warp has
+// finished loading; a stage the peer's bulk copy has completed -- the data
+// is complete in the peer's shared memory before its barrier flips).  A
+// .release arrive would first drain the thread's outstanding memory traffic.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 // wait with cluster-scope acquire (barriers that receive arrivals from the peer)
 __device__ __forceinline__ void mbar_wait_cl(uint32_t a, uint32_t parity) {
     asm volatile(
@@ -216,6 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     mbar_expect_tx(&b_full[st], L::kB + L::kSz);
                     tma_load_1d(sB + st * L::kB, P.opB + static_cast<uint64_t>(col + rank * kRowTile) * KA, L::kB,
@@ -241,11 +251,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                     // --------------------------------------------------- relay
                     // tell the leader's MMA issuer when this CTA's halves landed
                     mbar_spin(&a_full[aslot], (iseq >> 1) & 1);
-                    mbar_arrive_cluster(L_a_peer + 8 * aslot);
+                    mbar_arrive_cluster_relaxed(L_a_peer + 8 * aslot);
                     for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                         const int st = tseq % NS;
                         mbar_spin(&b_full[st], (tseq / NS) & 1);
-                        mbar_arrive_cluster(L_b_peer + 8 * st);
+                        mbar_arrive_cluster_relaxed(L_b_peer + 8 * st);
                     }
                     ++iseq;
                     continue;
@@ -259,7 +269,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                     const int as = aseq & 1;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
                     mbar_wait_cl(smem_u32(&b_peer[st]), (tseq / NS) & 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
                     mbar_wait_cl(smem_u32(&acc_empty[as]), ((aseq >> 1) & 1) ^ 1);
+                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
@@ -282,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         uint2* q = sQ + ew * kTcQueue;
         int qlen = 0;
-        uint32_t iseq = 0, st_idx = 0, st_phase = 0, acc_idx = 0, acc_phase = 0;
+        uint32_t iseq = 0, st_idx = 0, st_phase = 0, acc_idx = 0, acc_phase = 0, tile_seq = 0;
         for (;;) {
             const int slot = iseq & 1;
             mbar_wait_cl(smem_u32(&item_full[slot]), (iseq >> 1) & 1);
@@ -323,6 +335,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 mbar_wait_u32(smem_u32(&b_full[0]) + 8 * st_idx, st_phase);
                 mbar_wait_u32(smem_u32(&acc_full[0]) + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512)
+                    P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
                 const uint32_t* szs = sSz + st_idx * NT;
                 const int cw = part * L::kColsPerWarp;
                 const uint32_t wbase = info.c0 + t * NT + cw;
@@ -367,17 +381,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                         }
                         if (!__any_sync(0xFFFFFFFFu, bypass || (rm != 0 && any_above16_32(d, max(cmin, -32768)))))
                             continue;
-                        uint32_t m = 0xFFFFFFFFu;
-                        if (!bypass) {
-                            m = 0;
-                            rem = 0xFFFFFFFFu;
-                            while (rem) {
-                                const uint32_t sz = __shfl_sync(0xFFFFFFFFu, colsz, __ffs(rem) - 1);
-                                const uint32_t sel = __ballot_sync(0xFFFFFFFFu, colsz == sz);
-                                rem &= ~sel;
-                                m |= mask16_32(d, max(pc - maxham[si + sz] - 1, -32768)) & sel;
-                            }
+                        // (all lanes run the run loop: its shuffles need the full warp)
+                        uint32_t m = 0;
+                        rem = 0xFFFFFFFFu;
+                        while (rem) {
+                            const uint32_t sz = __shfl_sync(0xFFFFFFFFu, colsz, __ffs(rem) - 1);
+                            const uint32_t sel = __ballot_sync(0xFFFFFFFFu, colsz == sz);
+                            rem &= ~sel;
+                            m |= mask16_32(d, max(pc - maxham[si + sz] - 1, -32768)) & sel;
                         }
+                        if (bypass) m = 0xFFFFFFFFu;
                         m &= rm;
                         cnt += __popc(m);
                         if (__any_sync(0xFFFFFFFFu, m != 0)) tc_emit(m, gbase, i, q, qlen, P, lane);
@@ -386,8 +399,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) {
+                    if (P.trace && blockIdx.x == 0 && tile_seq < 512)
+                        P.trace[2048 + 8192 + tile_seq * 16 + (warp - 2)] = clock64();
                     if (leader) mbar_arrive(&acc_empty[acc_idx]);
-                    else mbar_arrive_cluster(L_acc_empty + 8 * acc_idx);
+                    else mbar_arrive_cluster_relaxed(L_acc_empty + 8 * acc_idx);
                     mbar_arrive(&b_empty[st_idx]);
                 }
                 if (++st_idx == NS) {
@@ -398,6 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                     acc_idx = 0;
                     acc_phase ^= 1u;
                 }
+                ++tile_seq;
             }
             if (valid && cnt) atomicAdd(P.rowcnt + (i - P.row_begin), cnt);
             if (P.item_counts && cnt) atomicAdd(P.item_counts + info.item * kRows2 + rank * kRowTile + rit, cnt);

@@ -96,6 +96,15 @@ struct Collection {
     mutable bool host_registered = false;
     // 16-bit copy of the tokens (universe <= 65536), page-locked: halves every upload
     mutable std::vector<uint16_t> tokens16;
+    // Delta-coded copy for dense universes (<= 65536 and small gaps), page-locked:
+    // record r occupies bytes [offsets[r] + r, offsets[r+1] + r + 1): its first
+    // token as u16, then one byte per token holding the gap to the previous one
+    // (1..254), 255 marking an exception whose absolute value is the next entry
+    // of exc_val (record r's exceptions start at exc_start[r]).  ~1 byte per token.
+    mutable std::vector<uint8_t> tokens8;
+    mutable std::vector<uint32_t> exc_start;
+    mutable std::vector<uint16_t> exc_val;
+    mutable bool use_delta8 = false;
     ~Collection();
 };
 

@@ -172,7 +172,8 @@ struct BuildParams2 {
     const uint64_t* offsets;
     uint64_t* bits;        // n * W words
     uint64_t* bits2;       // n * W2 words (W2 > 0)
-    uint32_t n;
+    uint32_t n;            // rows [row0, n) are built
+    uint32_t row0;
     uint32_t width, width2;
     int method;            // 0 Set, 1 Xor
     int hash_mult;
@@ -184,7 +185,7 @@ template <int W, int W2>
 __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
     const int lpr = 1 << P.lpr_log2;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t r = gtid >> P.lpr_log2;
+    const uint32_t r = P.row0 + (gtid >> P.lpr_log2);
     const int sub = static_cast<int>(gtid & (lpr - 1));
     const bool live = r < P.n;
     uint64_t row[W], row2[W2 > 0 ? W2 : 1];
@@ -568,13 +569,22 @@ struct RescanParams {
     int words;
     int bypass_all;
     uint32_t tile_rows;           // rows per work item (128, or 256 for the CTA-pair filter)
+    int maxham_len;
 };
+
+constexpr int kRescanLut = 4096;  // maxham[] entries staged in shared memory
 
 // One warp per row whose survivor count reaches the capacity: locate the
 // capacity-th survivor in window order (the reference's saturation point,
 // src/parallel_join.cpp:83-94).  With per-item counts from the filter only the
 // single 4096-column chunk holding it is rescanned; 128 columns per step.
-__global__ void rescan_saturated(RescanParams P) {
+__global__ void __launch_bounds__(256) rescan_saturated(RescanParams P) {
+    __shared__ int32_t lut[kRescanLut];
+    const bool lut_smem = P.maxham_len <= kRescanLut;
+    if (lut_smem)
+        for (int k = threadIdx.x; k < P.maxham_len; k += blockDim.x) lut[k] = P.maxham[k];
+    __syncthreads();
+    const int32_t* maxham = lut_smem ? lut : P.maxham;
     const int lane = threadIdx.x & 31;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < P.row_end - P.row_begin; r += warps) {
@@ -602,7 +612,11 @@ __global__ void rescan_saturated(RescanParams P) {
                 seen += cc;
             }
         }
-        const uint64_t* me = P.bits + static_cast<uint64_t>(i) * P.words;
+        uint64_t me[kMaxInlineWords];
+        const int words = min(P.words, kMaxInlineWords);
+        for (int w = 0; w < words; ++w) me[w] = __ldg(P.bits + static_cast<uint64_t>(i) * P.words + w);
+        // 128 columns per step in four lane-contiguous groups of 32 (coalesced
+        // sketch and size loads: a group reads 32 consecutive sketch rows)
         for (uint32_t jb = start; jb < stop; jb += 128) {
             uint32_t bal[4];
 #pragma unroll
@@ -610,10 +624,22 @@ __global__ void rescan_saturated(RescanParams P) {
                 const uint32_t j = jb + q * 32 + lane;
                 bool surv = false;
                 if (j < stop) {
-                    const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
+                    const uint32_t sj = __ldg(P.sizes + j);
                     int h = 0;
-                    for (int w = 0; w < P.words; ++w) h += __popcll(__ldg(me + w) ^ __ldg(o + w));
-                    surv = h <= __ldg(P.maxham + si + __ldg(P.sizes + j));
+                    if (P.words == 2) {
+                        const ulonglong2 o = __ldg(reinterpret_cast<const ulonglong2*>(P.bits) + j);
+                        h = __popcll(me[0] ^ o.x) + __popcll(me[1] ^ o.y);
+                    } else if (P.words == 1) {
+                        h = __popcll(me[0] ^ __ldg(P.bits + j));
+                    } else if (P.words <= kMaxInlineWords) {
+                        const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
+                        for (int w = 0; w < words; ++w) h += __popcll(me[w] ^ __ldg(o + w));
+                    } else {
+                        const uint64_t* o = P.bits + static_cast<uint64_t>(j) * P.words;
+                        const uint64_t* mi = P.bits + static_cast<uint64_t>(i) * P.words;
+                        for (int w = 0; w < P.words; ++w) h += __popcll(__ldg(mi + w) ^ __ldg(o + w));
+                    }
+                    surv = h <= maxham[si + sj];
                 }
                 bal[q] = __ballot_sync(0xFFFFFFFFu, surv);
             }

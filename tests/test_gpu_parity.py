@@ -75,6 +75,18 @@ def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
         assert_same(rep, e, flavour)
 
 
+@pytest.mark.parametrize("flavour", ["tc-i8", "tc-i8-pair", "tc-fp4"])
+def test_streamed_ingest(lib, golden, colls, flavour, monkeypatch):
+    """Every fixture with the collection streamed to the device in 3 row chunks
+    (sketches + filter work of a chunk overlap the next chunk's transfer)."""
+    set_filter(monkeypatch, flavour)
+    monkeypatch.setenv("SSJB_STREAM_MIN_ROWS", "1")
+    monkeypatch.setenv("SSJB_STREAM_CHUNKS", "3")
+    for e in golden["joins"]:
+        rep = S.join(colls(e["collection"]), options_of(lib, e))
+        assert_same(rep, e, "streamed " + flavour)
+
+
 def test_row_shards_add_up(lib, golden, colls):
     for e in golden["joins"]:
         if e["options"]["algorithm"] != capi.SSJ_ALGO_PAR_BITMAP or e["collection"].startswith("acc1_"):
