@@ -77,6 +77,45 @@ struct Arena {
     }
 };
 
+// Small host tables of a join packed into one page-locked staging buffer and
+// sent with a single copy (pageable cudaMemcpyAsync calls each cost a staged,
+// synchronous transfer).  The buffer is per host thread; a join synchronises
+// its stream before the next one reuses it.
+struct TableStage {
+    std::vector<std::pair<const void*, size_t>> parts;
+    std::vector<void**> targets;
+    size_t total = 0;
+    template <typename T>
+    void add(T** dev_ptr, const void* host, size_t bytes) {
+        parts.push_back({host, bytes});
+        targets.push_back(reinterpret_cast<void**>(dev_ptr));
+        total += (bytes + 15) & ~size_t(15);
+    }
+    // one H2D of every part; sets the device pointers
+    void flush(Arena& A, cudaStream_t s, uint64_t& h2d) {
+        static thread_local uint8_t* host = nullptr;
+        static thread_local size_t cap = 0;
+        if (total == 0) return;
+        if (total > cap) {
+            if (host) cudaFreeHost(host);
+            cap = std::max(total, size_t(1) << 20);
+            CK(cudaMallocHost(reinterpret_cast<void**>(&host), cap));
+        }
+        uint8_t* dev = A.alloc<uint8_t>(total);
+        size_t off = 0;
+        for (size_t k = 0; k < parts.size(); ++k) {
+            if (parts[k].second) std::memcpy(host + off, parts[k].first, parts[k].second);
+            *targets[k] = dev + off;
+            off += (parts[k].second + 15) & ~size_t(15);
+        }
+        CK(cudaMemcpyAsync(dev, host, total, cudaMemcpyHostToDevice, s));
+        h2d += total;
+        parts.clear();
+        targets.clear();
+        total = 0;
+    }
+};
+
 struct Timer {  // device-time spans on one stream; events recycled per host thread
     cudaStream_t stream;
     std::vector<cudaEvent_t> evs;
@@ -197,9 +236,11 @@ struct SketchSet {
     uint64_t* bits = nullptr;
     uint64_t* bits2 = nullptr;
     // expanded tcgen05 operand arrays (A, B) per variant: 0 int8, 1 int8 + level-2,
-    // 2 fp4, 3 int8 without the size chunk (CTA-pair kernel)
-    uint8_t* opA[4] = {nullptr, nullptr, nullptr, nullptr};
-    uint8_t* opB[4] = {nullptr, nullptr, nullptr, nullptr};
+    // 2 fp4, 3 int8 without the size chunk (CTA-pair kernel), 4 int8 without the
+    // popcount extension (+ per-column -pc pairs)
+    uint8_t* opA[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    uint8_t* opB[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    uint32_t* npc2 = nullptr;
     bool owned = false;  // cudaMalloc'd (persistent) rather than arena memory
     ~SketchSet() {
         if (!owned) return;
@@ -208,7 +249,8 @@ struct SketchSet {
         cudaSetDevice(device);
         cudaFree(bits);
         cudaFree(bits2);
-        for (int v = 0; v < 4; ++v) {
+        cudaFree(npc2);
+        for (int v = 0; v < 5; ++v) {
             cudaFree(opA[v]);
             cudaFree(opB[v]);
         }
@@ -285,6 +327,75 @@ __global__ void decode_delta8(const uint8_t* bytes, const uint64_t* offsets, con
     }
 }
 
+// Sub-warp variant: 2^lg lanes per record, each decoding a contiguous segment of
+// the record's gap bytes.  A segment either adds its gaps to the value coming
+// in, or (if it holds an exception) restarts from its last exception: a
+// segmented scan over the lanes gives every segment its starting value, and an
+// exclusive scan of exception counts its first exception index.
+__global__ void decode_delta8_sub(const uint8_t* bytes, const uint64_t* offsets, const uint32_t* exc_start,
+                                  const uint16_t* exc_val, uint32_t* out, uint32_t r0, uint32_t r1, int lg) {
+    const int lpr = 1 << lg;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t r = r0 + (gtid >> lg);
+    const int sub = static_cast<int>(gtid & (lpr - 1));
+    const bool live = r < r1;
+    uint64_t t0 = 0, t1 = 0;
+    if (live) {
+        t0 = offsets[r];
+        t1 = offsets[r + 1];
+    }
+    const uint32_t gaps = t1 > t0 ? static_cast<uint32_t>(t1 - t0 - 1) : 0u;  // gap bytes after the first token
+    const uint32_t seg = (gaps + lpr - 1) >> lg;
+    const uint32_t g0 = min(gaps, sub * seg), g1 = min(gaps, g0 + seg);
+    const uint8_t* b = bytes + t0 + r + 2;  // gap k of the record at b[k]
+    // pass 1: this segment's effect
+    uint32_t sum = 0, nexc = 0;
+    bool reset = false;
+    for (uint32_t k = g0; k < g1; ++k) {
+        const uint32_t d = b[k];
+        if (d == 255) {
+            ++nexc;
+            reset = true;
+            sum = 0;  // value restarts at the exception; the value itself is added below
+        } else {
+            sum += d;
+        }
+    }
+    // exclusive scan of exception counts within the group
+    uint32_t ex = nexc;
+    for (int o = 1; o < lpr; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, ex, o, lpr);
+        if (sub >= o) ex += v;
+    }
+    const uint32_t e_first = (live ? exc_start[r] : 0u) + ex - nexc;
+    // segment transform: reset -> exc_val[last] + sum, else in + sum
+    uint32_t val = sum + (reset ? exc_val[e_first + nexc - 1] : 0u);
+    bool rs = reset;
+    for (int o = 1; o < lpr; o <<= 1) {  // inclusive segmented scan
+        const uint32_t pv = __shfl_up_sync(0xFFFFFFFFu, val, o, lpr);
+        const bool pr = __shfl_up_sync(0xFFFFFFFFu, rs ? 1 : 0, o, lpr) != 0;
+        if (sub >= o && !rs) {
+            val += pv;
+            rs = pr;
+        }
+    }
+    // value entering this segment = inclusive result of the previous lane (+ first token)
+    const uint32_t first = live && t1 > t0 ? (static_cast<uint32_t>(bytes[t0 + r]) |
+                                              (static_cast<uint32_t>(bytes[t0 + r + 1]) << 8))
+                                           : 0u;
+    uint32_t prev_val = __shfl_up_sync(0xFFFFFFFFu, val, 1, lpr);
+    const bool prev_rs = __shfl_up_sync(0xFFFFFFFFu, rs ? 1 : 0, 1, lpr) != 0;
+    uint32_t v = sub == 0 ? first : (prev_rs ? prev_val : first + prev_val);
+    if (!live || t1 == t0) return;
+    if (sub == 0) out[t0] = first;
+    uint32_t e = e_first;
+    for (uint32_t k = g0; k < g1; ++k) {
+        const uint32_t d = b[k];
+        v = d == 255 ? exc_val[e++] : v + d;
+        out[t0 + 1 + k] = v;
+    }
+}
+
 struct Delta8Dev {
     uint8_t* bytes = nullptr;
     uint32_t* exc_start = nullptr;
@@ -305,9 +416,18 @@ Delta8Dev alloc_delta8(const Collection& c, cudaStream_t stream, uint64_t& h2d) 
 }
 
 void launch_decode(const Delta8Dev& d, const uint64_t* offsets, uint32_t* out, uint32_t r0, uint32_t r1,
-                   cudaStream_t stream, uint64_t& launches) {
+                   cudaStream_t stream, uint64_t& launches, double mean_size = 0) {
     if (r1 <= r0) return;
-    decode_delta8<<<(r1 - r0 + 127) / 128, 128, 0, stream>>>(d.bytes, offsets, d.exc_start, d.exc_val, out, r0, r1);
+    int lg = 0;  // about 6 gap bytes per lane
+    while (lg < 5 && (1 << lg) * 6.0 < mean_size) ++lg;
+    if (lg == 0) {
+        decode_delta8<<<(r1 - r0 + 127) / 128, 128, 0, stream>>>(d.bytes, offsets, d.exc_start, d.exc_val, out, r0,
+                                                                 r1);
+    } else {
+        const uint64_t threads = static_cast<uint64_t>(r1 - r0) << lg;
+        decode_delta8_sub<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(
+            d.bytes, offsets, d.exc_start, d.exc_val, out, r0, r1, lg);
+    }
     ++launches;
     CK(cudaGetLastError());
 }
@@ -346,7 +466,8 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
         Delta8Dev d = alloc_delta8(c, stream, tok_h2d);
         CK(cudaMemcpyAsync(d.bytes, c.tokens8.data(), c.tokens8.size(), cudaMemcpyHostToDevice, stream));
         tok_h2d += c.tokens8.size();
-        launch_decode(d, rep->offsets, rep->tokens, 0, static_cast<uint32_t>(n), stream, launches);
+        launch_decode(d, rep->offsets, rep->tokens, 0, static_cast<uint32_t>(n), stream, launches,
+                      n ? static_cast<double>(c.tokens.size()) / static_cast<double>(n) : 0.0);
         free_delta8(d, stream);
     } else if (narrow_tokens(c)) {
         // 16-bit upload, widened on the device
@@ -542,7 +663,13 @@ TcKernel tc_kernel() {
 //   fp4:  kind::mxf4, K = b + 64 e2m1 elements ((b+64)/2 bytes), 192-column tiles
 //   i8:   kind::i8, K = b + 32 bytes, 256-column tiles; with the level-2
 //         GEMM on 256-bit Xor sketches (l2gemm), 128-column tiles
-TcKernel tc_select(int words, bool l2gemm, bool fp4) {
+TcKernel tc_select(int words, bool l2gemm, bool fp4, bool noext = false) {
+    if (noext && !l2gemm && !fp4) {
+        switch (words) {
+            case 1: return tc_kernel<dev::kKindI8, 64, 0, 4, 6, 256>();
+            case 2: return tc_kernel<dev::kKindI8, 128, 0, 4, 4, 256>();
+        }
+    }
     const char* nenv = std::getenv("SSJB_TC_N");  // tile width override (experiments)
     const int nt = nenv && *nenv ? std::atoi(nenv) : 0;
     if (l2gemm) {
@@ -599,6 +726,7 @@ size_t operand_bytes(int words, bool fp4) { return fp4 ? 32 * words + 32 : 64 * 
 
 // Operand row bytes of a variant: level 1 | level 2 (int8, 256-bit sketch) | 16-byte size chunk.
 size_t operand_row(int words, int variant) {
+    if (variant == 4) return 64 * words;
     return operand_bytes(words, variant == 2) + (variant == 1 ? 64 * 4 + 32 : 0) + (variant == 3 ? 0 : 16);
 }
 
@@ -617,12 +745,22 @@ void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int w
     E.words = words;
     E.words2 = variant == 1 ? words2 : 0;
     E.fp4 = variant == 2 ? 1 : 0;
-    E.K1 = static_cast<int>(operand_bytes(words, variant == 2));
+    E.K1 = variant == 4 ? 64 * words : static_cast<int>(operand_bytes(words, variant == 2));
     E.K2 = variant == 1 ? 64 * words2 + 32 : 0;
-    E.with_size = variant == 3 ? 0 : 1;
+    E.with_size = (variant == 3 || variant == 4) ? 0 : 1;
     const int kct = (E.K1 + E.K2) / 16 + E.with_size;
     const uint64_t threads = static_cast<uint64_t>(rows - row0) * kct;
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
+    ++launches;
+    CK(cudaGetLastError());
+}
+
+// Per-column data of the no-extension variant for rows [row0, rows).
+void launch_column_info(const uint64_t* bits, int words, uint32_t row0, uint32_t rows, uint32_t* npc2,
+                        cudaStream_t s, uint64_t& launches) {
+    if (rows <= row0) return;
+    const uint32_t pairs = (rows - row0 + 1) / 2;
+    dev::column_info<<<(pairs + 255) / 256, 256, 0, s>>>(bits, words, row0, rows, npc2);
     ++launches;
     CK(cudaGetLastError());
 }
@@ -979,16 +1117,16 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     if (enabled && plan.bitmap.cutoff < 0) throw std::invalid_argument("bitmap cutoff must be >= 0");
 
     cudaEvent_t e0 = T.mark();
-    // plan tables
-    int32_t* d_maxham = A.alloc<int32_t>(plan.minov.size());
-    int32_t* d_minov = A.alloc<int32_t>(plan.minov.size());
-    uint32_t* d_wstart = A.alloc<uint32_t>(plan.window_start.size());
+    // plan tables (staged, sent with the tiling tables in one copy below)
+    TableStage stage;
+    int32_t* d_maxham = nullptr;
+    int32_t* d_minov = nullptr;
+    uint32_t* d_wstart = nullptr;
     std::vector<int32_t> maxham(plan.minov.size());
     for (size_t S = 0; S < maxham.size(); ++S) maxham[S] = static_cast<int32_t>(S) - 2 * plan.minov[S];
-    CK(cudaMemcpyAsync(d_maxham, maxham.data(), maxham.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_minov, plan.minov.data(), plan.minov.size() * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_wstart, plan.window_start.data(), plan.window_start.size() * 4, cudaMemcpyHostToDevice, s));
-    st.h2d_bytes += maxham.size() * 8 + plan.window_start.size() * 4;
+    stage.add(&d_maxham, maxham.data(), maxham.size() * 4);
+    stage.add(&d_minov, plan.minov.data(), plan.minov.size() * 4);
+    stage.add(&d_wstart, plan.window_start.data(), plan.window_start.size() * 4);
 
     // K1: sketches (+ level-2 Xor sketches), reused from a resident replica's cache
     const int W2 = enabled ? level2_words(W) : 0;
@@ -1020,6 +1158,11 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                      (kenv && *kenv ? std::string(kenv) == "fp4" : W >= 3);
     // int8 level-1-only filter on a CTA pair (M = 256): experimental, opt in with SSJB_TC2=1
     const bool use_tc2 = use_tc && !l2gemm && !fp4 && W <= 2 && env_u64("SSJB_TC2", 0) != 0;
+    // single-CTA int8 level-1 filter without the popcount extension (K = b, the
+    // -pc_j term added per column in the epilogue): 20% fewer MMA steps, but the
+    // extra epilogue work (and register pressure at 96 registers x 576 threads)
+    // outweighs them (C2 tau=0.7: 0.86 vs 0.69 ms) -- opt in with SSJB_NOEXT=1
+    const bool noext = use_tc && !l2gemm && !fp4 && !use_tc2 && W <= 2 && env_u64("SSJB_NOEXT", 0) != 0;
 
     // work items: (row tile, 4096-column chunk); the pair kernel takes 256-row tiles
     Tiling tl;
@@ -1028,15 +1171,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_item_tile = nullptr;
     auto set_tiling = [&](uint32_t tile_rows) {
         tl = make_tiling(c, plan, tile_rows);
-        d_item_base = A.alloc<uint64_t>(tl.item_base.size());
-        d_col_lo = A.alloc<uint32_t>(tl.col_lo.size());
-        d_item_tile = A.alloc<uint32_t>(tl.item_tile.size());
-        CK(cudaMemcpyAsync(d_item_base, tl.item_base.data(), tl.item_base.size() * 8, cudaMemcpyHostToDevice, s));
-        if (tl.ntiles)
-            CK(cudaMemcpyAsync(d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4, cudaMemcpyHostToDevice, s));
-        if (!tl.item_tile.empty())
-            CK(cudaMemcpyAsync(d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4, cudaMemcpyHostToDevice, s));
-        st.h2d_bytes += tl.item_base.size() * 8 + tl.col_lo.size() * 4 + tl.item_tile.size() * 4;
+        stage.add(&d_item_base, tl.item_base.data(), tl.item_base.size() * 8);
+        stage.add(&d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4);
+        stage.add(&d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4);
+        stage.flush(A, s, st.h2d_bytes);
     };
     set_tiling(use_tc2 ? 2 * dev::kRowTile : dev::kRowTile);
 
@@ -1110,7 +1248,12 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         sk = fresh;
         built = true;
     }
-    const int variant = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : (use_tc2 ? 3 : 0)));
+    const int variant = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : (use_tc2 ? 3 : (noext ? 4 : 0))));
+    if (variant == 4 && !sk->npc2) {
+        sk->npc2 = static_cast<uint32_t*>(get(static_cast<size_t>(n_pad / 2 + 1) * 4));
+        if (!streamed) launch_column_info(sk->bits, W, 0, n_pad, sk->npc2, s, st.launches);
+        built = true;
+    }
     if (variant >= 0 && !sk->opA[variant]) {
         const size_t rowb = operand_row(W, variant);
         sk->opA[variant] = static_cast<uint8_t*>(get(static_cast<size_t>(n_pad) * rowb));
@@ -1214,7 +1357,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     TcKernel tck{nullptr, 0};
     bool tc2_active = use_tc2;
     if (use_tc) {
-        tck = use_tc2 ? tc2_select(W) : tc_select(W, l2gemm, fp4);
+        tck = use_tc2 ? tc2_select(W) : tc_select(W, l2gemm, fp4, noext);
         set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
         TP.opA = d_opA;
         TP.opB = d_opB;
@@ -1237,6 +1380,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.row_end = static_cast<uint32_t>(plan.row_end);
         TP.cutoff = FP.cutoff;
         TP.neg1 = -1;
+        TP.npc2 = noext ? sk->npc2 : nullptr;
         TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
         if (TP.debug & 2) {
             TP.trace = A.alloc<unsigned long long>(2048 + 2 * 8192);
@@ -1388,11 +1532,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     {
         cudaEvent_t a = T.mark();
         if (streamed) {
-            const int variant_s = !use_tc ? -1 : (l2gemm ? 1 : (fp4 ? 2 : (use_tc2 ? 3 : 0)));
+            const int variant_s = variant;
+            // per-chunk filter launches (SSJB_STREAM=2) overlap more of the transfer
+            // but pay a launch tail per chunk; by default only the ingest kernels
+            // (decode, sketches, operands) are chunked
+            const bool stream_filter = env_u64("SSJB_STREAM", 1) >= 2;
             for (size_t k = 0; k < ingest.size(); ++k) {
                 const IngestChunk& ch = ingest[k];
                 CK(cudaStreamWaitEvent(s, ch.ev, 0));
-                if (ingest_d8.bytes) launch_decode(ingest_d8, rep->offsets, rep->tokens, ch.r0, ch.r1, s, st.launches);
+                if (ingest_d8.bytes)
+                    launch_decode(ingest_d8, rep->offsets, rep->tokens, ch.r0, ch.r1, s, st.launches,
+                                  static_cast<double>(c.tokens.size()) / static_cast<double>(std::max<size_t>(n, 1)));
                 if (ingest_t16 && ch.t1 > ch.t0) {
                     const uint64_t w0 = ch.t0 & ~uint64_t(3);  // 8-byte aligned vector loads
                     const uint64_t cnt = ch.t1 - w0;
@@ -1406,10 +1556,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 const bool last = k + 1 == ingest.size();
                 launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, d_opA, d_opB, last ? n_pad : ch.r1, variant_s,
                               s, st.launches, ch.r0);
-                const uint32_t ta = ch.r0 / tl.tile_rows;
-                const uint32_t tb2 = last ? tl.ntiles : ch.r1 / tl.tile_rows;
-                launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
+                if (variant_s == 4)
+                    launch_column_info(sk->bits, W, ch.r0, last ? n_pad : ch.r1, sk->npc2, s, st.launches);
+                if (stream_filter) {  // filter work items of this chunk's row tiles
+                    const uint32_t ta = ch.r0 / tl.tile_rows;
+                    const uint32_t tb2 = last ? tl.ntiles : ch.r1 / tl.tile_rows;
+                    launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
+                }
             }
+            if (!stream_filter) launch_filter(0, total_items, 0);  // one persistent launch after ingest
         } else {
             launch_filter(0, total_items, 0);
         }

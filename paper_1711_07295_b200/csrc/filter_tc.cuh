@@ -59,6 +59,7 @@ struct TcParams {
     uint32_t row_begin, row_end;
     int64_t cutoff;
     int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
+    const uint32_t* npc2;      // no-extension int8 operands: -pc of columns 2k, 2k+1 as s16x2
     int debug;                 // bit 0: skip the epilogue math (pipeline probe)
     unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
 };
@@ -304,6 +305,14 @@ __device__ __forceinline__ uint32_t stage_size(const uint8_t* stage, int col) {
     return *reinterpret_cast<const uint32_t*>(stage + ((col >> 3) * KCT + (KCT - 1)) * 128 + (col & 7) * 16);
 }
 
+// Column size of a tile column: from the side ring (no-extension operands) or
+// from the size chunk of the staged operand rows.
+template <bool kNoExt, int KCT>
+__device__ __forceinline__ uint32_t tile_col_size(const uint32_t* side, const uint8_t* stage, int col) {
+    if constexpr (kNoExt) return side[col];
+    else return stage_size<KCT>(stage, col);
+}
+
 // Non-uniform group (column sizes change inside it): per-column threshold.
 template <int KIND, int KCT>
 __device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int base, const int32_t* maxham,
@@ -369,18 +378,26 @@ struct TcItem {
 // (used when K2 == 0); NS: B stages; NT: columns per MMA tile.
 template <int KIND, int KA, int K2, int W2, int NS, int NT>
 struct TcLayout {
-    static constexpr int kWords = KIND == kKindI8 ? (KA - 32) / 64 : (KA - 32) / 32;  // level-1 sketch words
+    // int8 operands without the popcount extension (K = b): D = 2<b_i,b_j>, the
+    // -pc_j term is added in the epilogue from a per-stage s16x2 array
+    static constexpr bool kNoExt = KIND == kKindI8 && K2 == 0 && KA % 64 == 0;
+    static constexpr int kWords = kNoExt ? KA / 64 : (KIND == kKindI8 ? (KA - 32) / 64 : (KA - 32) / 32);
+    // no-extension operands carry no size chunk: the column sizes and -pc pairs of
+    // each tile go to a separate, deeper "side" ring, so a B stage is released as
+    // soon as its MMAs complete (the epilogue never holds it)
+    static constexpr int kSide = kNoExt ? NT * 4 + NT * 2 : 0;  // sizes u32[NT] | -pc pairs u32[NT/2]
+    static constexpr int NE = kNoExt ? 2 * NS : 1;              // side-ring slots
     static constexpr int kEpiWarps = NT == 192 ? 12 : 16;      // 3 or 4 per TMEM lane quarter
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
-    static constexpr int kRow = KA + K2 + 16;                  // operand row: L1 | L2 | size chunk
+    static constexpr int kRow = KA + K2 + (kNoExt ? 0 : 16);   // operand row: L1 | L2 | size chunk
     static constexpr int kKCT = kRow / 16;                     // 16-byte chunks per row
     static constexpr int kSbo = kKCT * 128;                    // stride between 8-row core groups
     static constexpr int kA = 128 * kRow;                      // one A slot
     static constexpr int kB = NT * kRow;                       // one B stage: a single bulk copy
     static constexpr int kAslots = K2 ? 1 : 2;
     static constexpr int kQueue = kEpiWarps * kTcQueue * 8;
-    static constexpr int kBytes = kAslots * kA + NS * kB + kQueue;
+    static constexpr int kBytes = kAslots * kA + NS * kB + (kNoExt ? NE * kSide : 0) + kQueue;
     // accumulator slots in flight: as many NT-column slots (x2 with the level-2
     // GEMM) as TMEM holds next to the fp4 scale factors, at most 4
     static constexpr int kAccSlots = (((KIND == kKindF4 ? 384 : 512) / (NT * (K2 ? 2 : 1))) < 4)
@@ -402,9 +419,11 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;                                   // [2][kA]
     uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
-    uint2* sQ = reinterpret_cast<uint2*>(sB + NS * L::kB);  // [8][kTcQueue]
+    uint8_t* sSide = sB + NS * L::kB;                     // [NE][kSide] (no-extension operands)
+    uint2* sQ = reinterpret_cast<uint2*>(sSide + (L::kNoExt ? L::NE * L::kSide : 0));  // [8][kTcQueue]
     __shared__ __align__(8) uint64_t item_full[2], item_empty[2], a_full[2], a_empty[2];
     __shared__ __align__(8) uint64_t b_full[NS], b_empty[NS], acc_full[L::kAccSlots], acc_empty[L::kAccSlots];
+    __shared__ __align__(8) uint64_t e_full[L::NE], e_empty[L::NE];
     __shared__ TcItem items[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t s_maxham[kTcLut];  // maxham[] when it fits (2*max_size + 1 <= kTcLut)
@@ -432,9 +451,13 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             mbar_init(&acc_full[s], 1);
             mbar_init(&acc_empty[s], kTcEpiWarps);
         }
+        for (int s = 0; s < L::NE; ++s) {
+            mbar_init(&e_full[s], 1);
+            mbar_init(&e_empty[s], kTcEpiWarps);
+        }
         for (int s = 0; s < NS; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], 1 + kTcEpiWarps);
+            mbar_init(&b_empty[s], L::kNoExt ? 1 : 1 + kTcEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -497,6 +520,14 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     uint8_t* dst = sB + st * L::kB;
+                    if constexpr (L::kNoExt) {
+                        const int se = tseq % L::NE;
+                        mbar_spin(&e_empty[se], ((tseq / L::NE) & 1) ^ 1);
+                        uint8_t* side = sSide + se * L::kSide;
+                        mbar_expect_tx(&e_full[se], L::kSide);
+                        tma_load_1d(side, P.sizes + col, NT * 4, &e_full[se]);
+                        tma_load_1d(side + NT * 4, P.npc2 + col / 2, NT * 2, &e_full[se]);
+                    }
                     mbar_expect_tx(&b_full[st], L::kB);
                     tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
                     if (t == 0) {
@@ -568,6 +599,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         int qlen = 0;
         uint32_t iseq = 0;
         uint32_t st_idx = 0, st_phase = 0, acc_idx = 0, acc_phase = 0;  // ring positions
+        uint32_t se_idx = 0, se_phase = 0;                                 // side ring (no-extension)
         uint32_t tile_seq = 0;
         const uint32_t bfull_u32 = smem_u32(&b_full[0]), bempty_u32 = smem_u32(&b_empty[0]);
         const uint32_t accfull_u32 = smem_u32(&acc_full[0]), accempty_u32 = smem_u32(&acc_empty[0]);
@@ -618,16 +650,19 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             int cim1 = 0, cim1_2 = 0, cim1_key = 0;
             for (uint32_t t = 0; t < info.ntiles; ++t) {
                 const int st = static_cast<int>(st_idx), as = static_cast<int>(acc_idx);
-                mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
+                if constexpr (L::kNoExt) mbar_wait_u32(smem_u32(&e_full[0]) + 8 * se_idx, se_phase);
+                else mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
                 mbar_wait_u32(accfull_u32 + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512) P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
                 ++tile_seq;
                 const uint8_t* stage = sB + st * L::kB;
+                const uint32_t* side_sz = reinterpret_cast<const uint32_t*>(sSide + se_idx * L::kSide);
+                const uint32_t* sNpc = side_sz + NT;  // -pc pairs of the tile's columns
                 const int cw = part * L::kColsPerWarp;               // this warp's first column
                 const uint32_t wbase = info.c0 + t * NT + cw;
-                const uint32_t szw0 = stage_size<L::kKCT>(stage, cw);
-                const uint32_t szw1 = stage_size<L::kKCT>(stage, cw + L::kColsPerWarp - 1);
+                const uint32_t szw0 = tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw);
+                const uint32_t szw1 = tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw + L::kColsPerWarp - 1);
                 // fast path: every group of this warp's range is inside all 32
                 // windows and of one column size (the bulk of the pair space)
                 const bool fast = szw0 == szw1 && wbase >= lo_max && wbase + L::kColsPerWarp <= hi_min;
@@ -663,6 +698,17 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         uint32_t d[32];
                         tmem_ld64_pack16(tmem_base + lane_base + as * NT + cw, d);
                         const int c16 = max(cim1, -32768);
+                        if constexpr (L::kNoExt) {  // D = 2<b_i,b_j>: subtract pc_j per column first
+                            const uint4* np = reinterpret_cast<const uint4*>(sNpc + cw / 2);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const uint4 v = np[k];
+                                d[4 * k] = __vadd2(d[4 * k], v.x);
+                                d[4 * k + 1] = __vadd2(d[4 * k + 1], v.y);
+                                d[4 * k + 2] = __vadd2(d[4 * k + 2], v.z);
+                                d[4 * k + 3] = __vadd2(d[4 * k + 3], v.w);
+                            }
+                        }
                         if (__any_sync(0xFFFFFFFFu, bypass || any_above16(d, c16))) {
                             uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
                             if (!bypass) masks16(d, c16, m0, m1);
@@ -693,8 +739,19 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         uint32_t d[16], d2[16];
                         tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cl, d);
                         if constexpr (K2 > 0) tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
-                        const uint32_t colsz = fast ? 0u : stage_size<L::kKCT>(stage, cl + lane);
+                        const uint32_t colsz = fast ? 0u : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cl + lane);
                         tmem_wait_ld();
+                        if constexpr (L::kNoExt) {  // D - pc_j per column
+                            const uint4* np = reinterpret_cast<const uint4*>(sNpc + cl / 2);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint4 v = np[k];
+                                d[4 * k] = __vadd2(d[4 * k], v.x);
+                                d[4 * k + 1] = __vadd2(d[4 * k + 1], v.y);
+                                d[4 * k + 2] = __vadd2(d[4 * k + 2], v.z);
+                                d[4 * k + 3] = __vadd2(d[4 * k + 3], v.w);
+                            }
+                        }
                         // lowest threshold over the group's size runs (pre-test)
                         int cmin = cim1;
                         if (!fast) {
@@ -775,11 +832,16 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 if (lane == 0) {
                     if (P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
                     mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
-                    mbar_arrive_u32(bempty_u32 + 8 * st_idx);
+                    if constexpr (L::kNoExt) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
+                    else mbar_arrive_u32(bempty_u32 + 8 * st_idx);
                 }
                 if (++st_idx == NS) {
                     st_idx = 0;
                     st_phase ^= 1u;
+                }
+                if (++se_idx == L::NE) {
+                    se_idx = 0;
+                    se_phase ^= 1u;
                 }
                 if (++acc_idx == L::kAccSlots) {
                     acc_idx = 0;
@@ -898,6 +960,21 @@ __global__ void expand_operands(ExpandParams P) {
     const uint64_t off = ((static_cast<uint64_t>(r / 8) * KCT + c) * 8 + (r % 8)) * 16;
     *reinterpret_cast<uint4*>(P.opA + off) = make_uint4(a[0], a[1], a[2], a[3]);
     *reinterpret_cast<uint4*>(P.opB + off) = make_uint4(b[0], b[1], b[2], b[3]);
+}
+
+// Per-column data of the no-extension int8 operands: npc2[k] = (-pc(2k), -pc(2k+1))
+// as s16x2 (padding rows have empty sketches: pc = 0).
+__global__ void column_info(const uint64_t* bits, int words, uint32_t row0, uint32_t rows, uint32_t* npc2) {
+    const uint32_t k = row0 / 2 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (2 * k >= rows) return;
+    int pc[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t r = 2 * k + h;
+        if (r >= rows) break;
+        for (int w = 0; w < words; ++w) pc[h] += __popcll(bits[static_cast<uint64_t>(r) * words + w]);
+    }
+    npc2[k] = (static_cast<uint32_t>(-pc[0]) & 0xFFFFu) | (static_cast<uint32_t>(-pc[1]) << 16);
 }
 
 }  // namespace dev

@@ -54,15 +54,17 @@ def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
         assert sha(store) == e["sha256"], e
 
 
-FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "popc", "tc-l2gemm"]
+FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "tc-i8-noext", "popc", "tc-l2gemm"]
 
 
 def set_filter(monkeypatch, flavour):
-    """tcgen05 fp4 / int8 CTA-pair / int8 single-CTA / level-2 GEMM, or POPC."""
+    """tcgen05 fp4 / int8 CTA-pair / int8 single-CTA (with the popcount extension
+    block, or K = b) / level-2 GEMM, or POPC."""
     monkeypatch.setenv("SSJB_FILTER", "popc" if flavour == "popc" else "tc")
     monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour == "tc-l2gemm" else "0")
     monkeypatch.setenv("SSJB_TC_KIND", "i8" if flavour.startswith("tc-i8") else "fp4")
     monkeypatch.setenv("SSJB_TC2", "1" if flavour == "tc-i8-pair" else "0")
+    monkeypatch.setenv("SSJB_NOEXT", "1" if flavour == "tc-i8-noext" else "0")
 
 
 @pytest.mark.parametrize("flavour", FILTERS)
@@ -75,11 +77,14 @@ def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
         assert_same(rep, e, flavour)
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("flavour", ["tc-i8", "tc-i8-pair", "tc-fp4"])
-def test_streamed_ingest(lib, golden, colls, flavour, monkeypatch):
+def test_streamed_ingest(lib, golden, colls, flavour, mode, monkeypatch):
     """Every fixture with the collection streamed to the device in 3 row chunks
-    (sketches + filter work of a chunk overlap the next chunk's transfer)."""
+    (decode + sketches + operands of a chunk overlap the next chunk's transfer;
+    mode 2 also launches each chunk's filter work items as it lands)."""
     set_filter(monkeypatch, flavour)
+    monkeypatch.setenv("SSJB_STREAM", mode)
     monkeypatch.setenv("SSJB_STREAM_MIN_ROWS", "1")
     monkeypatch.setenv("SSJB_STREAM_CHUNKS", "3")
     for e in golden["joins"]:
