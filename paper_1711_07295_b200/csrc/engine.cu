@@ -651,12 +651,14 @@ struct TcKernel {
     void (*fn)(dev::TcParams);
     int smem;
     int threads;
+    int nt = 256;    // columns per MMA tile
+    int parts = 4;   // epilogue column parts per tile (epilogue warps / 4)
 };
 
 template <int KIND, int KA, int K2, int W2, int NS, int NT>
 TcKernel tc_kernel() {
     using L = dev::TcLayout<KIND, KA, K2, W2, NS, NT>;
-    return TcKernel{dev::filter_tc_kernel<KIND, KA, K2, W2, NS, NT>, L::kBytes, L::kThreads};
+    return TcKernel{dev::filter_tc_kernel<KIND, KA, K2, W2, NS, NT>, L::kBytes, L::kThreads, NT, L::kEpiWarps / 4};
 }
 
 // Tensor-core filter instantiations: level-1 width b = 64*words.
@@ -1309,6 +1311,18 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         !naive && (ic_bytes <= (uint64_t(1) << 30) ||
                    (ic_bytes <= (uint64_t(16) << 30) && static_cast<double>(ic_bytes) <= 0.3 * double(free_b)));
     uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * tl.tile_rows) : nullptr;
+    // second level: per (item, filter tile, column part, row) counts written by the
+    // tcgen05 epilogue (plain u16 stores, no memset: every slot of a processed
+    // tile is written), so a saturated row's rescan covers one filter tile
+    // instead of a 4096-column chunk (32 tiles per item covers widths >= 128)
+    constexpr uint32_t kTilesPerItem = dev::kColChunk / 128;
+    const uint64_t tc_bytes = n_items * kTilesPerItem * 4 * dev::kRowTile * 2;
+    // (kept for the dense regime only -- the level-2 GEMM joins, where most rows
+    // saturate; elsewhere the stores cost the filter more than the rescan saves)
+    uint16_t* d_tile_counts = keep_item_counts && use_tc && l2gemm && !use_tc2 && tl.tile_rows == dev::kRowTile &&
+                                      tc_bytes <= std::min<uint64_t>(uint64_t(2) << 30, free_b / 5)
+                                  ? A.alloc<uint16_t>(n_items * kTilesPerItem * 4 * dev::kRowTile)
+                                  : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
     SB.ka = A.alloc<unsigned long long>(res_cap);
@@ -1373,6 +1387,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.surv = d_surv;
         TP.rowcnt = d_rowcnt;
         TP.item_counts = d_item_counts;
+        TP.tile_counts = d_tile_counts;
+        TP.tiles_per_item = kTilesPerItem;
         TP.ctl = d_ctl;
         TP.surv_cap = surv_cap;
         TP.ntiles = tl.ntiles;
@@ -1494,6 +1510,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.rowcnt = d_rowcnt;
             RP.item_counts = d_item_counts;
             RP.tile_rows = tl.tile_rows;
+            RP.tile_counts = use_tc ? TP.tile_counts : nullptr;
+            RP.tiles_per_item = kTilesPerItem;
+            RP.tile_cols = static_cast<uint32_t>(tck.nt);
+            RP.tile_parts = static_cast<uint32_t>(tck.parts);
             RP.item_base = d_item_base;
             RP.tile_col_lo = d_col_lo;
             RP.jstar = d_jstar;
@@ -1529,6 +1549,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // K4 chained on the stream with a single host synchronisation.
     double ms_filter = 0, ms_verify = 0;
     bool done = false;
+    const auto t_launch = Clock::now();  // host setup ends: the first filter launch
+    auto t_synced = t_launch;
     {
         cudaEvent_t a = T.mark();
         if (streamed) {
@@ -1583,7 +1605,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         CK(cudaMemcpyAsync(keys.data(), SB.ka, kSmallSort * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ov.data(), SB.va, kSmallSort * 4, cudaMemcpyDeviceToHost, s));
         cudaEvent_t dl = T.mark();
+        const auto t_enq = Clock::now();
         CK(cudaStreamSynchronize(s));
+        t_synced = Clock::now();
+        if (std::getenv("SSJB_HOST_TIMING"))
+            std::fprintf(stderr, "[host] setup %.3f ms, enqueue %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(t_launch - t_start).count(),
+                         std::chrono::duration<double, std::milli>(t_enq - t_launch).count());
         if (h_ctl.survivors <= surv_cap) {
             done = true;
             ms_filter = Timer::ms(a, b);
@@ -1742,6 +1770,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     out.index_s = (st.ms_upload + st.ms_build) * 1e-3;
     out.candidates_s = (st.ms_filter + st.ms_rescan) * 1e-3;
     const double total = std::chrono::duration<double>(Clock::now() - t_start).count();
+    if (std::getenv("SSJB_HOST_TIMING"))
+        std::fprintf(stderr, "[host] after sync %.3f ms, total %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(Clock::now() - t_synced).count(), total * 1e3);
     out.verify_s = std::max(0.0, total - out.index_s - out.candidates_s);
 }
 

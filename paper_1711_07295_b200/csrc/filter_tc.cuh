@@ -52,6 +52,9 @@ struct TcParams {
     uint2* surv;
     uint32_t* rowcnt;
     uint32_t* item_counts;     // per (item, row-in-tile), u32 (two column halves add)
+    uint16_t* tile_counts;     // per (item, tile-in-item, column part, row-in-tile), or null: the
+                               // rescan's 2nd level; every slot of a processed tile is written
+    uint32_t tiles_per_item;   // slots per item (>= ceil(kColChunk / NT))
     Control* ctl;
     unsigned long long surv_cap;
     unsigned long long item_begin, item_end;
@@ -645,7 +648,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 lo_max = max(lo_max, __shfl_xor_sync(0xFFFFFFFFu, lo_max, o));
                 hi_min = min(hi_min, __shfl_xor_sync(0xFFFFFFFFu, hi_min, o));
             }
-            uint32_t cnt = 0;
+            uint32_t cnt = 0, cnt_tile0 = 0;
             uint32_t last_sz = 0xFFFFFFFFu;  // cim1 cache: sizes are sorted, so it rarely changes
             int cim1 = 0, cim1_2 = 0, cim1_key = 0;
             for (uint32_t t = 0; t < info.ntiles; ++t) {
@@ -826,6 +829,11 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         m = bypass ? rm : (m & rm);
                     }
                     finish(cl, gbase, m, uni);
+                }
+                if (P.tile_counts) {  // this warp's survivors in this tile, per row (rescan locator)
+                    P.tile_counts[((info.item * P.tiles_per_item + t) * 4 + part) * kRowTile + rit] =
+                        static_cast<uint16_t>(cnt - cnt_tile0);
+                    cnt_tile0 = cnt;
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();

@@ -570,6 +570,8 @@ struct RescanParams {
     int bypass_all;
     uint32_t tile_rows;           // rows per work item (128, or 256 for the CTA-pair filter)
     int maxham_len;
+    const uint16_t* tile_counts;  // per (item, tile, part, row) survivors (tcgen05 filter), or null
+    uint32_t tiles_per_item, tile_cols, tile_parts;
 };
 
 constexpr int kRescanLut = 4096;  // maxham[] entries staged in shared memory
@@ -607,6 +609,19 @@ __global__ void __launch_bounds__(256) rescan_saturated(RescanParams P) {
                     const uint32_t c0 = P.tile_col_lo[tile] + static_cast<uint32_t>(it - ib) * kColChunk;
                     start = max(j0, c0);
                     stop = min(i, c0 + kColChunk);
+                    if (P.tile_counts) {  // narrow to the filter tile holding it
+                        for (uint32_t tt = 0; tt < P.tiles_per_item; ++tt) {
+                            uint32_t tc = 0;
+                            for (uint32_t pp = 0; pp < P.tile_parts; ++pp)
+                                tc += P.tile_counts[((it * P.tiles_per_item + tt) * 4 + pp) * P.tile_rows + t];
+                            if (seen + tc >= P.capacity) {
+                                start = max(j0, c0 + tt * P.tile_cols);
+                                stop = min(stop, c0 + (tt + 1) * P.tile_cols);
+                                break;
+                            }
+                            seen += tc;
+                        }
+                    }
                     break;
                 }
                 seen += cc;
