@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "filter_tc.cuh"
 #include "filter_tc2.cuh"
+#include "filter_tcm.cuh"
 
 namespace ssjb {
 
@@ -716,6 +717,21 @@ TcKernel tc2_kernel() {
     return TcKernel{dev::filter_tc2_kernel<KA, NS>, L::kBytes, L::kThreads};
 }
 
+// Single-CTA int8 filter with two row tiles per staged column tile (filter_tcm.cuh).
+template <int KA, int NS>
+TcKernel tcm_kernel() {
+    using L = dev::TcmLayout<KA, NS>;
+    return TcKernel{dev::filter_tcm_kernel<KA, NS>, L::kBytes, L::kThreads, 256, 4};
+}
+
+TcKernel tcm_select(int words) {
+    switch (words) {
+        case 1: return tcm_kernel<96, 3>();
+        case 2: return tcm_kernel<160, 2>();
+    }
+    throw DeviceError("no two-row-tile filter instantiation for this width");
+}
+
 TcKernel tc2_select(int words) {
     switch (words) {
         case 1: return tc2_kernel<96, 8>();
@@ -1165,6 +1181,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // extra epilogue work (and register pressure at 96 registers x 576 threads)
     // outweighs them (C2 tau=0.7: 0.86 vs 0.69 ms) -- opt in with SSJB_NOEXT=1
     const bool noext = use_tc && !l2gemm && !fp4 && !use_tc2 && W <= 2 && env_u64("SSJB_NOEXT", 0) != 0;
+    // two row tiles per staged column tile (256-row work items, one CTA)
+    const bool use_tcm = use_tc && !l2gemm && !fp4 && !use_tc2 && !noext && W <= 2 && env_u64("SSJB_TCM", 1) != 0;
 
     // work items: (row tile, 4096-column chunk); the pair kernel takes 256-row tiles
     Tiling tl;
@@ -1178,7 +1196,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         stage.add(&d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4);
         stage.flush(A, s, st.h2d_bytes);
     };
-    set_tiling(use_tc2 ? 2 * dev::kRowTile : dev::kRowTile);
+    set_tiling(use_tc2 || use_tcm ? 2 * dev::kRowTile : dev::kRowTile);
 
     // the collection on the device: a pinned replica, or uploaded for this join --
     // streamed in row chunks (overlapping the first chunks' sketches and filter
@@ -1371,7 +1389,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     TcKernel tck{nullptr, 0};
     bool tc2_active = use_tc2;
     if (use_tc) {
-        tck = use_tc2 ? tc2_select(W) : tc_select(W, l2gemm, fp4, noext);
+        tck = use_tc2 ? tc2_select(W) : (use_tcm ? tcm_select(W) : tc_select(W, l2gemm, fp4, noext));
         set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
         TP.opA = d_opA;
         TP.opB = d_opB;
@@ -1640,8 +1658,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 uint8_t* b1 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * rowb);
                 launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, a1, b1, n_pad, 1, s, st.launches);
                 l2gemm = true;
-                if (tc2_active) {
-                    // the single-CTA kernels take 128-row work items
+                if (tl.tile_rows != dev::kRowTile) {
+                    // the level-2 GEMM kernel takes 128-row work items
                     tc2_active = false;
                     set_tiling(dev::kRowTile);
                     total_items = n_items = tl.item_base.back();
