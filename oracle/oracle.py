@@ -46,6 +46,11 @@ def lib():
                                              C.POINTER(C.c_size_t), C.POINTER(_Counters)]
         L.oracle_naive_join.argtypes = [P, P, C.c_size_t, C.c_int64, C.c_int64, C.POINTER(P),
                                         C.POINTER(C.c_size_t), C.POINTER(_Counters)]
+        L.oracle_naive_join_sim.argtypes = [P, P, C.c_size_t, P, P, C.c_size_t, C.c_int, C.c_int,
+                                            C.c_int64, C.c_int64, C.POINTER(P),
+                                            C.POINTER(C.c_size_t), C.POINTER(_Counters)]
+        L.oracle_required_overlap_sim.argtypes = [C.c_int] + [C.c_int64] * 4
+        L.oracle_required_overlap_sim.restype = C.c_int64
         L.oracle_build_bitmaps.argtypes = [P, P, C.c_size_t, C.c_int, C.c_int, C.c_int, P]
         L.oracle_build_row.argtypes = [P, P, C.c_size_t, C.c_int, C.c_int, C.c_int]
         L.oracle_canonicalize.argtypes = [P, P, C.c_size_t, P, P]
@@ -103,6 +108,24 @@ def naive_join(tokens, offsets, p, q):
                                C.byref(n), C.byref(cnt)) != 0:
         raise RuntimeError("oracle_naive_join failed")
     return _take_pairs(ptr, n.value), {f: int(getattr(cnt, f)) for f in COUNTER_FIELDS}
+
+
+def naive_join_sim(tokens, offsets, sim, p, q, s_tokens=None, s_offsets=None):
+    """NAIVE self-join (s_* None) or R x S join with any similarity
+    (reference src/join.cpp:91-126; sim 0 overlap, 1 jaccard, 2 cosine, 3 dice)."""
+    t, o = _csr(tokens, offsets)
+    self_join = s_tokens is None
+    st, so = (t, o) if self_join else _csr(s_tokens, s_offsets)
+    ptr, n, cnt = C.c_void_p(), C.c_size_t(), _Counters()
+    if lib().oracle_naive_join_sim(t.ctypes.data, o.ctypes.data, len(o) - 1, st.ctypes.data,
+                                   so.ctypes.data, len(so) - 1, 1 if self_join else 0, sim, p, q,
+                                   C.byref(ptr), C.byref(n), C.byref(cnt)) != 0:
+        raise RuntimeError("oracle_naive_join_sim failed")
+    return _take_pairs(ptr, n.value), {f: int(getattr(cnt, f)) for f in COUNTER_FIELDS}
+
+
+def required_overlap_sim(sim, p, q, sr, ss):
+    return int(lib().oracle_required_overlap_sim(sim, p, q, sr, ss))
 
 
 def build_bitmaps(tokens, offsets, method, width, hash=0):

@@ -262,6 +262,78 @@ int oracle_naive_join(const uint32_t* tokens, const uint64_t* offsets, size_t n,
     return 0;
 }
 
+/* isqrt_ceil of src/rational.cpp:51-71 (Newton from a long double estimate,
+ * exact correction) */
+static uint64_t isqrt_ceil_u128(unsigned __int128 v) {
+    if (v == 0) return 0;
+    unsigned __int128 m = v - 1, x;
+    if (m == 0) return 1;
+    x = (unsigned __int128)sqrtl((long double)m);
+    if (x == 0) x = 1;
+    for (int i = 0; i < 6; ++i) {
+        unsigned __int128 nx = (x + m / x) >> 1;
+        if (nx == x) break;
+        x = nx;
+    }
+    while (x * x > m) --x;
+    while ((x + 1) * (x + 1) <= m) ++x;
+    return (uint64_t)x + 1;
+}
+
+int64_t oracle_required_overlap_sim(int sim, int64_t p, int64_t q, int64_t sr, int64_t ss) {
+    /* equivalent_overlap (src/similarity.cpp:93-111) for Overlap 0 / Jaccard 1 /
+     * Cosine 2 / Dice 3, then the max(1, .) clamp (:113-115) */
+    int64_t o = 0;
+    switch (sim) {
+        case 0: o = p; break;
+        case 1: o = ceil_div((i128)p * (sr + ss), (i128)p + q); break;
+        case 2: {
+            unsigned __int128 target = (unsigned __int128)p * (unsigned __int128)p;
+            target *= (unsigned __int128)sr * (unsigned __int128)ss;
+            o = ceil_div((i128)isqrt_ceil_u128(target), (i128)q);
+            break;
+        }
+        case 3: o = ceil_div((i128)p * (sr + ss), (i128)2 * q); break;
+        default: return -1;
+    }
+    return o < 1 ? 1 : o;
+}
+
+int oracle_naive_join_sim(const uint32_t* rt, const uint64_t* ro, size_t rn, const uint32_t* st,
+                          const uint64_t* so, size_t sn, int self_join, int sim, int64_t p, int64_t q,
+                          oracle_pair** pairs, size_t* pair_count, oracle_counters* counters) {
+    /* src/join.cpp:91-126: self (pairs (i, j), i < j) or R x S (pairs (r, s)) */
+    memset(counters, 0, sizeof(*counters));
+    pair_vec out = {0, 0, 0};
+    if (self_join) {
+        st = rt;
+        so = ro;
+        sn = rn;
+    }
+    for (size_t a = 0; a < (self_join ? sn : rn); ++a) {
+        size_t bend = self_join ? a : sn;
+        for (size_t b = 0; b < bend; ++b) {
+            /* self: r = b (earlier), s = a; RS: r = a, s = b */
+            size_t ri = self_join ? b : a, si = self_join ? a : b;
+            int64_t nr = (int64_t)(ro[ri + 1] - ro[ri]), ns = (int64_t)(so[si + 1] - so[si]);
+            int64_t ov, minov = oracle_required_overlap_sim(sim, p, q, nr, ns);
+            counters->candidates += 1;
+            counters->verified += 1;
+            if (oracle_verify(rt + ro[ri], (size_t)nr, st + so[si], (size_t)ns, minov, &ov)) {
+                counters->matched += 1;
+                if (push_pair(&out, (uint32_t)ri, (uint32_t)si, ov)) {
+                    free(out.data);
+                    return -1;
+                }
+            }
+        }
+    }
+    qsort(out.data, out.size, sizeof(oracle_pair), pair_cmp);
+    *pairs = out.data;
+    *pair_count = out.size;
+    return 0;
+}
+
 static int u32_cmp(const void* x, const void* y) {
     uint32_t a = *(const uint32_t*)x, b = *(const uint32_t*)y;
     return a < b ? -1 : (a > b ? 1 : 0);

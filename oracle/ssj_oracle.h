@@ -79,6 +79,16 @@ int oracle_naive_join(const uint32_t* tokens, const uint64_t* offsets, size_t n,
                       int64_t q, oracle_pair** pairs, size_t* pair_count,
                       oracle_counters* counters);
 
+/* required_overlap for sim 0 Overlap / 1 Jaccard / 2 Cosine / 3 Dice
+ * -- reference src/similarity.cpp:93-115 (Cosine via isqrt_ceil, src/rational.cpp:51-71) */
+int64_t oracle_required_overlap_sim(int sim, int64_t p, int64_t q, int64_t sr, int64_t ss);
+
+/* NAIVE join with any similarity, reference src/join.cpp:91-126: a self-join of
+ * (rt, ro, rn) when self_join != 0 (s arguments ignored), else R x S. */
+int oracle_naive_join_sim(const uint32_t* rt, const uint64_t* ro, size_t rn, const uint32_t* st,
+                          const uint64_t* so, size_t sn, int self_join, int sim, int64_t p, int64_t q,
+                          oracle_pair** pairs, size_t* pair_count, oracle_counters* counters);
+
 /* Canonical order of a raw CSR collection (per-record sort + dedup, records by
  * (size, tokens)), reference src/collection.cpp:44-54.  Writes the canonical
  * CSR into out_tokens (capacity >= input token count) / out_offsets (n+1). */

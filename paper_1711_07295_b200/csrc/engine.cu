@@ -1426,7 +1426,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     dev::VerifyParams VP{};
     VP.tokens = rep->tokens;
     VP.offsets = rep->offsets;
-    VP.minov = d_minov;
+    VP.need.minov = d_minov;
+    VP.need.cosine = plan.cosine ? 1 : 0;
+    VP.need.cp = plan.p;
+    VP.need.cq = plan.q;
     VP.surv = d_surv;
     VP.res_keys = SB.ka;
     VP.res_ov = SB.va;
@@ -1792,6 +1795,140 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         std::fprintf(stderr, "[host] after sync %.3f ms, total %.3f ms\n",
                      std::chrono::duration<double, std::milli>(Clock::now() - t_synced).count(), total * 1e3);
     out.verify_s = std::max(0.0, total - out.index_s - out.candidates_s);
+}
+
+// NAIVE RS-join block on one GPU: R rows [r_begin, r_end) x all of S
+// (reference src/join.cpp:110-121).  No filter: launches of verify_rs over
+// contiguous ranges of the row-major pair index, each sized so its matches
+// fit the result buffer; every launch's matches are sorted (K4) and
+// downloaded as one run, and consecutive runs are already in (id_r, id_s)
+// order, so they concatenate.  Overflowing launches are redone smaller.
+void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& plan, int device, EngineResult& out) {
+    using Clock = std::chrono::steady_clock;
+    set_device(device);
+    static thread_local cudaStream_t streams[16] = {};
+    if (!streams[device & 15]) CK(cudaStreamCreateWithFlags(&streams[device & 15], cudaStreamNonBlocking));
+    cudaStream_t s = streams[device & 15];
+    EngineStats& st = out.stats;
+    const auto t_start = Clock::now();
+    Timer T(s);
+    Arena A(s);
+    const uint64_t nS = Sc.size();
+    const uint64_t rows = plan.r_end - plan.r_begin;
+    const uint64_t total = rows * nS;
+    st.window_pairs = total;
+    out.candidates = out.verified = total;
+    if (total == 0) return;
+
+    cudaEvent_t e0 = T.mark();
+    auto repR = replica_for(R, device, s, st.h2d_bytes, st.launches);
+    auto repS = &R == &Sc ? repR : replica_for(Sc, device, s, st.h2d_bytes, st.launches);
+    TableStage stage;
+    int32_t* d_minov = nullptr;
+    stage.add(&d_minov, plan.minov.data(), plan.minov.size() * 4);
+    stage.flush(A, s, st.h2d_bytes);
+    cudaEvent_t e_up = T.mark();
+
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), 1024);
+    dev::Control* d_ctl = A.alloc<dev::Control>(1);
+    SortBufs SB{};
+    SB.ka = A.alloc<unsigned long long>(res_cap);
+    SB.va = A.alloc<uint32_t>(res_cap);
+    SB.kb = A.alloc<unsigned long long>(res_cap);
+    SB.vb = A.alloc<uint32_t>(res_cap);
+    const uint32_t max_tiles = static_cast<uint32_t>((res_cap + dev::kSortTile - 1) / dev::kSortTile);
+    SB.hist = A.alloc<uint32_t>(256ull * max_tiles);
+    SB.sums = A.alloc<uint32_t>((256ull * max_tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+    SB.count = &d_ctl->results;
+    CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
+    int idbits = 1;
+    while ((uint64_t(1) << idbits) < std::max<uint64_t>(R.size(), nS) + 1) ++idbits;
+
+    dev::VerifyRsParams VP{};
+    VP.ta = repR->tokens;
+    VP.oa = repR->offsets;
+    VP.tb = repS->tokens;
+    VP.ob = repS->offsets;
+    VP.nS = nS;
+    VP.r_begin = plan.r_begin;
+    VP.need.minov = d_minov;
+    VP.need.cosine = plan.cosine ? 1 : 0;
+    VP.need.cp = plan.p;
+    VP.need.cq = plan.q;
+    VP.res_keys = SB.ka;
+    VP.res_ov = SB.va;
+    VP.res_cap = res_cap;
+    VP.ctl = d_ctl;
+
+    std::vector<PairVec> runs;
+    uint64_t k0 = 0;
+    uint64_t batch = std::min<uint64_t>(total, env_u64("SSJB_RS_BATCH", uint64_t(1) << 32));
+    double ms_verify = 0;
+    dev::Control h_ctl{};
+    uint64_t verify_bytes = 0;
+    while (k0 < total) {
+        const uint64_t k1 = std::min(total, k0 + std::max<uint64_t>(batch, 1));
+        CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
+        VP.k0 = k0;
+        VP.k1 = k1;
+        const uint64_t blocks = std::min<uint64_t>((k1 - k0 + 255) / 256, uint64_t(sms) * 16);
+        cudaEvent_t a = T.mark();
+        dev::verify_rs<<<static_cast<unsigned>(blocks), 256, 0, s>>>(VP);
+        ++st.launches;
+        CK(cudaGetLastError());
+        cudaEvent_t b = T.mark();
+        CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ms_verify += Timer::ms(a, b);
+        const uint64_t cnt = h_ctl.results;
+        if (cnt > res_cap) {  // matches overflowed the buffer: redo a smaller range
+            batch = std::max<uint64_t>(1, (k1 - k0) * res_cap / cnt * 7 / 10);
+            continue;
+        }
+        verify_bytes += h_ctl.verify_bytes;
+        ++st.batches;
+        if (cnt) {
+            cudaEvent_t c0 = T.mark();
+            const bool inb = sort_results(SB, cnt, idbits, s, st.launches);
+            PairOut* packed = A.alloc<PairOut>(cnt);
+            pack_pairs<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(inb ? SB.kb : SB.ka,
+                                                                              inb ? SB.vb : SB.va, packed, cnt);
+            ++st.launches;
+            CK(cudaGetLastError());
+            cudaEvent_t c1 = T.mark();
+            PairVec run(cnt);
+            d2h_staged(run.data(), packed, cnt * sizeof(PairOut), s);
+            cudaEvent_t c2 = T.mark();
+            CK(cudaStreamSynchronize(s));
+            st.d2h_bytes += cnt * sizeof(PairOut);
+            st.ms_sort += Timer::ms(c0, c1);
+            st.ms_download += Timer::ms(c1, c2);
+            runs.push_back(std::move(run));
+        }
+        k0 = k1;
+    }
+    size_t n_out = 0;
+    for (auto& r : runs) n_out += r.size();
+    if (runs.size() == 1) {
+        out.pairs = std::move(runs[0]);
+    } else if (n_out) {
+        out.pairs.resize(n_out);
+        size_t at = 0;
+        for (auto& r : runs) {
+            std::memcpy(out.pairs.data() + at, r.data(), r.size() * sizeof(PairOut));
+            at += r.size();
+        }
+    }
+    out.matched = out.pairs.size();
+    st.survivors = total;
+    st.verify_bytes = verify_bytes;
+    st.ms_upload = Timer::ms(e0, e_up);
+    st.ms_verify = ms_verify;
+    out.index_s = 0;
+    out.candidates_s = 0;
+    out.verify_s = std::chrono::duration<double>(Clock::now() - t_start).count();
 }
 
 }  // namespace ssjb

@@ -64,6 +64,9 @@ struct EngineResult {
 int engine_device_count();
 // One shard (plan.row_begin..row_end) of a self-join on `device`.
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out);
+// NAIVE RS-join block (plan.r_begin..r_end of R) x S on `device`; pairs are
+// (R id, S id), sorted.
+void engine_join_rs(const Collection& r, const Collection& s, const RsPlan& plan, int device, EngineResult& out);
 // The sketch-build kernel alone; copies the store (n * width/64 words) to out_host.
 void engine_build_bitmaps(const Collection& c, Method method, int width, int hash, int device,
                           uint64_t* out_host);

@@ -531,6 +531,60 @@ ResolvedBitmap resolve_bitmap(const Collection& c, const Options& o) {
 }
 
 // ==================================================================== plan
+int64_t required_overlap(Sim f, const Rational& t, int64_t size_r, int64_t size_s) {
+    // reference src/similarity.cpp:93-115
+    const int64_t p = t.num, q = t.den;
+    int64_t v = 0;
+    switch (f) {
+        case Sim::Overlap: v = p; break;
+        case Sim::Jaccard: v = ceil_div(static_cast<__int128>(p) * (size_r + size_s), static_cast<__int128>(p) + q); break;
+        case Sim::Dice: v = ceil_div(static_cast<__int128>(p) * (size_r + size_s), static_cast<__int128>(2) * q); break;
+        case Sim::Cosine: {
+            unsigned __int128 target = static_cast<unsigned __int128>(p) * static_cast<unsigned __int128>(p);
+            target *= static_cast<unsigned __int128>(size_r) * static_cast<unsigned __int128>(size_s);
+            uint64_t root = 0;
+            if (target != 0) {  // isqrt_ceil (src/rational.cpp:51-71)
+                const unsigned __int128 m = target - 1;
+                unsigned __int128 x = static_cast<unsigned __int128>(std::sqrt(static_cast<long double>(m)));
+                if (x == 0) x = 1;
+                for (int i = 0; i < 6; ++i) {
+                    unsigned __int128 nx = (x + m / x) >> 1;
+                    if (nx == x) break;
+                    x = nx;
+                }
+                while (x * x > m) --x;
+                while ((x + 1) * (x + 1) <= m) ++x;
+                root = static_cast<uint64_t>(x) + 1;
+            }
+            v = ceil_div(static_cast<__int128>(root), q);
+            break;
+        }
+    }
+    return std::max<int64_t>(1, v);
+}
+
+std::vector<int32_t> minov_table(Sim f, const Rational& t, size_t smax) {
+    std::vector<int32_t> m(smax + 1, 1);
+    if (f == Sim::Cosine) return m;  // depends on |r|*|s|: computed per pair
+    for (size_t S = 0; S <= smax; ++S) {
+        const int64_t v = required_overlap(f, t, static_cast<int64_t>(S), 0);
+        m[S] = static_cast<int32_t>(std::min<int64_t>(v, std::numeric_limits<int32_t>::max()));
+    }
+    return m;
+}
+
+RsPlan make_rs_plan(const Collection& r, const Collection& s, const Options& o, size_t r_begin, size_t r_end) {
+    RsPlan plan;
+    plan.sim = o.sim;
+    plan.p = o.threshold.num;
+    plan.q = o.threshold.den;
+    plan.r_begin = std::min(r_begin, r.size());
+    plan.r_end = std::max(plan.r_begin, std::min(r_end, r.size()));
+    plan.minov = minov_table(o.sim, o.threshold, static_cast<size_t>(r.max_size) + s.max_size);
+    plan.cosine = o.sim == Sim::Cosine;
+    return plan;
+}
+
 uint32_t window_start_of(const Collection& c, const JoinPlan& plan, size_t row) {
     return plan.naive ? 0u : plan.window_start[c.rec_size(row)];
 }
@@ -547,13 +601,11 @@ JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size
     plan.capacity = static_cast<uint32_t>(o.buffer_capacity);
     if (!plan.naive) plan.bitmap = resolve_bitmap(c, o);
     const uint32_t ms = c.max_size;
-    // minov over S in [0, 2*max_size] (reference src/similarity.cpp:99-100,113-115)
-    plan.minov.resize(2 * static_cast<size_t>(ms) + 1);
-    for (size_t S = 0; S < plan.minov.size(); ++S) {
-        int64_t v = ceil_div(static_cast<__int128>(plan.p) * static_cast<int64_t>(S),
-                             static_cast<__int128>(plan.p) + plan.q);
-        plan.minov[S] = static_cast<int32_t>(std::max<int64_t>(1, v));
-    }
+    // minov over S in [0, 2*max_size] (reference src/similarity.cpp:99-100,113-115);
+    // NAIVE takes every similarity function (src/join.cpp:91-126)
+    const Sim sim = plan.naive ? o.sim : Sim::Jaccard;
+    plan.minov = minov_table(sim, o.threshold, 2 * static_cast<size_t>(ms));
+    plan.cosine = sim == Sim::Cosine;
     // j0 per size from the collection's size index (reference src/parallel_join.cpp:65-70)
     const std::vector<uint32_t>& first_ge = c.first_ge;
     plan.window_start.resize(static_cast<size_t>(ms) + 1);

@@ -163,11 +163,29 @@ struct JoinPlan {
     uint32_t capacity = 2048;    // per-record buffer (counter semantics only)
     size_t row_begin = 0, row_end = 0;
     // minov[S] = max(1, ceil(p*S/(p+q))) for S = |r|+|s| in [0, 2*max_size]
+    // (NAIVE with Dice / Overlap: that function's required overlap of S)
     std::vector<int32_t> minov;
+    bool cosine = false;         // NAIVE with Cosine: required overlap computed per pair
     // j0 of a record of size s: first index whose size >= ceil(p*s/q)
     std::vector<uint32_t> window_start;
     uint64_t window_pairs = 0;   // sum over rows of (i - j0(i))
 };
+
+// Required overlap of the similarity functions (reference src/similarity.cpp:93-115).
+int64_t required_overlap(Sim f, const Rational& t, int64_t size_r, int64_t size_s);
+// minov[S] for S in [0, smax] (Jaccard / Dice / Overlap; Cosine: all 1, unused).
+std::vector<int32_t> minov_table(Sim f, const Rational& t, size_t smax);
+
+// NAIVE RS-join (two collections) over R rows [r_begin, r_end) x all of S
+// (reference src/join.cpp:110-121).
+struct RsPlan {
+    Sim sim = Sim::Jaccard;
+    int64_t p = 1, q = 2;
+    std::vector<int32_t> minov;  // minov[|r|+|s|]
+    bool cosine = false;
+    size_t r_begin = 0, r_end = 0;
+};
+RsPlan make_rs_plan(const Collection& r, const Collection& s, const Options& o, size_t r_begin, size_t r_end);
 
 uint32_t window_start_of(const Collection& c, const JoinPlan& plan, size_t row);
 JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size_t row_end);

@@ -733,10 +733,49 @@ __global__ void reduce_counters(CountParams P) {
 }
 
 // ================================================================ K3: verify
+// Required overlap of a pair for the similarity functions the NAIVE join
+// accepts (reference src/similarity.cpp:93-115).  Jaccard, Dice and Overlap
+// depend on |r|+|s| only and come from the host-exact table minov[|r|+|s|];
+// Cosine depends on |r|*|s| and is computed here with the reference's own
+// 128-bit arithmetic: ceil(isqrt_ceil(p^2 |r| |s|) / q)
+// (src/similarity.cpp:103-107, src/rational.cpp:43-71).
+struct SimNeed {
+    const int32_t* minov;  // minov[|r|+|s|]
+    int cosine;            // 1: Cosine, minov unused
+    long long cp, cq;      // reduced threshold p/q (Cosine)
+};
+
+__device__ __forceinline__ uint64_t isqrt_floor_u128(unsigned __int128 v) {
+    // Newton from a double estimate, then exact correction (src/rational.cpp:51-65)
+    if (v == 0) return 0;
+    const double est = static_cast<double>(static_cast<uint64_t>(v >> 64)) * 18446744073709551616.0 +
+                       static_cast<double>(static_cast<uint64_t>(v));
+    unsigned __int128 x = static_cast<unsigned __int128>(sqrt(est));
+    if (x == 0) x = 1;
+    for (int it = 0; it < 6; ++it) {
+        const unsigned __int128 nx = (x + v / x) >> 1;
+        if (nx == x) break;
+        x = nx;
+    }
+    while (x * x > v) --x;
+    while ((x + 1) * (x + 1) <= v) ++x;
+    return static_cast<uint64_t>(x);
+}
+
+__device__ __forceinline__ int32_t need_overlap(const SimNeed& N, uint32_t na, uint32_t nb) {
+    if (!N.cosine) return N.minov[na + nb];
+    unsigned __int128 target = static_cast<unsigned __int128>(N.cp) * static_cast<unsigned __int128>(N.cp);
+    target *= static_cast<unsigned __int128>(na) * nb;
+    const uint64_t root = target == 0 ? 0 : isqrt_floor_u128(target - 1) + 1;
+    const __int128 q = N.cq;
+    const long long v = static_cast<long long>((static_cast<__int128>(root) + q - 1) / q);
+    return static_cast<int32_t>(max(1ll, min(v, 0x7FFFFFFFll)));
+}
+
 struct VerifyParams {
     const uint32_t* tokens;
     const uint64_t* offsets;
-    const int32_t* minov;     // minov[|r|+|s|]
+    SimNeed need;             // required overlap per (|r|, |s|)
     const uint2* surv;
     const unsigned long long* count_ptr;  // survivors emitted by K2 (device memory)
     unsigned long long count_cap;         // survivor buffer capacity
@@ -772,7 +811,7 @@ __global__ void verify_pairs(VerifyParams P) {
             const uint64_t ab = P.offsets[j], ae = P.offsets[j + 1];
             const uint64_t bb = P.offsets[i], be = P.offsets[i + 1];
             const uint32_t na = static_cast<uint32_t>(ae - ab), nb = static_cast<uint32_t>(be - bb);
-            const int32_t need = P.minov[na + nb];
+            const int32_t need = need_overlap(P.need, na, nb);
             const uint32_t* A = P.tokens + ab;
             const uint32_t* B = P.tokens + bb;
             uint32_t ia = 0, ib = 0;
@@ -816,6 +855,76 @@ __global__ void verify_pairs(VerifyParams P) {
             slot = __shfl_sync(0xFFFFFFFFu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
             if (matched && slot < P.res_cap) {
                 P.res_keys[slot] = (static_cast<unsigned long long>(j) << 32) | i;
+                P.res_ov[slot] = ov;
+            }
+        }
+    }
+}
+
+// ===================================================== K3 (RS): naive R x S
+// NAIVE RS-join (reference src/join.cpp:110-121): every (r, s) in
+// [r_begin, r_end) x [0, nS) is merged, no filter.  Pair index k enumerates
+// the block row-major, k -> (r = k / nS, s = k % nS), so a warp shares one
+// r-record (broadcast loads) and walks consecutive, size-sorted s-records;
+// a contiguous k range yields keys (r << 32 | s) in one contiguous key range,
+// so runs of consecutive launches concatenate in canonical order.
+struct VerifyRsParams {
+    const uint32_t* ta;
+    const uint64_t* oa;   // R
+    const uint32_t* tb;
+    const uint64_t* ob;   // S
+    unsigned long long nS;
+    unsigned long long k0, k1;
+    unsigned long long r_begin;
+    SimNeed need;
+    unsigned long long* res_keys;  // (r << 32) | s
+    uint32_t* res_ov;
+    unsigned long long res_cap;
+    Control* ctl;
+};
+
+__global__ void verify_rs(VerifyRsParams P) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = P.k0 + static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < P.k1;
+         base += stride) {
+        const unsigned long long k = base + threadIdx.x;
+        bool matched = false;
+        uint32_t r = 0, sidx = 0, ov = 0;
+        unsigned long long vb = 0;
+        if (k < P.k1) {
+            r = static_cast<uint32_t>(P.r_begin + k / P.nS);
+            sidx = static_cast<uint32_t>(k % P.nS);
+            const uint64_t ab = P.oa[r], ae = P.oa[r + 1];
+            const uint64_t bb = P.ob[sidx], be = P.ob[sidx + 1];
+            const uint32_t na = static_cast<uint32_t>(ae - ab), nb = static_cast<uint32_t>(be - bb);
+            const int32_t need = need_overlap(P.need, na, nb);
+            const uint32_t* A = P.ta + ab;
+            const uint32_t* B = P.tb + bb;
+            uint32_t ia = 0, ib = 0;
+            int32_t o = 0;
+            while (ia < na && ib < nb) {  // early exit of src/similarity.cpp:174-175
+                const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
+                if (o + rest < need) break;
+                const uint32_t x = __ldg(A + ia), y = __ldg(B + ib);
+                o += x == y;
+                ia += x <= y;
+                ib += y <= x;
+            }
+            matched = o >= need;
+            ov = static_cast<uint32_t>(o);
+            vb = 4ull * (na + nb) + (matched ? 16 : 0);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
+        if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, matched);
+        if (bal) {
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(&P.ctl->results, static_cast<unsigned long long>(__popc(bal)));
+            slot = __shfl_sync(0xFFFFFFFFu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
+            if (matched && slot < P.res_cap) {
+                P.res_keys[slot] = (static_cast<unsigned long long>(r) << 32) | sidx;
                 P.res_ov[slot] = ov;
             }
         }

@@ -10,6 +10,6 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:filter_tc_kernel -c 8 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:filter_tc -c 8 \
   -o gpurun_out/filter_tc python tools/c2_phases.py 128 1 > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
