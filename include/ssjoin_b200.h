@@ -72,6 +72,37 @@ ssj_status ssjb_report_stats(const ssj_report* report, ssjb_stats* out);
 ssj_status ssjb_build_bitmaps(const ssj_collection* coll, int method, int bits, int hash,
                               int device, uint64_t* out_host);
 
+/* ---- result delivery for outputs beyond host memory ----
+ * The ssj_report these return holds the counters, timings and
+ * saturated_records of the join (counters.matched = number of result pairs)
+ * but NO pairs: ssj_report_pair_count() is 0.  RS-joins (s_or_null != NULL)
+ * follow ssj_join's rules (NAIVE only). */
+
+/* Receives consecutive chunks of the canonical (id_r, id_s)-sorted pair list;
+ * a non-zero return stops the join (SSJ_ERROR_IO). */
+typedef int (*ssjb_pair_sink)(const ssj_pair* pairs, size_t count, void* user);
+
+/* Streams the join's pairs to `sink` in chunks of whole id_r ranges of about
+ * chunk_pairs pairs (0: 16M), without ever holding the full list in host
+ * memory: sorted result runs stay in HBM and are merged per chunk on the GPU.
+ * `out` may be NULL. */
+ssj_status ssjb_join_stream(const ssj_collection* r, const ssj_collection* s_or_null,
+                            const ssj_join_options* opts, size_t chunk_pairs, ssjb_pair_sink sink,
+                            void* user, ssj_report** out);
+
+/* Count-first: counters (incl. matched) without sorting or downloading pairs. */
+ssj_status ssjb_join_count(const ssj_collection* r, const ssj_collection* s_or_null,
+                           const ssj_join_options* opts, ssj_report** out);
+
+/* Streams the pairs into a text file in the reference CLI's pairs format,
+ * one "id_r id_s overlap" line per pair (reference tools/ssjoin_cli.cpp:290-294).
+ * `out` may be NULL. */
+ssj_status ssjb_join_write_pairs(const ssj_collection* r, const ssj_collection* s_or_null,
+                                 const ssj_join_options* opts, const char* path, ssj_report** out);
+
+/* Writes a materialised report's pairs in the same text format. */
+ssj_status ssjb_report_write_pairs(const ssj_report* report, const char* path);
+
 const char* ssjb_version(void);
 
 #ifdef __cplusplus

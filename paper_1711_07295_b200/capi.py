@@ -108,8 +108,16 @@ class Stats(C.Structure):
                [("devices", C.c_int), ("filter_kernel", C.c_int)]
 
 
+# ssjb_pair_sink: int (*)(const ssj_pair*, size_t, void*)
+PAIR_SINK = C.CFUNCTYPE(C.c_int, C.POINTER(Pair), C.c_size_t, C.c_void_p)
+
 # Extension entry points of the B200 library (include/ssjoin_b200.h).
 _EXT_PROTOS = {
+    "ssjb_join_stream": (C.c_int, [P, P, C.POINTER(JoinOptions), C.c_size_t, PAIR_SINK, P,
+                                   C.POINTER(P)]),
+    "ssjb_join_count": (C.c_int, [P, P, C.POINTER(JoinOptions), C.POINTER(P)]),
+    "ssjb_join_write_pairs": (C.c_int, [P, P, C.POINTER(JoinOptions), C.c_char_p, C.POINTER(P)]),
+    "ssjb_report_write_pairs": (C.c_int, [P, C.c_char_p]),
     "ssjb_collection_from_csr": (C.c_int, [P, P, C.c_size_t, C.POINTER(P)]),
     "ssjb_collection_csr": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_size_t)]),
     "ssjb_collection_pin_device": (C.c_int, [P, C.c_int]),

@@ -3,9 +3,12 @@
 // texts and option validation follow reference src/capi.cpp; joins run on the
 // GPU engine (engine.cu), split over several GPUs when configured.
 #include <algorithm>
+#include <charconv>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <thread>
@@ -184,12 +187,13 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
     rep.timings.verify_s = std::max(0.0, total_s - rep.timings.index_s - rep.timings.candidates_s);
 }
 
-// Runs rows [row_begin, row_end) split over `devices` GPUs (first_device..).
-std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
-                                         size_t row_end, int devices, int first_device) {
-    const auto t0 = std::chrono::steady_clock::now();
+// Runs rows [row_begin, row_end) split over `devices` GPUs (first_device..);
+// the engines' results per device (delivery: see JoinPlan::delivery).
+std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
+                                               size_t row_end, int devices, int first_device, int delivery) {
     if (coll.size() >= (size_t(1) << 31)) throw std::invalid_argument("collections above 2^31 records are not supported");
     ssjb::JoinPlan whole = ssjb::make_plan(coll, o, row_begin, row_end);
+    whole.delivery = delivery;
     const int avail = ssjb::engine_device_count();
     if (avail <= 0) throw ssjb::DeviceError("no CUDA device available for the B200 join");
     devices = std::max(1, std::min(devices, avail - first_device));
@@ -220,6 +224,7 @@ std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssj
             pool.emplace_back([&, g]() {
                 try {
                     ssjb::JoinPlan p = ssjb::make_plan(coll, o, bounds[g], bounds[g + 1]);
+                    p.delivery = delivery;
                     ssjb::engine_join(coll, p, first_device + g, parts[static_cast<size_t>(g)]);
                 } catch (...) {
                     errs[static_cast<size_t>(g)] = std::current_exception();
@@ -230,6 +235,13 @@ std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssj
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
     }
+    return parts;
+}
+
+std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
+                                         size_t row_end, int devices, int first_device) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto parts = run_self_parts(coll, o, row_begin, row_end, devices, first_device, 0);
     auto rep = std::make_unique<ssj_report>();
     const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     fill_report(*rep, parts, total);
@@ -239,9 +251,8 @@ std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssj
 // NAIVE RS-join (reference src/capi.cpp:225-232 -> src/join.cpp:110-121): R rows
 // split into contiguous blocks over `devices` GPUs; each block's pairs are
 // (R id, S id)-sorted and the blocks' id_r ranges ascend, so they concatenate.
-std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssjb::Collection& sc,
-                                            const ssjb::Options& o, int devices) {
-    const auto t0 = std::chrono::steady_clock::now();
+std::vector<ssjb::EngineResult> run_rs_parts(const ssjb::Collection& r, const ssjb::Collection& sc,
+                                             const ssjb::Options& o, int devices, int delivery) {
     if (r.size() >= (size_t(1) << 31) || sc.size() >= (size_t(1) << 31))
         throw std::invalid_argument("collections above 2^31 records are not supported");
     const int avail = ssjb::engine_device_count();
@@ -256,6 +267,7 @@ std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssj
         auto work = [&, g, b, e]() {
             try {
                 ssjb::RsPlan p = ssjb::make_rs_plan(r, sc, o, b, e);
+                p.delivery = delivery;
                 ssjb::engine_join_rs(r, sc, p, g, parts[static_cast<size_t>(g)]);
             } catch (...) {
                 errs[static_cast<size_t>(g)] = std::current_exception();
@@ -267,6 +279,14 @@ std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssj
     for (auto& t : pool) t.join();
     for (auto& e : errs)
         if (e) std::rethrow_exception(e);
+    return parts;
+}
+
+std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssjb::Collection& sc,
+                                            const ssjb::Options& o, int devices) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto parts = run_rs_parts(r, sc, o, devices, 0);
+    devices = static_cast<int>(parts.size());
     // blocks own ascending id_r ranges: concatenation is the canonical order
     ssjb::PairVec all;
     if (devices > 1) {
@@ -286,6 +306,163 @@ std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssj
     if (devices > 1) rep->pairs = std::move(all);
     rep->timings.index_s = rep->timings.candidates_s = 0;  // naive: all verify (src/join.cpp:124)
     rep->timings.verify_s = total;
+    return rep;
+}
+
+// ------------------------------------------------------------ delivery
+// Streams the engines' output in canonical (id_r, id_s) order to `sink`, in
+// chunks of whole id_r ranges holding about chunk_pairs pairs (one id_r with
+// more pairs is one chunk).  Each part contributes its small host run and its
+// sorted device runs (plan.delivery 2); per chunk the device side extracts the
+// id_r range (merged on the GPU), the host merges the parts' sequences.
+using Sink = std::function<void(const ssjb::PairOut*, size_t)>;
+
+void stream_parts(std::vector<ssjb::EngineResult>& parts, size_t n_ids, size_t chunk_pairs, const Sink& sink) {
+    chunk_pairs = std::max<size_t>(chunk_pairs, 1);
+    bool any_runs = false;
+    for (auto& p : parts) any_runs |= p.runs != nullptr;
+    if (!any_runs && parts.size() == 1) {  // one sorted host run: slice it
+        const ssjb::PairVec& v = parts[0].pairs;
+        for (size_t a = 0; a < v.size(); a += chunk_pairs) sink(v.data() + a, std::min(chunk_pairs, v.size() - a));
+        return;
+    }
+    std::vector<uint64_t> hist(n_ids, 0);
+    for (auto& p : parts) {
+        for (const auto& x : p.pairs)
+            if (x.id_r < n_ids) ++hist[x.id_r];
+        if (p.runs) ssjb::runs_histogram(*p.runs, hist);
+    }
+    auto key_less = [](const ssjb::PairOut& x, const ssjb::PairOut& y) {
+        return x.id_r != y.id_r ? x.id_r < y.id_r : x.id_s < y.id_s;
+    };
+    size_t ja = 0;
+    while (ja < n_ids) {
+        uint64_t tot = hist[ja];
+        size_t jb = ja + 1;
+        while (jb < n_ids && tot + hist[jb] <= chunk_pairs) tot += hist[jb++];
+        if (tot == 0) {
+            ja = jb;
+            continue;
+        }
+        std::vector<ssjb::PairVec> seqs;
+        for (auto& p : parts) {
+            if (!p.pairs.empty()) {
+                auto lo = std::lower_bound(p.pairs.begin(), p.pairs.end(), ja,
+                                           [](const ssjb::PairOut& x, size_t j) { return x.id_r < j; });
+                auto hi = std::lower_bound(lo, p.pairs.end(), jb,
+                                           [](const ssjb::PairOut& x, size_t j) { return x.id_r < j; });
+                if (lo != hi) seqs.emplace_back(lo, hi);
+            }
+            if (p.runs) {
+                ssjb::PairVec v;
+                ssjb::runs_extract(*p.runs, static_cast<uint32_t>(ja), static_cast<uint32_t>(jb), v);
+                if (!v.empty()) seqs.push_back(std::move(v));
+            }
+        }
+        while (seqs.size() > 1) {  // pairwise merges (a handful of sequences per chunk)
+            std::vector<ssjb::PairVec> next;
+            for (size_t k = 0; k + 1 < seqs.size(); k += 2) {
+                ssjb::PairVec m(seqs[k].size() + seqs[k + 1].size());
+                std::merge(seqs[k].begin(), seqs[k].end(), seqs[k + 1].begin(), seqs[k + 1].end(), m.begin(),
+                           key_less);
+                next.push_back(std::move(m));
+            }
+            if (seqs.size() & 1) next.push_back(std::move(seqs.back()));
+            seqs.swap(next);
+        }
+        if (!seqs.empty()) sink(seqs[0].data(), seqs[0].size());
+        ja = jb;
+    }
+}
+
+// Text pairs in the reference CLI's format, "id_r id_s overlap\n" per pair
+// (tools/ssjoin_cli.cpp:290-294); chunks are formatted by several threads and
+// written in order.
+struct PairTextWriter {
+    std::FILE* f = nullptr;
+    std::string path;
+    explicit PairTextWriter(const char* p) : path(p) {
+        f = std::fopen(p, "wb");
+        if (!f) throw ssjb::IoError("cannot open output file '" + path + "'");
+    }
+    ~PairTextWriter() {
+        if (f) std::fclose(f);
+    }
+    void close() {
+        if (f && std::fclose(f) != 0) {
+            f = nullptr;
+            throw ssjb::IoError("error writing '" + path + "'");
+        }
+        f = nullptr;
+    }
+    static size_t format(const ssjb::PairOut* p, size_t n, std::vector<char>& buf) {
+        buf.resize(n * 42 + 1);
+        char* o = buf.data();
+        for (size_t k = 0; k < n; ++k) {
+            o = std::to_chars(o, o + 10, p[k].id_r).ptr;
+            *o++ = ' ';
+            o = std::to_chars(o, o + 10, p[k].id_s).ptr;
+            *o++ = ' ';
+            o = std::to_chars(o, o + 20, p[k].overlap).ptr;
+            *o++ = '\n';
+        }
+        return static_cast<size_t>(o - buf.data());
+    }
+    void write(const ssjb::PairOut* p, size_t n) {
+        const size_t piece = size_t(1) << 16;
+        const unsigned nt = static_cast<unsigned>(
+            std::max<size_t>(1, std::min<size_t>((n + piece - 1) / piece, std::min(16u, std::thread::hardware_concurrency()))));
+        std::vector<std::vector<char>> bufs(nt);
+        std::vector<size_t> lens(nt, 0);
+        const size_t per = (n + nt - 1) / nt;
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t) {
+            const size_t a = std::min(n, t * per), b = std::min(n, a + per);
+            if (t == 0) continue;
+            th.emplace_back([&, t, a, b]() { lens[t] = format(p + a, b - a, bufs[t]); });
+        }
+        lens[0] = format(p, std::min(n, per), bufs[0]);
+        for (auto& x : th) x.join();
+        for (unsigned t = 0; t < nt; ++t)
+            if (lens[t] && std::fwrite(bufs[t].data(), 1, lens[t], f) != lens[t])
+                throw ssjb::IoError("error writing '" + path + "'");
+    }
+};
+
+// The join of (r, s_or_null) with the given delivery; the report carries the
+// counters (pairs only for delivery 0).
+std::vector<ssjb::EngineResult> run_parts(const ssj_collection* r, const ssj_collection* s_or_null,
+                                          const ssjb::Options& o, int delivery) {
+    if (s_or_null != nullptr) return run_rs_parts(*r->c, *s_or_null->c, o, configured_devices(), delivery);
+    return run_self_parts(*r->c, o, 0, r->c->size(), configured_devices(), 0, delivery);
+}
+
+ssj_status checked_options(const ssj_collection* r, const ssj_collection* s_or_null, const ssj_join_options* opts,
+                           ssjb::Options& o) {
+    if (r == nullptr || opts == nullptr) {
+        set_error("null argument");
+        return SSJ_ERROR_INVALID_ARGUMENT;
+    }
+    o = to_options(*opts);
+    if (s_or_null != nullptr && o.algorithm != ssjb::Algo::Naive) {
+        set_error("RS-joins are only supported by the naive algorithm");
+        return SSJ_ERROR_INVALID_ARGUMENT;
+    }
+    check_supported(o);
+    return SSJ_OK;
+}
+
+std::unique_ptr<ssj_report> report_of(std::vector<ssjb::EngineResult>& parts, double total_s, bool rs) {
+    for (auto& p : parts) {
+        p.pairs = ssjb::PairVec();
+        p.runs.reset();
+    }
+    auto rep = std::make_unique<ssj_report>();
+    fill_report(*rep, parts, total_s);
+    if (rs) {
+        rep->timings.index_s = rep->timings.candidates_s = 0;
+        rep->timings.verify_s = total_s;
+    }
     return rep;
 }
 
@@ -595,3 +772,85 @@ SSJB_API ssj_status ssjb_build_bitmaps(const ssj_collection* coll, int method, i
 }
 
 SSJB_API const char* ssjb_version(void) { return "ssjoin-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------ delivery
+SSJB_API ssj_status ssjb_join_stream(const ssj_collection* r, const ssj_collection* s_or_null,
+                                     const ssj_join_options* opts, size_t chunk_pairs, ssjb_pair_sink sink, void* user,
+                                     ssj_report** out) {
+    return guarded([&]() {
+        ssjb::Options o;
+        if (sink == nullptr) {
+            set_error("null argument");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        ssj_status st = checked_options(r, s_or_null, opts, o);
+        if (st != SSJ_OK) return st;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto parts = run_parts(r, s_or_null, o, 2);
+        stream_parts(parts, r->c->size(), chunk_pairs ? chunk_pairs : (size_t(1) << 24),
+                     [&](const ssjb::PairOut* p, size_t n) {
+                         if (sink(reinterpret_cast<const ssj_pair*>(p), n, user) != 0)
+                             throw ssjb::IoError("the pair sink stopped the delivery");
+                     });
+        const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        auto rep = report_of(parts, total, s_or_null != nullptr);
+        if (out) *out = rep.release();
+        return SSJ_OK;
+    });
+}
+
+SSJB_API ssj_status ssjb_join_count(const ssj_collection* r, const ssj_collection* s_or_null,
+                                    const ssj_join_options* opts, ssj_report** out) {
+    return guarded([&]() {
+        ssjb::Options o;
+        if (out == nullptr) {
+            set_error("null argument");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        ssj_status st = checked_options(r, s_or_null, opts, o);
+        if (st != SSJ_OK) return st;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto parts = run_parts(r, s_or_null, o, 1);
+        const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = report_of(parts, total, s_or_null != nullptr).release();
+        return SSJ_OK;
+    });
+}
+
+SSJB_API ssj_status ssjb_join_write_pairs(const ssj_collection* r, const ssj_collection* s_or_null,
+                                          const ssj_join_options* opts, const char* path, ssj_report** out) {
+    return guarded([&]() {
+        ssjb::Options o;
+        if (path == nullptr) {
+            set_error("null argument");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        ssj_status st = checked_options(r, s_or_null, opts, o);
+        if (st != SSJ_OK) return st;
+        const auto t0 = std::chrono::steady_clock::now();
+        PairTextWriter w(path);
+        auto parts = run_parts(r, s_or_null, o, 2);
+        stream_parts(parts, r->c->size(), size_t(1) << 24,
+                     [&](const ssjb::PairOut* p, size_t n) { w.write(p, n); });
+        w.close();
+        const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        auto rep = report_of(parts, total, s_or_null != nullptr);
+        if (out) *out = rep.release();
+        return SSJ_OK;
+    });
+}
+
+SSJB_API ssj_status ssjb_report_write_pairs(const ssj_report* report, const char* path) {
+    return guarded([&]() {
+        if (report == nullptr || path == nullptr) {
+            set_error("null argument");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        PairTextWriter w(path);
+        const size_t n = report->pairs.size();
+        for (size_t a = 0; a < n; a += size_t(1) << 24)
+            w.write(report->pairs.data() + a, std::min(size_t(1) << 24, n - a));
+        w.close();
+        return SSJ_OK;
+    });
+}

@@ -869,6 +869,7 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
 // returns the buffer holding the result (a or b).
 struct SortBufs {
     const unsigned long long* count;  // device-side element count (small-sort path)
+    unsigned long long* count_store = nullptr;  // writable count slot (when count is not ctl->results)
     unsigned long long* ka;
     uint32_t* va;
     unsigned long long* kb;
@@ -1045,6 +1046,184 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
 }
 
 }  // namespace
+
+// ------------------------------------------------------------ delivery
+// Sorted result runs kept in HBM for the streaming delivery (plan.delivery 2):
+// each run is (key = id_r << 32 | id_s, overlap) sorted by key.  A chunk of the
+// canonical output is every pair with id_r in [ja, jb): per run a binary
+// search bounds the segment, the segments are gathered, merged by K4 when
+// there is more than one, packed to ssj_pair and downloaded.
+struct DeviceRuns {
+    int device = -1;
+    int idbits = 1;
+    std::vector<unsigned long long*> keys;
+    std::vector<uint32_t*> ov;
+    std::vector<uint64_t> len;
+    ~DeviceRuns() {
+        if (device < 0) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        for (auto* p : keys) cudaFree(p);
+        for (auto* p : ov) cudaFree(p);
+        cudaSetDevice(cur);
+    }
+};
+
+namespace {
+
+void keep_device_run(EngineResult& out, int device, cudaStream_t s, const unsigned long long* keys,
+                     const uint32_t* ov, uint64_t count, int idbits) {
+    if (!count) return;
+    if (!out.runs) {
+        out.runs = std::make_shared<DeviceRuns>();
+        out.runs->device = device;
+    }
+    DeviceRuns& R = *out.runs;
+    R.idbits = std::max(R.idbits, idbits);
+    unsigned long long* k = nullptr;
+    uint32_t* v = nullptr;
+    CK(cudaMalloc(&k, count * 8));
+    CK(cudaMalloc(&v, count * 4));
+    CK(cudaMemcpyAsync(k, keys, count * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(v, ov, count * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    R.keys.push_back(k);
+    R.ov.push_back(v);
+    R.len.push_back(count);
+}
+
+// per-id_r counts of one run
+__global__ void run_histogram(const unsigned long long* keys, uint64_t n, unsigned int* hist, uint32_t hlen) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t j = static_cast<uint32_t>(keys[k] >> 32);
+        if (j < hlen) atomicAdd(hist + j, 1u);
+    }
+}
+
+// lower_bound of key in each run: one thread per (run, bound)
+struct RunTable {
+    const unsigned long long* keys[64];
+    uint64_t len[64];
+};
+__global__ void run_bounds(RunTable T, int nruns, unsigned long long lo_key, unsigned long long hi_key,
+                           uint64_t* out) {
+    const int t = threadIdx.x;
+    if (t >= 2 * nruns) return;
+    const int r = t >> 1;
+    const unsigned long long key = (t & 1) ? hi_key : lo_key;
+    uint64_t a = 0, b = T.len[r];
+    while (a < b) {
+        const uint64_t m = (a + b) >> 1;
+        if (T.keys[r][m] < key) a = m + 1;
+        else b = m;
+    }
+    out[t] = a;
+}
+
+cudaStream_t runs_stream(int device) {
+    static thread_local cudaStream_t streams[16] = {};
+    if (!streams[device & 15]) CK(cudaStreamCreateWithFlags(&streams[device & 15], cudaStreamNonBlocking));
+    return streams[device & 15];
+}
+
+}  // namespace
+
+uint64_t runs_total(const DeviceRuns& R) {
+    uint64_t t = 0;
+    for (uint64_t l : R.len) t += l;
+    return t;
+}
+
+void runs_histogram(const DeviceRuns& R, std::vector<uint64_t>& hist) {
+    if (R.keys.empty() || hist.empty()) return;
+    set_device(R.device);
+    cudaStream_t s = runs_stream(R.device);
+    const uint32_t hlen = static_cast<uint32_t>(hist.size());
+    unsigned int* d = nullptr;
+    CK(cudaMallocAsync(&d, hlen * 4ull, s));
+    CK(cudaMemsetAsync(d, 0, hlen * 4ull, s));
+    for (size_t r = 0; r < R.keys.size(); ++r) {
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((R.len[r] + 255) / 256, 148 * 16));
+        run_histogram<<<g, 256, 0, s>>>(R.keys[r], R.len[r], d, hlen);
+        CK(cudaGetLastError());
+    }
+    std::vector<unsigned int> h(hlen);
+    CK(cudaMemcpyAsync(h.data(), d, hlen * 4ull, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(d, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t j = 0; j < hlen; ++j) hist[j] += h[j];
+}
+
+void runs_extract(const DeviceRuns& R, uint32_t ja, uint32_t jb, PairVec& out) {
+    if (R.keys.empty() || ja >= jb) return;
+    set_device(R.device);
+    cudaStream_t s = runs_stream(R.device);
+    // segment bounds per run (in groups of 64 runs)
+    std::vector<uint64_t> lo(R.keys.size()), hi(R.keys.size());
+    {
+        uint64_t* d = nullptr;
+        CK(cudaMallocAsync(&d, 128 * 8, s));
+        for (size_t base = 0; base < R.keys.size(); base += 64) {
+            RunTable T{};
+            const int nr = static_cast<int>(std::min<size_t>(64, R.keys.size() - base));
+            for (int r = 0; r < nr; ++r) {
+                T.keys[r] = R.keys[base + r];
+                T.len[r] = R.len[base + r];
+            }
+            run_bounds<<<1, 128, 0, s>>>(T, nr, static_cast<unsigned long long>(ja) << 32,
+                                         static_cast<unsigned long long>(jb) << 32, d);
+            CK(cudaGetLastError());
+            uint64_t h[128];
+            CK(cudaMemcpyAsync(h, d, 2 * nr * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (int r = 0; r < nr; ++r) {
+                lo[base + r] = h[2 * r];
+                hi[base + r] = h[2 * r + 1];
+            }
+        }
+        CK(cudaFreeAsync(d, s));
+    }
+    uint64_t total = 0;
+    for (size_t r = 0; r < lo.size(); ++r) total += hi[r] - lo[r];
+    if (!total) return;
+    Arena A(s);
+    uint64_t launches = 0;
+    SortBufs SB{};
+    SB.ka = A.alloc<unsigned long long>(total);
+    SB.va = A.alloc<uint32_t>(total);
+    uint64_t at = 0;
+    int nonempty = 0;
+    for (size_t r = 0; r < lo.size(); ++r) {
+        const uint64_t len = hi[r] - lo[r];
+        if (!len) continue;
+        ++nonempty;
+        CK(cudaMemcpyAsync(SB.ka + at, R.keys[r] + lo[r], len * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(SB.va + at, R.ov[r] + lo[r], len * 4, cudaMemcpyDeviceToDevice, s));
+        at += len;
+    }
+    bool inb = false;
+    if (nonempty > 1) {  // merge the runs' segments (K4 over the gathered chunk)
+        SB.kb = A.alloc<unsigned long long>(total);
+        SB.vb = A.alloc<uint32_t>(total);
+        const uint32_t max_tiles = static_cast<uint32_t>((total + dev::kSortTile - 1) / dev::kSortTile);
+        SB.hist = A.alloc<uint32_t>(256ull * max_tiles);
+        SB.sums = A.alloc<uint32_t>((256ull * max_tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+        unsigned long long* cnt = A.alloc<unsigned long long>(1);
+        const unsigned long long tot = total;
+        CK(cudaMemcpyAsync(cnt, &tot, 8, cudaMemcpyHostToDevice, s));
+        SB.count = cnt;
+        inb = sort_results(SB, total, R.idbits, s, launches);
+    }
+    PairOut* packed = A.alloc<PairOut>(total);
+    pack_pairs<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va,
+                                                                        packed, total);
+    CK(cudaGetLastError());
+    const size_t old = out.size();
+    out.resize(old + total);
+    d2h_staged(out.data() + old, packed, total * sizeof(PairOut), s);
+}
 
 int engine_device_count() {
     int count = 0;
@@ -1447,7 +1626,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     while ((uint64_t(1) << idbits) < n + 1) ++idbits;
     SB.count = &d_ctl->results;
 
+    uint64_t counted = 0;  // matches in runs (every delivery mode)
     auto take_run = [&](const unsigned long long* keys, const uint32_t* ov, uint64_t count) {
+        counted += count;
+        if (plan.delivery == 1) return;
         PairVec run(count);
         for (uint64_t k = 0; k < count; ++k)
             run[k] = PairOut{static_cast<uint32_t>(keys[k] >> 32), static_cast<uint32_t>(keys[k] & 0xFFFFFFFFu),
@@ -1458,8 +1640,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     auto flush_results = [&](uint64_t count) {
         // K4 on the current result buffer, packed to ssj_pair records on the
         // device, then one (staged) download of the sorted run
+        counted += count;
+        if (plan.delivery == 1) {  // count only: nothing sorted or downloaded
+            CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
+            return;
+        }
         cudaEvent_t a = T.mark();
         bool inb = sort_results(SB, count, idbits, s, st.launches);
+        if (plan.delivery == 2) {  // keep the sorted run in HBM for the streaming delivery
+            cudaEvent_t b = T.mark();
+            keep_device_run(out, device, s, inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va, count, idbits);
+            st.ms_sort += Timer::ms(a, b);
+            CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
+            return;
+        }
         PairOut* packed = count ? A.alloc<PairOut>(count) : nullptr;
         if (count) {
             pack_pairs<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(inb ? SB.kb : SB.ka,
@@ -1750,7 +1944,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // merge sorted runs (one run unless the result buffer overflowed)
     if (runs.size() == 1) {
         out.pairs = std::move(runs[0]);
-    } else {
+    } else if (!runs.empty()) {
         PairVec merged;
         for (auto& r : runs) {
             PairVec tmp(merged.size() + r.size());
@@ -1783,7 +1977,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     out.verified = h_ctl.verified;
     out.saturated = h_ctl.saturated;
     st.verify_bytes = h_ctl.verify_bytes;
-    out.matched = out.pairs.size();
+    out.matched = counted;
     st.ms_upload = Timer::ms(e0, e_up);
     st.ms_build = Timer::ms(e_up, e_build);
     st.ms_filter = ms_filter;
@@ -1863,6 +2057,8 @@ void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& pla
     VP.ctl = d_ctl;
 
     std::vector<PairVec> runs;
+    uint64_t counted = 0;
+    SB.count_store = A.alloc<unsigned long long>(1);
     uint64_t k0 = 0;
     uint64_t batch = std::min<uint64_t>(total, env_u64("SSJB_RS_BATCH", uint64_t(1) << 32));
     double ms_verify = 0;
@@ -1889,7 +2085,14 @@ void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& pla
         }
         verify_bytes += h_ctl.verify_bytes;
         ++st.batches;
-        if (cnt) {
+        counted += cnt;
+        if (cnt && plan.delivery == 2) {
+            cudaEvent_t c0 = T.mark();
+            const bool inb = sort_results(SB, cnt, idbits, s, st.launches);
+            cudaEvent_t c1 = T.mark();
+            keep_device_run(out, device, s, inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va, cnt, idbits);
+            st.ms_sort += Timer::ms(c0, c1);
+        } else if (cnt && plan.delivery == 0) {
             cudaEvent_t c0 = T.mark();
             const bool inb = sort_results(SB, cnt, idbits, s, st.launches);
             PairOut* packed = A.alloc<PairOut>(cnt);
@@ -1921,7 +2124,7 @@ void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& pla
             at += r.size();
         }
     }
-    out.matched = out.pairs.size();
+    out.matched = counted;
     st.survivors = total;
     st.verify_bytes = verify_bytes;
     st.ms_upload = Timer::ms(e0, e_up);

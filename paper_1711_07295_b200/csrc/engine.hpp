@@ -53,8 +53,13 @@ struct EngineStats {
     int filter_kernel = 0;
 };
 
+// Sorted result runs left in device memory (delivery mode 2): the streaming
+// delivery extracts them id_r range by id_r range (engine.cu).
+struct DeviceRuns;
+
 struct EngineResult {
     PairVec pairs;  // sorted by (id_r, id_s)
+    std::shared_ptr<DeviceRuns> runs;  // delivery 2: further sorted runs in HBM (null if none)
     uint64_t candidates = 0, bitmap_tested = 0, pruned_bitmap = 0, verified = 0, matched = 0;
     uint64_t saturated = 0;
     double index_s = 0, candidates_s = 0, verify_s = 0;
@@ -67,6 +72,12 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 // NAIVE RS-join block (plan.r_begin..r_end of R) x S on `device`; pairs are
 // (R id, S id), sorted.
 void engine_join_rs(const Collection& r, const Collection& s, const RsPlan& plan, int device, EngineResult& out);
+// Streaming delivery over device runs: per-id_r match counts added into
+// hist[0..hist.size()), and the sorted pairs with id_r in [ja, jb) (all runs
+// merged) appended to out.
+void runs_histogram(const DeviceRuns& runs, std::vector<uint64_t>& hist);
+void runs_extract(const DeviceRuns& runs, uint32_t ja, uint32_t jb, PairVec& out);
+uint64_t runs_total(const DeviceRuns& runs);
 // The sketch-build kernel alone; copies the store (n * width/64 words) to out_host.
 void engine_build_bitmaps(const Collection& c, Method method, int width, int hash, int device,
                           uint64_t* out_host);

@@ -169,6 +169,7 @@ struct JoinPlan {
     // j0 of a record of size s: first index whose size >= ceil(p*s/q)
     std::vector<uint32_t> window_start;
     uint64_t window_pairs = 0;   // sum over rows of (i - j0(i))
+    int delivery = 0;            // 0 pairs to host, 1 count only, 2 sorted runs kept in HBM
 };
 
 // Required overlap of the similarity functions (reference src/similarity.cpp:93-115).
@@ -184,6 +185,7 @@ struct RsPlan {
     std::vector<int32_t> minov;  // minov[|r|+|s|]
     bool cosine = false;
     size_t r_begin = 0, r_end = 0;
+    int delivery = 0;            // as JoinPlan::delivery
 };
 RsPlan make_rs_plan(const Collection& r, const Collection& s, const Options& o, size_t r_begin, size_t r_end);
 

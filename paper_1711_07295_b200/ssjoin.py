@@ -249,6 +249,52 @@ def join(coll: Collection, opts: capi.JoinOptions, other: Collection | None = No
     return _take_report(lib, out)
 
 
+def join_stream(coll: Collection, opts: capi.JoinOptions, on_chunk, other: Collection | None = None,
+                chunk_pairs: int = 0) -> Report:
+    """Streaming delivery (B200 extension, ssjb_join_stream): ``on_chunk(pairs)``
+    receives consecutive chunks of the canonical pair list as numpy views
+    valid only during the call (copy to keep); returning True stops the join.
+    The returned report holds counters only (no pairs)."""
+    lib = coll.lib
+    err = []
+
+    def sink(ptr, n, _user):
+        try:
+            raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), (n * 16,))
+            return 1 if on_chunk(raw.view(PAIR_DTYPE)) else 0
+        except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
+            err.append(e)
+            return 1
+
+    cb = capi.PAIR_SINK(sink)
+    out = C.c_void_p()
+    status = lib.ssjb_join_stream(coll.handle, other.handle if other is not None else None,
+                                  C.byref(opts), chunk_pairs, cb, None, C.byref(out))
+    if err:
+        raise err[0]
+    _check(lib, status)
+    return _take_report(lib, out)
+
+
+def join_count(coll: Collection, opts: capi.JoinOptions, other: Collection | None = None) -> Report:
+    """Count-first (ssjb_join_count): counters incl. matched, no pairs."""
+    lib = coll.lib
+    out = C.c_void_p()
+    _check(lib, lib.ssjb_join_count(coll.handle, other.handle if other is not None else None,
+                                    C.byref(opts), C.byref(out)))
+    return _take_report(lib, out)
+
+
+def join_write_pairs(coll: Collection, opts: capi.JoinOptions, path: str,
+                     other: Collection | None = None) -> Report:
+    """Streams the pairs into ``path`` as "id_r id_s overlap" lines (ssjb_join_write_pairs)."""
+    lib = coll.lib
+    out = C.c_void_p()
+    _check(lib, lib.ssjb_join_write_pairs(coll.handle, other.handle if other is not None else None,
+                                          C.byref(opts), os.fsencode(path), C.byref(out)))
+    return _take_report(lib, out)
+
+
 def join_rows(coll: Collection, opts: capi.JoinOptions, row_begin: int, row_end: int,
               device: int = -1) -> Report:
     """Rows [row_begin, row_end) of a self-join (B200 extension, ssjb_join_rows)."""

@@ -186,3 +186,24 @@ def test_partition_rows_balances_window_pairs(lib, golden_arrays):
     for parts in (1, 2, 3, 8):
         b = S.partition_rows(coll, opts, parts)
         assert b[0] == 0 and b[-1] == len(coll) and (np.diff(b.astype(np.int64)) >= 0).all()
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_delivery_entry_points_fail_loudly_without_gpu(lib, tmp_path):
+    import ctypes as C
+    coll = S.Collection.from_records(lib, [[1, 2], [1, 2, 3]])
+    opts = S.par_bitmap_options(lib, threshold=(1, 2))
+    for call in (lambda: S.join_count(coll, opts),
+                 lambda: S.join_stream(coll, opts, lambda a: None),
+                 lambda: S.join_write_pairs(coll, opts, str(tmp_path / "p.txt")),
+                 lambda: S.join(coll, S.default_options(lib, algorithm=capi.SSJ_ALGO_NAIVE), coll)):
+        with pytest.raises(S.SsjError) as e:
+            call()
+        assert e.value.status == capi.SSJ_ERROR_INTERNAL and "CUDA" in e.value.message
+    # argument errors come first, like ssj_join's (reference src/capi.cpp:220-228)
+    out = C.c_void_p()
+    assert lib.ssjb_join_count(None, None, C.byref(opts), C.byref(out)) == capi.SSJ_ERROR_INVALID_ARGUMENT
+    assert lib.ssjb_join_count(coll.handle, coll.handle, C.byref(opts), C.byref(out)) == \
+        capi.SSJ_ERROR_INVALID_ARGUMENT
+    assert b"naive" in lib.ssj_last_error()
+    assert lib.ssjb_report_write_pairs(None, b"x") == capi.SSJ_ERROR_INVALID_ARGUMENT
