@@ -3,6 +3,9 @@
 #include "host_core.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -232,39 +235,145 @@ double Collection::mean_size() const {
     return static_cast<double>(tokens.size()) / static_cast<double>(size());
 }
 
+// ------------------------------------------------------- host parallelism
+// Host threads for ingest (parse, canonical sort, write): SSJB_HOST_THREADS or
+// the hardware concurrency, at most 64.
+unsigned host_threads() {
+    static const unsigned t = []() {
+        const char* v = std::getenv("SSJB_HOST_THREADS");
+        long x = v && *v ? std::strtol(v, nullptr, 10) : static_cast<long>(std::thread::hardware_concurrency());
+        return static_cast<unsigned>(std::max(1L, std::min(64L, x)));
+    }();
+    return t;
+}
+
+namespace {
+
+// f(t, begin, end) over T contiguous slices of [0, n); serial below `grain`.
+template <class F>
+void parallel_for(size_t n, F&& f, size_t grain = 1 << 14) {
+    const unsigned T = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(host_threads(), n / grain)));
+    if (T <= 1) {
+        f(0u, size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::exception_ptr err;
+    std::mutex mu;
+    for (unsigned t = 0; t < T; ++t) {
+        const size_t a = n * t / T, b = n * (t + 1) / T;
+        th.emplace_back([&, t, a, b]() {
+            try {
+                f(t, a, b);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!err) err = std::current_exception();
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+    if (err) std::rethrow_exception(err);
+}
+
+// Parallel merge sort: T sorted slices, then rounds of pairwise merges.
+template <class T, class Less>
+void parallel_sort(std::vector<T>& v, Less less) {
+    const size_t n = v.size();
+    unsigned P = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(host_threads(), n / (1 << 15))));
+    if (P <= 1) {
+        std::sort(v.begin(), v.end(), less);
+        return;
+    }
+    std::vector<size_t> cut(P + 1);
+    for (unsigned k = 0; k <= P; ++k) cut[k] = n * k / P;
+    parallel_for(P, [&](unsigned, size_t a, size_t b) {
+        for (size_t k = a; k < b; ++k) std::sort(v.begin() + cut[k], v.begin() + cut[k + 1], less);
+    }, 1);
+    std::vector<T> tmp(n);
+    std::vector<T>* src = &v;
+    std::vector<T>* dst = &tmp;
+    while (cut.size() > 2) {
+        std::vector<size_t> next;
+        const size_t runs = cut.size() - 1;
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < runs; k += 2) {
+            next.push_back(cut[k]);
+            if (k + 1 < runs) {
+                th.emplace_back([=, &less]() {
+                    std::merge(src->begin() + cut[k], src->begin() + cut[k + 1], src->begin() + cut[k + 1],
+                               src->begin() + cut[k + 2], dst->begin() + cut[k], less);
+                });
+            } else {
+                std::copy(src->begin() + cut[k], src->begin() + cut[k + 1], dst->begin() + cut[k]);
+            }
+        }
+        for (auto& x : th) x.join();
+        next.push_back(n);
+        cut.swap(next);
+        std::swap(src, dst);
+    }
+    if (src != &v) v.swap(*src);
+}
+
+}  // namespace
+
 void canonicalize(Collection& c, std::vector<uint32_t>&& raw, const std::vector<uint64_t>& off) {
     // reference src/collection.cpp:44-54: per-record sort + dedup, then records
-    // by (size, lexicographic tokens); id = position.
+    // by (size, lexicographic tokens); id = position.  Host-parallel: records
+    // are sorted in slices, the record order is a parallel merge sort over
+    // (size, first two tokens, index) keys that touch the token array only on
+    // ties, and the canonical CSR is filled by slices.
     const size_t n = off.size() - 1;
     std::vector<uint32_t> len(n);
-    for (size_t r = 0; r < n; ++r) {
-        auto b = raw.begin() + static_cast<ptrdiff_t>(off[r]);
-        auto e = raw.begin() + static_cast<ptrdiff_t>(off[r + 1]);
-        std::sort(b, e);
-        len[r] = static_cast<uint32_t>(std::unique(b, e) - b);
-    }
-    std::vector<uint32_t> order(n);
-    std::iota(order.begin(), order.end(), 0u);
-    auto less = [&](uint32_t a, uint32_t b) {
-        if (len[a] != len[b]) return len[a] < len[b];
-        const uint32_t* pa = raw.data() + off[a];
-        const uint32_t* pb = raw.data() + off[b];
-        return std::lexicographical_compare(pa, pa + len[a], pb, pb + len[b]);
+    parallel_for(n, [&](unsigned, size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) {
+            auto rb = raw.begin() + static_cast<ptrdiff_t>(off[r]);
+            auto re = raw.begin() + static_cast<ptrdiff_t>(off[r + 1]);
+            std::sort(rb, re);
+            len[r] = static_cast<uint32_t>(std::unique(rb, re) - rb);
+        }
+    }, 4096);
+    struct Item {
+        uint64_t key;  // (t0 << 32 | t1) of the deduplicated record (missing tokens 0)
+        uint32_t len;
+        uint32_t idx;
     };
-    std::sort(order.begin(), order.end(), less);
+    std::vector<Item> items(n);
+    parallel_for(n, [&](unsigned, size_t a, size_t b) {
+        for (size_t r = a; r < b; ++r) {
+            const uint32_t* p = raw.data() + off[r];
+            const uint64_t k = (len[r] > 0 ? static_cast<uint64_t>(p[0]) << 32 : 0) | (len[r] > 1 ? p[1] : 0u);
+            items[r] = Item{k, len[r], static_cast<uint32_t>(r)};
+        }
+    });
+    const uint32_t* rd = raw.data();
+    const uint64_t* od = off.data();
+    parallel_sort(items, [rd, od](const Item& x, const Item& y) {
+        if (x.len != y.len) return x.len < y.len;
+        if (x.key != y.key) return x.key < y.key;
+        // same size, same first two tokens: the rest of the sequence, then
+        // the input position (std::sort in the reference is not stable, but
+        // equal records are indistinguishable in the canonical output)
+        const uint32_t* pa = rd + od[x.idx];
+        const uint32_t* pb = rd + od[y.idx];
+        for (uint32_t k = 2; k < x.len; ++k)
+            if (pa[k] != pb[k]) return pa[k] < pb[k];
+        return x.idx < y.idx;
+    });
     c.offsets.assign(n + 1, 0);
     uint64_t total = 0;
+    uint32_t ms = 0;
     for (size_t k = 0; k < n; ++k) {
-        total += len[order[k]];
+        total += items[k].len;
         c.offsets[k + 1] = total;
+        ms = std::max(ms, items[k].len);
     }
     c.tokens.resize(total);
-    c.max_size = 0;
-    for (size_t k = 0; k < n; ++k) {
-        uint32_t r = order[k];
-        std::memcpy(c.tokens.data() + c.offsets[k], raw.data() + off[r], len[r] * sizeof(uint32_t));
-        c.max_size = std::max(c.max_size, len[r]);
-    }
+    c.max_size = ms;
+    parallel_for(n, [&](unsigned, size_t a, size_t b) {
+        for (size_t k = a; k < b; ++k)
+            std::memcpy(c.tokens.data() + c.offsets[k], raw.data() + off[items[k].idx], items[k].len * sizeof(uint32_t));
+    });
     // size index of the sorted collection (the length filter's window starts)
     c.first_ge.assign(static_cast<size_t>(c.max_size) + 2, static_cast<uint32_t>(n));
     for (size_t k = n; k-- > 0;) c.first_ge[c.rec_size(k)] = static_cast<uint32_t>(k);
@@ -293,39 +402,110 @@ std::unique_ptr<Collection> collection_from_csr(const uint32_t* tokens, const ui
 
 namespace {
 
-std::unique_ptr<Collection> read_id_lines(std::istream& in) {
-    // reference src/collection.cpp:97-137 (ids as-is; line-numbered parse errors)
-    std::vector<uint32_t> raw;
-    std::vector<uint64_t> off{0};
-    std::string line;
-    size_t line_no = 0;
+// reference src/collection.cpp:97-137 (ids as-is; line-numbered parse errors).
+// The file is read whole and cut at line boundaries into one slice per host
+// thread; slices parse independently and the first error in file order wins.
+std::unique_ptr<Collection> read_id_lines(const std::string& path) {
+    std::vector<char> buf;
+    {
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        if (!f) throw IoError("cannot open " + path);
+        std::fseek(f, 0, SEEK_END);
+        const long size = std::ftell(f);
+        std::fseek(f, 0, SEEK_SET);
+        buf.resize(size > 0 ? static_cast<size_t>(size) : 0);
+        const size_t got = buf.empty() ? 0 : std::fread(buf.data(), 1, buf.size(), f);
+        std::fclose(f);
+        if (got != buf.size()) throw IoError("cannot read " + path);
+    }
+    const size_t L = buf.size();
+    const char* d = buf.data();
+    const unsigned T = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(host_threads(), L >> 20)));
+    std::vector<size_t> cut(T + 1, L);
+    cut[0] = 0;
+    for (unsigned t = 1; t < T; ++t) {  // slices start right after a newline
+        size_t p = std::max(cut[t - 1], L * t / T);
+        while (p < L && (p == 0 || d[p - 1] != '\n')) ++p;
+        cut[t] = p;
+    }
+    struct Slice {
+        std::vector<uint32_t> tokens;
+        std::vector<uint64_t> ends;  // per line: token count so far
+        uint32_t max_id = 0;
+        bool any = false;
+        size_t err_line = SIZE_MAX;  // 0-based line within the slice
+        std::string err;
+    };
+    std::vector<Slice> sl(T);
+    parallel_for(T, [&](unsigned, size_t ta, size_t tb) {
+        for (size_t t = ta; t < tb; ++t) {
+            Slice& S = sl[t];
+            S.tokens.reserve((cut[t + 1] - cut[t]) / 3);
+            size_t pos = cut[t];
+            const size_t end = cut[t + 1];
+            size_t line = 0;
+            // getline semantics: every '\n' ends a line; trailing text without
+            // one is a last line
+            while (pos < end) {
+                size_t eol = pos;
+                while (eol < end && d[eol] != '\n') ++eol;
+                size_t q = pos;
+                while (q < eol) {
+                    while (q < eol && d[q] == ' ') ++q;
+                    if (q >= eol) break;
+                    uint64_t value = 0;
+                    while (q < eol && d[q] != ' ') {
+                        const char ch = d[q];
+                        if (ch < '0' || ch > '9' || value > 0xFFFFFFFFull) {
+                            S.err_line = line;
+                            S.err = "expected a token id";
+                            return;
+                        }
+                        value = value * 10 + static_cast<uint64_t>(ch - '0');
+                        ++q;
+                    }
+                    if (value > 0xFFFFFFFFull) {
+                        S.err_line = line;
+                        S.err = "token id out of range";
+                        return;
+                    }
+                    S.tokens.push_back(static_cast<uint32_t>(value));
+                    S.max_id = std::max(S.max_id, static_cast<uint32_t>(value));
+                    S.any = true;
+                }
+                S.ends.push_back(S.tokens.size());
+                ++line;
+                pos = eol + 1;
+            }
+        }
+    }, 1);
+    size_t lines_before = 0;
+    for (unsigned t = 0; t < T; ++t) {
+        if (sl[t].err_line != SIZE_MAX)
+            throw ParseError("parse error at line " + std::to_string(lines_before + sl[t].err_line + 1) + ": " +
+                             sl[t].err);
+        lines_before += sl[t].ends.size();
+    }
+    std::vector<uint64_t> tok_base(T + 1, 0), line_base(T + 1, 0);
     uint32_t max_id = 0;
     bool any = false;
-    while (std::getline(in, line)) {
-        ++line_no;
-        size_t pos = 0;
-        const size_t L = line.size();
-        while (pos < L) {
-            while (pos < L && line[pos] == ' ') ++pos;
-            if (pos >= L) break;
-            size_t end = pos;
-            uint64_t value = 0;
-            while (end < L && line[end] != ' ') {
-                char ch = line[end];
-                if (ch < '0' || ch > '9' || value > 0xFFFFFFFFull)
-                    throw ParseError("parse error at line " + std::to_string(line_no) + ": expected a token id");
-                value = value * 10 + static_cast<uint64_t>(ch - '0');
-                ++end;
-            }
-            if (value > 0xFFFFFFFFull)
-                throw ParseError("parse error at line " + std::to_string(line_no) + ": token id out of range");
-            raw.push_back(static_cast<uint32_t>(value));
-            max_id = std::max(max_id, static_cast<uint32_t>(value));
-            any = true;
-            pos = end;
-        }
-        off.push_back(raw.size());
+    for (unsigned t = 0; t < T; ++t) {
+        tok_base[t + 1] = tok_base[t] + sl[t].tokens.size();
+        line_base[t + 1] = line_base[t] + sl[t].ends.size();
+        max_id = std::max(max_id, sl[t].max_id);
+        any |= sl[t].any;
     }
+    std::vector<uint32_t> raw(tok_base[T]);
+    std::vector<uint64_t> off(line_base[T] + 1, 0);
+    parallel_for(T, [&](unsigned, size_t ta, size_t tb) {
+        for (size_t t = ta; t < tb; ++t) {
+            if (!sl[t].tokens.empty())
+                std::memcpy(raw.data() + tok_base[t], sl[t].tokens.data(), sl[t].tokens.size() * 4);
+            for (size_t k = 0; k < sl[t].ends.size(); ++k) off[line_base[t] + k + 1] = tok_base[t] + sl[t].ends[k];
+            std::vector<uint32_t>().swap(sl[t].tokens);
+        }
+    }, 1);
+    std::vector<char>().swap(buf);
     auto c = std::make_unique<Collection>();
     c->universe = any ? static_cast<uint64_t>(max_id) + 1 : 0;
     canonicalize(*c, std::move(raw), off);
@@ -421,9 +601,9 @@ int64_t poisson_draw(std::mt19937_64& rng, double mean) {
 }  // namespace
 
 std::unique_ptr<Collection> read_collection(const std::string& path, int input_format, int q) {
+    if (input_format == 0) return read_id_lines(path);
     std::ifstream in(path);
     if (!in) throw IoError("cannot open " + path);
-    if (input_format == 0) return read_id_lines(in);
     // Any other code is text; q-grams only for SSJ_INPUT_QGRAMS (reference src/capi.cpp:134-140).
     const int kind = input_format == 2 ? 1 : 0;
     const int qq = input_format == 2 ? q : 2;
@@ -434,27 +614,36 @@ std::unique_ptr<Collection> read_collection(const std::string& path, int input_f
 }
 
 void write_collection(const Collection& c, const std::string& path) {
-    // reference src/collection.cpp:153-168
-    std::ofstream out(path);
-    if (!out) throw IoError("cannot open " + path + " for writing");
-    std::string buf;
-    buf.reserve(1 << 20);
-    char num[16];
-    for (size_t r = 0; r < c.size(); ++r) {
-        for (uint64_t k = c.offsets[r]; k < c.offsets[r + 1]; ++k) {
-            if (k != c.offsets[r]) buf.push_back(' ');
-            int l = std::snprintf(num, sizeof num, "%u", c.tokens[k]);
-            buf.append(num, static_cast<size_t>(l));
-        }
-        buf.push_back('\n');
-        if (buf.size() > (1u << 20)) {
-            out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
-            buf.clear();
-        }
+    // reference src/collection.cpp:153-168: one line per record, tokens
+    // separated by one space.  Record slices are formatted by the host threads
+    // and written in order.
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open " + path + " for writing");
+    const size_t n = c.size();
+    const size_t block = size_t(1) << 16;  // records per formatting task
+    const unsigned T = host_threads();
+    bool ok = true;
+    for (size_t base = 0; base < n && ok; base += block * T) {
+        const size_t span = std::min(n - base, block * T);
+        std::vector<std::string> out(T);
+        parallel_for(span, [&](unsigned t, size_t a, size_t b) {
+            std::string& o = out[t];
+            o.reserve((c.offsets[base + b] - c.offsets[base + a]) * 8 + (b - a));
+            char num[16];
+            for (size_t r = base + a; r < base + b; ++r) {
+                for (uint64_t k = c.offsets[r]; k < c.offsets[r + 1]; ++k) {
+                    if (k != c.offsets[r]) o.push_back(' ');
+                    char* e = std::to_chars(num, num + sizeof num, c.tokens[k]).ptr;
+                    o.append(num, static_cast<size_t>(e - num));
+                }
+                o.push_back('\n');
+            }
+        }, 1024);
+        for (auto& o : out)
+            if (!o.empty() && std::fwrite(o.data(), 1, o.size(), f) != o.size()) ok = false;
     }
-    out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
-    out.flush();
-    if (!out) throw IoError("write failed for " + path);
+    if (std::fclose(f) != 0) ok = false;
+    if (!ok) throw IoError("write failed for " + path);
 }
 
 std::unique_ptr<Collection> generate(const GeneratorConfig& cfg) {

@@ -108,6 +108,8 @@ struct Collection {
     ~Collection();
 };
 
+// Host threads used by ingest (env SSJB_HOST_THREADS, default: all cores).
+unsigned host_threads();
 // Canonicalises raw id records in place (per-record sort+dedup, record order).
 void canonicalize(Collection& c, std::vector<uint32_t>&& raw_tokens,
                   const std::vector<uint64_t>& raw_offsets);

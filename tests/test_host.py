@@ -207,3 +207,70 @@ def test_delivery_entry_points_fail_loudly_without_gpu(lib, tmp_path):
         capi.SSJ_ERROR_INVALID_ARGUMENT
     assert b"naive" in lib.ssj_last_error()
     assert lib.ssjb_report_write_pairs(None, b"x") == capi.SSJ_ERROR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("threads", ["1", "3", "8"])
+def test_parallel_ingest_matches_reference(lib, ref, tmp_path, threads):
+    """Multi-MB id files parse in per-thread slices (SSJB_HOST_THREADS); the
+    canonical collection, universe and error lines must equal the reference's
+    read_id_lines (src/collection.cpp:97-137) regardless of slicing."""
+    import subprocess
+    import sys
+    rng = np.random.default_rng(7)
+    n = 150_000
+    sizes = rng.integers(0, 12, n)
+    lines = []
+    for k, sz in enumerate(sizes):
+        toks = rng.integers(0, 5000 if k % 3 else 70, sz)       # duplicates inside records
+        sep = "  " if k % 11 == 0 else " "
+        lines.append(sep.join(map(str, toks.tolist())) + (" " if k % 13 == 0 else ""))
+    body = "\n".join(lines)
+    cases = {"trailing_nl": body + "\n", "no_trailing_nl": body, "blank_tail": body + "\n\n \n"}
+    bad_line = 123_457
+    bad = lines[:]
+    bad[bad_line - 1] = bad[bad_line - 1] + " 12x"
+    cases["error"] = "\n".join(bad) + "\n"
+    over = lines[:]
+    over[140_001 - 1] = "4294967296"
+    cases["overflow"] = "\n".join(over) + "\n"
+    for name, text in cases.items():
+        p = tmp_path / f"{name}.txt"
+        p.write_text(text)
+        # run the product in a child so SSJB_HOST_THREADS takes effect
+        code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+                "from paper_1711_07295_b200 import load_library, ssjoin as S\n"
+                "lib = load_library()\n"
+                "try:\n"
+                "    c = S.Collection.load(lib, %r); t, o = c.csr()\n"
+                "    np.savez(%r, t=t, o=o, u=c.universe)\n"
+                "except S.SsjError as e:\n"
+                "    print('ERR', e.status, e.message)\n") % (ROOT, str(p), str(tmp_path / "out.npz"))
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                           env={**os.environ, "SSJB_HOST_THREADS": threads}, check=True)
+        try:
+            want = S.Collection.load(ref, str(p))
+        except S.SsjError as e:
+            assert r.stdout.startswith("ERR"), (name, r.stdout)
+            assert r.stdout.split(None, 2)[2].strip() == e.message, name
+            continue
+        got = np.load(tmp_path / "out.npz")
+        tw, ow = want.csr()
+        assert (got["t"] == tw).all() and (got["o"] == ow).all(), name
+        assert int(got["u"]) == want.universe, name
+
+
+def test_parallel_canonical_sort_matches_reference(lib, ref):
+    """collection_from_csr's parallel record sort == the reference canonical
+    order, on records with long shared prefixes (ties beyond the first two
+    tokens) and many exact duplicates."""
+    rng = np.random.default_rng(11)
+    recs = []
+    for k in range(60_000):
+        base = [1, 2, 3, 4] if k % 4 == 0 else [int(x) for x in rng.integers(0, 50, 2)]
+        recs.append(base + [int(x) for x in rng.integers(0, 9, k % 5)])
+    recs += [[9, 9, 9]] * 500 + [[]] * 100
+    a = S.Collection.from_records(lib, recs)
+    b = S.Collection.from_records(ref, recs)
+    ta, oa = a.csr()
+    tb, ob = b.csr()
+    assert (ta == tb).all() and (oa == ob).all()
