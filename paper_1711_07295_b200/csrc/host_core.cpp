@@ -663,6 +663,18 @@ std::unique_ptr<Collection> generate(const GeneratorConfig& cfg) {
         }
         for (auto& v : cumulative) v /= total;
     }
+    // guide table: u in [b/G, (b+1)/G) (exact, G a power of two) has its
+    // upper_bound in [guide[b], guide[b+1]]; the search runs on that bracket
+    constexpr int kGuideBits = 16;
+    std::vector<uint32_t> guide;
+    if (cfg.distribution == 1) {
+        const size_t G = size_t(1) << kGuideBits;
+        guide.resize(G + 1);
+        for (size_t b = 0; b <= G; ++b)
+            guide[b] = static_cast<uint32_t>(
+                std::upper_bound(cumulative.begin(), cumulative.end(), std::ldexp(static_cast<double>(b), -kGuideBits)) -
+                cumulative.begin());
+    }
     const uint64_t span = static_cast<uint64_t>(cfg.universe);
     const uint64_t limit = std::numeric_limits<uint64_t>::max() - std::numeric_limits<uint64_t>::max() % span;
     auto draw_token = [&]() -> int64_t {
@@ -672,28 +684,77 @@ std::unique_ptr<Collection> generate(const GeneratorConfig& cfg) {
             return static_cast<int64_t>(v % span);
         }
         double u = uniform01(rng);
-        auto it = std::upper_bound(cumulative.begin(), cumulative.end(), u);
+        const size_t b = static_cast<size_t>(std::ldexp(u, kGuideBits));  // u < 1
+        auto it = std::upper_bound(cumulative.begin() + guide[b], cumulative.begin() + guide[b + 1], u);
         if (it == cumulative.end()) --it;
         return static_cast<int64_t>(it - cumulative.begin());
     };
-    std::vector<std::vector<int64_t>> sets;
-    sets.reserve(static_cast<size_t>(cfg.num_sets));
+    // Records as CSR of distinct ranks.  A record draws until it holds `size`
+    // distinct ranks (the draw count depends on the repeats, so the stream is
+    // consumed serially); membership is a bitmap over the universe with the
+    // record's bits cleared afterwards.
+    const bool dense = cfg.universe <= (int64_t(1) << 30);
+    std::vector<uint64_t> seen(dense ? (static_cast<size_t>(cfg.universe) + 63) / 64 : 0, 0);
     std::unordered_set<int64_t> drawn;
+    std::vector<std::vector<int64_t>> sparse;  // records of universes above 2^30
+    std::vector<uint32_t> raw;
+    std::vector<uint64_t> off{0};
+    raw.reserve(static_cast<size_t>(cfg.num_sets * cfg.mean_size * 1.05) + 16);
+    off.reserve(static_cast<size_t>(cfg.num_sets) + 1);
     for (int64_t i = 0; i < cfg.num_sets; ++i) {
         int64_t size = 0;
         while (size == 0) size = poisson_draw(rng, cfg.mean_size);
         size = std::min(size, cfg.universe);
-        drawn.clear();
-        int64_t attempts = 0;
+        const size_t start = raw.size();
+        if (!dense) sparse.emplace_back();
+        int64_t have = 0, attempts = 0;
         const int64_t budget = 1000 * size + 1000;
-        while (static_cast<int64_t>(drawn.size()) < size && attempts < budget) {
-            drawn.insert(draw_token());
+        auto add = [&](int64_t t) {
+            if (!dense) {
+                if (drawn.insert(t).second) {
+                    sparse.back().push_back(t);
+                    ++have;
+                }
+                return;
+            }
+            uint64_t& w = seen[static_cast<size_t>(t) >> 6];
+            const uint64_t bit = uint64_t(1) << (t & 63);
+            if (!(w & bit)) {
+                w |= bit;
+                raw.push_back(static_cast<uint32_t>(t));
+                ++have;
+            }
+        };
+        while (have < size && attempts < budget) {
+            add(draw_token());
             ++attempts;
         }
-        for (int64_t t = 0; static_cast<int64_t>(drawn.size()) < size; ++t) drawn.insert(t);
-        sets.emplace_back(drawn.begin(), drawn.end());
+        for (int64_t t = 0; have < size; ++t) add(t);
+        if (dense)
+            for (size_t k = start; k < raw.size(); ++k) seen[raw[k] >> 6] = 0;
+        else
+            drawn.clear();
+        off.push_back(raw.size());
     }
-    return build_renumbered(sets, decimal_less);
+    if (!dense) return build_renumbered(sparse, decimal_less);  // the general renumbering
+    // renumber rarest-first, ties by the decimal text of the rank
+    // (reference src/collection.cpp:58-93 over std::to_string keys)
+    std::vector<uint64_t> freq(static_cast<size_t>(cfg.universe), 0);
+    for (uint32_t t : raw) ++freq[t];
+    std::vector<uint32_t> order;
+    for (size_t t = 0; t < freq.size(); ++t)
+        if (freq[t]) order.push_back(static_cast<uint32_t>(t));
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+        if (freq[a] != freq[b]) return freq[a] < freq[b];
+        return decimal_less(a, b);
+    });
+    std::vector<uint32_t> id(static_cast<size_t>(cfg.universe), 0);
+    for (size_t k = 0; k < order.size(); ++k) id[order[k]] = static_cast<uint32_t>(k);
+    for (auto& t : raw) t = id[t];
+    auto c = std::make_unique<Collection>();
+    c->universe = order.size();
+    canonicalize(*c, std::move(raw), off);
+    return c;
 }
 
 // ================================================================= options
