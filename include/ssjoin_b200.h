@@ -103,6 +103,11 @@ ssj_status ssjb_join_write_pairs(const ssj_collection* r, const ssj_collection* 
 /* Writes a materialised report's pairs in the same text format. */
 ssj_status ssjb_report_write_pairs(const ssj_report* report, const char* path);
 
+/* Mean device time in ms of the sketch-build kernel (K1) over `reps` launches
+ * on the device replica, L2 flushed before each (the K1 roofline probe). */
+ssj_status ssjb_time_build(const ssj_collection* coll, int method, int bits, int hash, int device,
+                           int reps, double* ms_per_launch);
+
 const char* ssjb_version(void);
 
 #ifdef __cplusplus

@@ -129,6 +129,8 @@ _EXT_PROTOS = {
     "ssjb_set_devices": (C.c_int, [C.c_int]),
     "ssjb_report_stats": (C.c_int, [P, C.POINTER(Stats)]),
     "ssjb_build_bitmaps": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
+    "ssjb_time_build": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(C.c_double)]),
     "ssjb_version": (C.c_char_p, []),
 }
 SSJB_SYMBOLS = tuple(_EXT_PROTOS)

@@ -756,6 +756,22 @@ SSJB_API ssj_status ssjb_report_stats(const ssj_report* report, ssjb_stats* out)
     });
 }
 
+SSJB_API ssj_status ssjb_time_build(const ssj_collection* coll, int method, int bits, int hash, int device, int reps,
+                                    double* ms_per_launch) {
+    return guarded([&]() {
+        if (coll == nullptr || ms_per_launch == nullptr || reps < 1) {
+            set_error("null argument or reps < 1");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        ssjb::Method m = to_method(method);
+        if (m == ssjb::Method::Combined) throw std::invalid_argument("combined method must be resolved before building");
+        if (bits <= 0 || bits % 64 != 0) throw std::invalid_argument("bitmap width must be a positive multiple of 64");
+        *ms_per_launch = ssjb::engine_time_build(*coll->c, m, bits, hash == SSJ_HASH_MULT ? 1 : 0,
+                                                 device < 0 ? 0 : device, reps);
+        return SSJ_OK;
+    });
+}
+
 SSJB_API ssj_status ssjb_build_bitmaps(const ssj_collection* coll, int method, int bits, int hash, int device,
                                        uint64_t* out_host) {
     return guarded([&]() {

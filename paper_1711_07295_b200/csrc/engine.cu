@@ -1290,6 +1290,36 @@ void engine_build_bitmaps(const Collection& c, Method method, int width, int has
     cudaStreamDestroy(s);
 }
 
+double engine_time_build(const Collection& c, Method method, int width, int hash, int device, int reps) {
+    // K1 alone on the device replica, L2 flushed (256 MiB write) before every
+    // timed launch so the token stream comes from HBM; mean ms per launch
+    set_device(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double total = 0;
+    {
+        uint64_t h2d = 0, launches = 0;
+        auto rep = replica_for(c, device, s, h2d, launches);
+        Arena A(s);
+        const int W = width / 64;
+        uint64_t* bits = A.alloc<uint64_t>((c.size() + kPadRows) * W);
+        const size_t flush_bytes = size_t(256) << 20;
+        uint8_t* flush = A.alloc<uint8_t>(flush_bytes);
+        Timer T(s);
+        for (int r = 0; r < reps + 1; ++r) {
+            CK(cudaMemsetAsync(flush, r & 0xFF, flush_bytes, s));
+            cudaEvent_t a = T.mark();
+            if (!launch_build_sub(*rep, bits, nullptr, method, width, 0, hash, s, launches))
+                launch_build(*rep, bits, method, width, hash, s, launches);
+            cudaEvent_t b = T.mark();
+            CK(cudaStreamSynchronize(s));
+            if (r > 0) total += Timer::ms(a, b);  // first launch: warm-up
+        }
+    }
+    cudaStreamDestroy(s);
+    return reps > 0 ? total / reps : 0.0;
+}
+
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
     using Clock = std::chrono::steady_clock;
     set_device(device);

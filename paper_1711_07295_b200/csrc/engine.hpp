@@ -81,6 +81,8 @@ uint64_t runs_total(const DeviceRuns& runs);
 // The sketch-build kernel alone; copies the store (n * width/64 words) to out_host.
 void engine_build_bitmaps(const Collection& c, Method method, int width, int hash, int device,
                           uint64_t* out_host);
+// Mean device time (ms) of the sketch-build kernel over `reps` launches, L2 flushed.
+double engine_time_build(const Collection& c, Method method, int width, int hash, int device, int reps);
 void engine_pin(const Collection& c, int device);
 void engine_unpin(const Collection& c, int device);
 void engine_release_host(const Collection& c);  // undo host page registration
