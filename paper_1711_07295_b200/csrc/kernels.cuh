@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kBuildRecs) build_sketches(BuildParams P) {
 }
 
 // Set / Xor sketches with LPR lanes per record (LPR = 1..32, a power of two):
-// lane k of a record's group folds tokens k, k+LPR, ... into register
+// lane k of a record's group folds 16-byte chunks k, k+LPR, ... into register
 // sketches, then the group combines them with shuffles (OR for Set, XOR for
 // Xor -- both order-independent, reference src/bitmap.cpp:70-81).  Token loads
 // are coalesced across the group.  With W2 > 0 the same token pass also
@@ -179,6 +179,7 @@ struct BuildParams2 {
     int hash_mult;
     int pow2, pow2_2;
     int lpr_log2;          // log2(lanes per record)
+    uint64_t total_tokens; // tokens in the array (bound of the 16-byte loads)
 };
 
 template <int W, int W2>
@@ -193,10 +194,7 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
     for (int w = 0; w < W; ++w) row[w] = 0;
 #pragma unroll
     for (int w = 0; w < (W2 > 0 ? W2 : 1); ++w) row2[w] = 0;
-    if (live) {
-        const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
-        for (uint64_t k = b + sub; k < e; k += lpr) {
-            const uint32_t t = __ldg(P.tokens + k);
+    auto fold = [&](uint32_t t) {
             const uint32_t h = hash_token(t, P.width, P.hash_mult, P.pow2);
             const uint64_t bit = 1ull << (h & 63);
 #pragma unroll
@@ -209,6 +207,34 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
                 const uint64_t bit2 = 1ull << (h2 & 63);
 #pragma unroll
                 for (int w = 0; w < W2; ++w) row2[w] ^= (h2 >> 6) == uint32_t(w) ? bit2 : 0ull;
+            }
+    };
+    if (live) {
+        // the record's span as aligned 16-byte chunks, chunk c to lane c mod
+        // lpr, four 128-bit loads in flight per lane before folding (a scalar
+        // strided loop is bound by one load round trip per token)
+        const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
+        for (uint64_t c = (b & ~uint64_t(3)) + 4ull * sub; c < e; c += 16ull * lpr) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t cc = c + 4ull * lpr * u;
+                if (cc + 4 <= P.total_tokens) {
+                    v[u] = cc < e ? __ldg(reinterpret_cast<const uint4*>(P.tokens + cc)) : make_uint4(0, 0, 0, 0);
+                } else {
+                    v[u].x = cc < e ? P.tokens[cc] : 0u;
+                    v[u].y = cc + 1 < e ? P.tokens[cc + 1] : 0u;
+                    v[u].z = cc + 2 < e ? P.tokens[cc + 2] : 0u;
+                    v[u].w = 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t cc = c + 4ull * lpr * u;
+                const uint32_t t4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (cc + q >= b && cc + q < e) fold(t4[q]);
             }
         }
     }
