@@ -1723,6 +1723,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     VP.res_ov = SB.va;
     VP.res_cap = res_cap;
     VP.ctl = d_ctl;
+    VP.warp_mode = static_cast<int>(env_u64("SSJB_WARP_VERIFY", 1));
     if (W2 && !naive) {  // level-2 re-test of level-1 survivors before the merge
         VP.bits2 = d_bits2;
         VP.maxham = d_maxham;
@@ -1815,7 +1816,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         // survivor count read on the device: no host round trip between K2 and K3
         VP.count_ptr = &d_ctl->survivors;
         VP.count_cap = surv_cap;
-        const unsigned vgrid = static_cast<unsigned>(sms) * 8;
+        static const unsigned vmul = static_cast<unsigned>(env_u64("SSJB_VERIFY_GRID", 8));
+        const unsigned vgrid = static_cast<unsigned>(sms) * vmul;
         if (VP.w2 == 4) dev::verify_pairs<4><<<vgrid, 256, 0, s>>>(VP);
         else if (VP.w2 == 8) dev::verify_pairs<8><<<vgrid, 256, 0, s>>>(VP);
         else dev::verify_pairs<0><<<vgrid, 256, 0, s>>>(VP);

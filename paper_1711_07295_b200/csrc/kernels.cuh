@@ -812,6 +812,7 @@ struct VerifyParams {
     const uint64_t* bits2;    // level-2 Xor sketches (n x w2 words), or null
     const int32_t* maxham;    // maxham[|r|+|s|] (with bits2)
     int w2;
+    int warp_mode;            // 1: warp per pair when the survivors are few
 };
 
 // One thread per surviving pair: branch-free sorted merge with the
@@ -820,10 +821,84 @@ struct VerifyParams {
 // With bits2, a pair is first re-tested against the wider level-2 Xor sketch
 // (the same exact bound, reference src/bitmap.cpp:125-143, at 64*w2 bits):
 // level-1 survivors the wider sketch rejects cannot match and skip the merge.
+// Survivor counts up to this are verified one warp per pair: the merge of a
+// thread-per-pair kernel is a chain of ~|r|+|s| dependent loads, so a launch
+// with few survivors costs that chain's latency (~30 us at C2's 86-token
+// records) however few pairs it has.  A warp instead takes 32 tokens of the
+// shorter record at a time, each lane binary-searches its token in the
+// longer one (independent searches, ~log2|s| loads deep), and the ballot
+// counts the overlap.  On a match the overlap is the full intersection, the
+// same exact value the merge produces; the early exit (overlap + tokens left
+// < required) only ever stops non-matching pairs, as in the reference's
+// verify (src/similarity.cpp:174-175).
+constexpr unsigned long long kWarpVerifyMax = 1ull << 15;
+
+template <int W2>
+__device__ __forceinline__ void verify_warp_mode(const VerifyParams& P, unsigned long long count, int lane) {
+    const unsigned long long nwarps = static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5);
+    const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (unsigned long long k = gw; k < count; k += nwarps) {
+        const uint2 pr = P.surv[k];
+        const uint32_t j = pr.x, i = pr.y;
+        const uint64_t ab = P.offsets[j], ae = P.offsets[j + 1];
+        const uint64_t bb = P.offsets[i], be = P.offsets[i + 1];
+        const uint32_t na = static_cast<uint32_t>(ae - ab), nb = static_cast<uint32_t>(be - bb);
+        if constexpr (W2 > 0) {
+            int h = 0;
+            if (lane < W2) h = __popcll(__ldg(P.bits2 + static_cast<uint64_t>(j) * W2 + lane) ^
+                                        __ldg(P.bits2 + static_cast<uint64_t>(i) * W2 + lane));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+            if (h > P.maxham[na + nb]) continue;  // rejected by the level-2 sketch (warp-uniform)
+        }
+        const int32_t need = need_overlap(P.need, na, nb);
+        const bool a_short = na <= nb;
+        const uint32_t* S = P.tokens + (a_short ? ab : bb);
+        const uint32_t* L = P.tokens + (a_short ? bb : ab);
+        const uint32_t ns = a_short ? na : nb, nl = a_short ? nb : na;
+        int32_t o = 0;
+        for (uint32_t base = 0; base < ns; base += 32) {
+            bool hit = false;
+            if (base + lane < ns) {
+                const uint32_t t = __ldg(S + base + lane);
+                uint32_t lo = 0, len = nl;  // lower_bound of t in L
+                while (len > 0) {
+                    const uint32_t half = len >> 1;
+                    if (__ldg(L + lo + half) < t) {
+                        lo += half + 1;
+                        len -= half + 1;
+                    } else {
+                        len = half;
+                    }
+                }
+                hit = lo < nl && __ldg(L + lo) == t;
+            }
+            o += __popc(__ballot_sync(0xFFFFFFFFu, hit));
+            const uint32_t left = ns - min(ns, base + 32);
+            if (o + static_cast<int32_t>(left) < need) break;
+        }
+        const bool matched = o >= need;
+        if (lane == 0) {
+            atomicAdd(&P.ctl->verify_bytes, 4ull * (na + nb) + (matched ? 16ull : 0ull));
+            if (matched) {
+                const unsigned long long slot = atomicAdd(&P.ctl->results, 1ull);
+                if (slot < P.res_cap) {
+                    P.res_keys[slot] = (static_cast<unsigned long long>(j) << 32) | i;
+                    P.res_ov[slot] = static_cast<uint32_t>(o);
+                }
+            }
+        }
+    }
+}
+
 template <int W2>
 __global__ void verify_pairs(VerifyParams P) {
     const int lane = threadIdx.x & 31;
     const unsigned long long count = min(*P.count_ptr, P.count_cap);
+    if (count <= kWarpVerifyMax && P.warp_mode) {
+        verify_warp_mode<W2>(P, count, lane);
+        return;
+    }
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < count;
          base += stride) {
