@@ -1610,6 +1610,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
+    uint32_t* d_satlist = A.alloc<uint32_t>(rows + 1);
     // per-(item,row) survivor counts let the saturation rescan touch one chunk per row
     uint64_t n_items = tl.item_base.back();
     const uint64_t ic_bytes = n_items * tl.tile_rows * 4;
@@ -1849,9 +1850,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.cutoff = FP.cutoff;
             RP.words = W;
             RP.bypass_all = FP.bypass_all;
+            RP.sat_list = d_satlist;
+            RP.sat_count = &d_ctl->sat_rows;
+            const unsigned gf = static_cast<unsigned>(std::min<uint64_t>((rows + 255) / 256, uint64_t(sms) * 8));
+            dev::find_saturated<<<gf, 256, 0, s>>>(d_rowcnt, rows, plan.capacity, d_satlist, d_ctl);
             const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, uint64_t(sms) * 8));
             dev::rescan_saturated<<<g, 256, 0, s>>>(RP);
-            ++st.launches;
+            st.launches += 2;
             CK(cudaGetLastError());
         }
         dev::CountParams CP{};

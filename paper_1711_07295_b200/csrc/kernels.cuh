@@ -29,7 +29,8 @@ struct Control {
     unsigned long long work_next;   // persistent-kernel work counter
     unsigned long long tested, pruned, verified, saturated;  // counter sums
     unsigned long long verify_bytes;  // algorithmic bytes of K3
-    unsigned long long pad[7];
+    unsigned long long sat_rows;      // rows listed by find_saturated
+    unsigned long long pad[6];
 };
 
 // ------------------------------------------------------------------ hashing
@@ -598,7 +599,28 @@ struct RescanParams {
     int maxham_len;
     const uint16_t* tile_counts;  // per (item, tile, part, row) survivors (tcgen05 filter), or null
     uint32_t tiles_per_item, tile_cols, tile_parts;
+    const uint32_t* sat_list;     // rows (row - row_begin) whose count reaches the capacity
+    const unsigned long long* sat_count;
 };
+
+// Saturated rows into a list (coalesced count reads, one atomic per warp), so
+// the rescan runs one warp per listed row: no per-row scan of the whole shard
+// (a chain of dependent loads per warp) when few or no rows saturate.
+__global__ void find_saturated(const uint32_t* rowcnt, uint32_t nrows, uint32_t capacity, uint32_t* list,
+                               Control* ctl) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < nrows;
+         base += gridDim.x * blockDim.x) {
+        const uint32_t r = base + lane;
+        const bool sat = r < nrows && rowcnt[r] >= capacity;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, sat);
+        if (!bal) continue;
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(&ctl->sat_rows, static_cast<unsigned long long>(__popc(bal)));
+        at = __shfl_sync(0xFFFFFFFFu, at, 0);
+        if (sat) list[at + __popc(bal & ((1u << lane) - 1u))] = r;
+    }
+}
 
 constexpr int kRescanLut = 4096;  // maxham[] entries staged in shared memory
 
@@ -615,9 +637,9 @@ __global__ void __launch_bounds__(256) rescan_saturated(RescanParams P) {
     const int32_t* maxham = lut_smem ? lut : P.maxham;
     const int lane = threadIdx.x & 31;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < P.row_end - P.row_begin; r += warps) {
-        const uint32_t c = P.rowcnt[r];
-        if (c < P.capacity) continue;
+    const uint32_t nsat = static_cast<uint32_t>(*P.sat_count);
+    for (uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < nsat; idx += warps) {
+        const uint32_t r = P.sat_list[idx];
         const uint32_t i = P.row_begin + r;
         const uint32_t si = P.sizes[i];
         const uint32_t j0 = P.wstart[si];
