@@ -64,6 +64,8 @@ struct TcParams {
     int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
     const uint32_t* npc2;      // no-extension int8 operands: -pc of columns 2k, 2k+1 as s16x2
     int debug;                 // bit 0: skip the epilogue math (pipeline probe)
+    int bias;                  // added to every level-1 accumulator by the operands' extension
+                               // (non-negative accumulators: SWAR masks, masks16_nonneg)
     unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
 };
 
@@ -246,6 +248,29 @@ __device__ __forceinline__ void masks16(const uint32_t (&d)[32], int c, uint32_t
     m1 = x1;
 }
 
+// Survivor masks of a packed 64-column load whose accumulators are
+// non-negative and below 0x8000 (biased operands): per register one
+// subtraction whose halves cannot borrow into each other -- (c + 0x8000) - d
+// has bit 15 clear exactly when d > c -- then one shift and one LOP3 place
+// the two survivor bits.  Bit order per 32 columns: bit k (k < 16) = column
+// 2k, bit 16 + k = column 2k + 1 (see mask_col<true>).  c < 0: all survive.
+__device__ __forceinline__ void masks16_nonneg(const uint32_t (&d)[32], int c, uint32_t& m0, uint32_t& m1) {
+    if (c < 0) {
+        m0 = m1 = 0xFFFFFFFFu;
+        return;
+    }
+    const uint32_t C2 = ((static_cast<uint32_t>(min(c, 0x7FFE)) | 0x8000u)) * 0x10001u;
+    uint32_t x0 = 0, x1 = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t bits = (1u << k) | (1u << (16 + k));
+        x0 |= ~((C2 - d[k]) >> (15 - k)) & bits;
+        x1 |= ~((C2 - d[16 + k]) >> (15 - k)) & bits;
+    }
+    m0 = x0;
+    m1 = x1;
+}
+
 // Survivor mask of 32 accumulator columns: column k survives iff
 // cim1_k - D_k < 0 (sign bit set).  Four independent funnel-shift chains
 // (8 columns each) keep the ALU pipe fed; the subtraction is an IMAD on the
@@ -337,6 +362,14 @@ __device__ __forceinline__ void tc_flush(uint2* q, int& qlen, const TcParams& P,
     __syncwarp();
 }
 
+// Column of mask bit k: identity, or (PERM) the masks16_nonneg order where bit
+// k < 16 is column 2k and bit 16 + k is column 2k + 1.
+template <bool PERM>
+__device__ __forceinline__ uint32_t mask_col(int k) {
+    return PERM ? static_cast<uint32_t>(2 * (k & 15) + (k >> 4)) : static_cast<uint32_t>(k);
+}
+
+template <bool PERM = false>
 __device__ __forceinline__ void tc_emit(uint32_t m, uint32_t base_col, uint32_t row, uint2* q, int& qlen,
                                         const TcParams& P, int lane) {
     const int c = __popc(m);
@@ -355,7 +388,7 @@ __device__ __forceinline__ void tc_emit(uint32_t m, uint32_t base_col, uint32_t 
         while (m) {
             int k = __ffs(m) - 1;
             m &= m - 1;
-            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + k, row);
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + mask_col<PERM>(k), row);
             ++base;
         }
         return;
@@ -365,7 +398,7 @@ __device__ __forceinline__ void tc_emit(uint32_t m, uint32_t base_col, uint32_t 
     while (m) {
         int k = __ffs(m) - 1;
         m &= m - 1;
-        q[pos++] = make_uint2(base_col + k, row);
+        q[pos++] = make_uint2(base_col + mask_col<PERM>(k), row);
     }
     qlen += total;
     __syncwarp();
@@ -629,6 +662,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 bypass = static_cast<int64_t>(si) > P.cutoff;
 #pragma unroll
                 for (int w = 0; w < L::kWords; ++w) pc += __popcll(P.bits[static_cast<uint64_t>(i) * L::kWords + w]);
+                pc += P.bias;  // thresholds shift with the biased accumulators
                 if constexpr (K2 > 0) {
 #pragma unroll
                     for (int w = 0; w < W2; ++w) mine2[w] = P.bits2[static_cast<uint64_t>(i) * W2 + w];
@@ -888,6 +922,7 @@ struct ExpandParams {
     int K2;                 // level-2 bytes per row (0: none)
     int fp4;                // level-1 encoding
     int with_size;          // append the 16-byte size chunk (single-CTA kernels)
+    int ext_bias;           // added to each level-1 extension byte of B (accumulator bias / 2)
 };
 
 __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -4, -6
@@ -901,7 +936,8 @@ __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -
 }
 
 // int8 segment chunk c (16 bytes = 16 elements) of a sketch with `words` words
-__device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c, uint32_t (&a)[4], uint32_t (&b)[4]) {
+__device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c, uint32_t (&a)[4], uint32_t (&b)[4],
+                                          int ext_bias = 0) {
     const int bitsn = 64 * words;
     if (16 * c < bitsn) {
         const uint32_t bits16 = static_cast<uint32_t>(row[(16 * c) / 64] >> ((16 * c) % 64)) & 0xFFFFu;
@@ -916,7 +952,8 @@ __device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c,
         for (int w = 0; w < words; ++w) pcnt += __popcll(row[w]);
         const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
         a[0] = 0x0101u;
-        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(-hi))) | (static_cast<uint32_t>(static_cast<uint8_t>(-lo)) << 8);
+        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(ext_bias - hi))) |
+               (static_cast<uint32_t>(static_cast<uint8_t>(ext_bias - lo)) << 8);
     }
 }
 
@@ -959,7 +996,7 @@ __global__ void expand_operands(ExpandParams P) {
     if (c < P.K1 / 16) {
         const uint64_t* row = P.bits + static_cast<uint64_t>(r) * P.words;
         if (P.fp4) expand_f4(row, P.words, c, a, b);
-        else expand_i8(row, P.words, c, a, b);
+        else expand_i8(row, P.words, c, a, b, P.ext_bias);
     } else if (c < (P.K1 + P.K2) / 16) {
         expand_i8(P.bits2 + static_cast<uint64_t>(r) * P.words2, P.words2, c - P.K1 / 16, a, b);
     } else {

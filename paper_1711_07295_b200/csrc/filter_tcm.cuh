@@ -60,6 +60,13 @@ __device__ __forceinline__ void tcm_block(TcmRow& R, uint32_t acc_col, const uin
         const int c16 = max(R.cim1, -32768);
         if (__any_sync(0xFFFFFFFFu, R.bypass || any_above16(d, c16))) {
             uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
+            if (P.bias > 0) {  // non-negative accumulators: 3-instruction SWAR masks, permuted bits
+                if (!R.bypass) masks16_nonneg(d, R.cim1, m0, m1);
+                R.cnt += __popc(m0) + __popc(m1);
+                if (__any_sync(0xFFFFFFFFu, m0 != 0)) tc_emit<true>(m0, wbase, R.i, q, qlen, P, lane);
+                if (__any_sync(0xFFFFFFFFu, m1 != 0)) tc_emit<true>(m1, wbase + 32, R.i, q, qlen, P, lane);
+                return;
+            }
             if (!R.bypass) masks16(d, c16, m0, m1);
             R.cnt += __popc(m0) + __popc(m1);
             if (__any_sync(0xFFFFFFFFu, m0 != 0)) tc_emit(m0, wbase, R.i, q, qlen, P, lane);
@@ -261,6 +268,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
 #pragma unroll
                     for (int w = 0; w < L::kWords; ++w)
                         R[r].pc += __popcll(P.bits[static_cast<uint64_t>(i) * L::kWords + w]);
+                    R[r].pc += P.bias;  // thresholds shift with the biased accumulators
                 }
                 R[r].lo = R[r].valid ? max(j0, info.c0) : info.c1;
                 R[r].hi = R[r].valid ? min(i, info.c1) : info.c1;
