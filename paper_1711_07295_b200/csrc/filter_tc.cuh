@@ -83,15 +83,20 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
 
 // Spin without a suspend hint (single-lane producer / MMA roles: wake-up
 // latency is on the critical path there).
+// try_wait suspend-time hint: a waiting warp is parked until the phase
+// completes (or this many ns pass) instead of re-issuing the probe, leaving
+// issue slots to the epilogue warps that share the SM sub-partitions
+constexpr uint32_t kSuspendNs = 1u << 20;
+
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
@@ -100,10 +105,10 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "r"(kSuspendNs)
         : "memory");
 }
 
