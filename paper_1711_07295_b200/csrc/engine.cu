@@ -748,13 +748,21 @@ size_t operand_row(int words, int variant) {
     return operand_bytes(words, variant == 2) + (variant == 1 ? 64 * 4 + 32 : 0) + (variant == 3 ? 0 : 16);
 }
 
-// Bias of the level-1 accumulators built into variant 0's extension bytes:
-// with b <= 128, D = 2<b_i,b_j> - pc_j lies in [-b, b]; each of the two
-// extension bytes gains b/2 (still an int8), so D + b lies in [0, 2b] and the
-// epilogue can use borrow-free packed subtractions (masks16_nonneg).
-int level1_ext_bias(int words, int variant) {
+// Accumulator bias built into the int8 operands' extension bytes: with
+// b <= 128, D = 2<b_i,b_j> - pc_j lies in [-b, b]; adding b (spread over the
+// extension bytes, each still an int8) puts D + b in [0, 2b], so the epilogue
+// can use borrow-free packed subtractions (masks16_nonneg).  Level 1 of
+// variants 0 (level-1 GEMM) and 1 (level-1 + level-2 GEMM); level 2 of
+// variant 1 (256-bit sketch: bias 256 over four bytes).
+bool acc_bias_on() {
     static const bool on = env_u64("SSJB_BIAS", 1) != 0;
-    return on && variant == 0 && words <= 2 ? 32 * words : 0;
+    return on;
+}
+int level1_acc_bias(int words, int variant) {
+    return acc_bias_on() && (variant == 0 || variant == 1) && words <= 2 ? 64 * words : 0;
+}
+int level2_acc_bias(int words2, int variant) {
+    return acc_bias_on() && variant == 1 && words2 == 4 ? 256 : 0;
 }
 
 void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int words2, const uint32_t* sizes,
@@ -775,7 +783,8 @@ void launch_expand(const uint64_t* bits, int words, const uint64_t* bits2, int w
     E.K1 = variant == 4 ? 64 * words : static_cast<int>(operand_bytes(words, variant == 2));
     E.K2 = variant == 1 ? 64 * words2 + 32 : 0;
     E.with_size = (variant == 3 || variant == 4) ? 0 : 1;
-    E.ext_bias = level1_ext_bias(words, variant);
+    E.acc_bias = level1_acc_bias(words, variant);
+    E.acc_bias2 = level2_acc_bias(words2, variant);
     const int kct = (E.K1 + E.K2) / 16 + E.with_size;
     const uint64_t threads = static_cast<uint64_t>(rows - row0) * kct;
     dev::expand_operands<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(E);
@@ -1735,7 +1744,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.neg1 = -1;
         TP.npc2 = noext ? sk->npc2 : nullptr;
         TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
-        TP.bias = 2 * level1_ext_bias(W, variant);
+        TP.bias = level1_acc_bias(W, variant);
+        TP.bias2 = level2_acc_bias(W2, variant);
         if (TP.debug & 2) {
             TP.trace = A.alloc<unsigned long long>(2048 + 2 * 8192);
             CK(cudaMemsetAsync(TP.trace, 0, (2048 + 2 * 8192) * 8, s));
@@ -2021,7 +2031,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
                 TP.opA = a1;
                 TP.opB = b1;
-                TP.bias = 0;  // variant-1 operands carry no accumulator bias
+                TP.bias = level1_acc_bias(W, 1);  // the variant-1 operands' biases
+                TP.bias2 = level2_acc_bias(W2, 1);
                 st.filter_kernel = 2;
             }
         }

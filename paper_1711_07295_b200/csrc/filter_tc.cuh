@@ -64,8 +64,8 @@ struct TcParams {
     int neg1;                  // always -1 (keeps the epilogue subtraction an IMAD)
     const uint32_t* npc2;      // no-extension int8 operands: -pc of columns 2k, 2k+1 as s16x2
     int debug;                 // bit 0: skip the epilogue math (pipeline probe)
-    int bias;                  // added to every level-1 accumulator by the operands' extension
-                               // (non-negative accumulators: SWAR masks, masks16_nonneg)
+    int bias, bias2;           // added to every level-1 / level-2 accumulator by the operands'
+                               // extension (non-negative accumulators: SWAR masks, masks16_nonneg)
     unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
 };
 
@@ -274,6 +274,16 @@ __device__ __forceinline__ void masks16_nonneg(const uint32_t (&d)[32], int c, u
     }
     m0 = x0;
     m1 = x1;
+}
+
+// 32-column version (16 packed registers) of masks16_nonneg, same bit order.
+__device__ __forceinline__ uint32_t mask16_32_nonneg(const uint32_t (&d)[16], int c) {
+    if (c < 0) return 0xFFFFFFFFu;
+    const uint32_t C2 = ((static_cast<uint32_t>(min(c, 0x7FFE)) | 0x8000u)) * 0x10001u;
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x |= ~((C2 - d[k]) >> (15 - k)) & ((1u << k) | (1u << (16 + k)));
+    return x;
 }
 
 // Survivor mask of 32 accumulator columns: column k survives iff
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             if constexpr (K2 > 0) {
 #pragma unroll
                 for (int w = 0; w < W2; ++w) pc2 += __popcll(mine2[w]);
+                pc2 += P.bias2;
             }
             const uint32_t lo_i = valid ? max(j0, info.c0) : info.c1;
             const uint32_t hi_i = valid ? min(i, info.c1) : info.c1;
@@ -762,13 +773,17 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 // (the level-2 GEMM variant keeps the unpacked path below: it is bound
                 // by shared-memory operand traffic, and the packed s16 masks cost more
                 // ALU per group when most pairs survive level 1 -- 3.17 vs 2.68 ms, C2 tau=0.5)
-                if constexpr (KIND == kKindI8 && K2 == 0) {
+                // (with biased operands the level-2 GEMM variant takes the packed
+                // path too: non-negative accumulators make its masks 3 instructions
+                // per register -- masks16_nonneg -- so the packed path wins there)
+                const bool packed32 = K2 == 0 || (P.bias > 0 && P.bias2 > 0);
+                if constexpr (KIND == kKindI8) {
                     // int8 groups of 32 columns: level-1 accumulators
                     // as packed s16 in one load latency.  Thresholds per run of equal
                     // column size (sizes are sorted, so a group holds 1-3 runs): a
                     // ballot over the lanes' column sizes gives each run's columns.
 #pragma unroll 1
-                    for (int g = 0; g < (groups_done ? 0 : L::kColsPerWarp / 32); ++g) {
+                    for (int g = 0; g < (groups_done || !packed32 ? 0 : L::kColsPerWarp / 32); ++g) {
                         const int cl = cw + g * 32;
                         const uint32_t gbase = wbase + g * 32;
                         uint32_t rm = 0xFFFFFFFFu;
@@ -808,7 +823,13 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         if (!__any_sync(0xFFFFFFFFu, bypass || (rm != 0 && any_above16_32(d, max(cmin, -32768)))))
                             continue;
                         uint32_t m = 0xFFFFFFFFu, e2 = 0xFFFFFFFFu;
-                        if (fast) {
+                        bool perm = false;
+                        if (fast && P.bias > 0 && (K2 == 0 || P.bias2 > 0)) {
+                            // biased accumulators: SWAR masks in the permuted bit order
+                            perm = true;
+                            if (!bypass) m = mask16_32_nonneg(d, cim1);
+                            if constexpr (K2 > 0) e2 = mask16_32_nonneg(d2, cim1_2);
+                        } else if (fast) {
                             if (!bypass) m = mask16_32(d, max(cim1, -32768));
                             if constexpr (K2 > 0) e2 = mask16_32(d2, max(cim1_2, -32768));
                         } else {
@@ -824,12 +845,15 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                             if (!bypass) m = mm;
                             if constexpr (K2 > 0) e2 = ee;
                         }
-                        m &= rm;
+                        m &= rm;  // (rm is all ones on the fast path, so the bit order is moot)
                         cnt += __popc(m);
                         const uint32_t e = m & e2;
-                        if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
+                        if (__any_sync(0xFFFFFFFFu, e != 0)) {
+                            if (perm) tc_emit<true>(e, gbase, i, q, qlen, P, lane);
+                            else tc_emit(e, gbase, i, q, qlen, P, lane);
+                        }
                     }
-                    groups_done = true;
+                    if (packed32) groups_done = true;
                 }
 #pragma unroll 1
                 for (int g = 0; g < (groups_done ? 0 : L::kColsPerWarp / 32); ++g) {
@@ -927,7 +951,7 @@ struct ExpandParams {
     int K2;                 // level-2 bytes per row (0: none)
     int fp4;                // level-1 encoding
     int with_size;          // append the 16-byte size chunk (single-CTA kernels)
-    int ext_bias;           // added to each level-1 extension byte of B (accumulator bias / 2)
+    int acc_bias, acc_bias2;  // bias the extension adds to level-1 / level-2 accumulators
 };
 
 __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -4, -6
@@ -941,8 +965,15 @@ __device__ __forceinline__ uint32_t e2m1_neg(int v) {  // codes of -1, -2, -3, -
 }
 
 // int8 segment chunk c (16 bytes = 16 elements) of a sketch with `words` words
+// Extension chunk: A holds 1 in bytes [0, nb), B holds shares of
+// (acc_bias - pc_j) in those bytes -- floor((v + k) / nb) for byte k, which
+// sum to v exactly (Hermite's identity) -- so the GEMM adds acc_bias - pc_j to
+// every accumulator of column j.  nb = 2 without a bias (shares -ceil(pc/2),
+// -floor(pc/2)); 4 for the level-2 bias of 256 so every share fits an int8.
+__device__ __forceinline__ int floor_div_int(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
 __device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c, uint32_t (&a)[4], uint32_t (&b)[4],
-                                          int ext_bias = 0) {
+                                          int acc_bias = 0) {
     const int bitsn = 64 * words;
     if (16 * c < bitsn) {
         const uint32_t bits16 = static_cast<uint32_t>(row[(16 * c) / 64] >> ((16 * c) % 64)) & 0xFFFFu;
@@ -955,10 +986,12 @@ __device__ __forceinline__ void expand_i8(const uint64_t* row, int words, int c,
     } else if (16 * c == bitsn) {
         int pcnt = 0;
         for (int w = 0; w < words; ++w) pcnt += __popcll(row[w]);
-        const int hi = (pcnt + 1) / 2, lo = pcnt / 2;  // each <= 128 for b <= 256
-        a[0] = 0x0101u;
-        b[0] = (static_cast<uint32_t>(static_cast<uint8_t>(ext_bias - hi))) |
-               (static_cast<uint32_t>(static_cast<uint8_t>(ext_bias - lo)) << 8);
+        const int nb = acc_bias > 128 ? 4 : 2;
+        const int v = acc_bias - pcnt;
+        for (int k = 0; k < nb; ++k) {
+            a[0] |= 1u << (8 * k);
+            b[0] |= static_cast<uint32_t>(static_cast<uint8_t>(floor_div_int(v + k, nb))) << (8 * k);
+        }
     }
 }
 
@@ -1001,9 +1034,9 @@ __global__ void expand_operands(ExpandParams P) {
     if (c < P.K1 / 16) {
         const uint64_t* row = P.bits + static_cast<uint64_t>(r) * P.words;
         if (P.fp4) expand_f4(row, P.words, c, a, b);
-        else expand_i8(row, P.words, c, a, b, P.ext_bias);
+        else expand_i8(row, P.words, c, a, b, P.acc_bias);
     } else if (c < (P.K1 + P.K2) / 16) {
-        expand_i8(P.bits2 + static_cast<uint64_t>(r) * P.words2, P.words2, c - P.K1 / 16, a, b);
+        expand_i8(P.bits2 + static_cast<uint64_t>(r) * P.words2, P.words2, c - P.K1 / 16, a, b, P.acc_bias2);
     } else {
         a[0] = b[0] = P.sizes[r];  // the size chunk
     }
