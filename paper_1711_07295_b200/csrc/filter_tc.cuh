@@ -367,6 +367,17 @@ __device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int
     return m;
 }
 
+// survivors_mixed with the tile's column sizes read from global memory
+template <int KIND>
+__device__ __forceinline__ uint32_t survivors_mixed_g(const uint32_t (&d)[32], int base, const int32_t* maxham,
+                                                      uint32_t si, const uint32_t* gsz, int cl) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+        m |= ((base - maxham[si + __ldg(gsz + cl + k)] - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
+    return m;
+}
+
 __device__ __forceinline__ void tc_flush(uint2* q, int& qlen, const TcParams& P, int lane) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(qlen));
@@ -438,6 +449,11 @@ struct TcLayout {
     // soon as its MMAs complete (the epilogue never holds it)
     static constexpr int kSide = kNoExt ? NT * 4 + NT * 2 : 0;  // sizes u32[NT] | -pc pairs u32[NT/2]
     static constexpr int NE = kNoExt ? 2 * NS : 1;              // side-ring slots
+    // level-2 GEMM: the epilogue reads column sizes from global memory (L2) so a
+    // B stage is released when its MMAs complete, not when the epilogue is done
+    // with the tile -- with only two 59 KB stages fitting, a stage's lifetime
+    // (copy + MMAs + epilogue) otherwise paces the pipeline
+    static constexpr bool kEarlyB = K2 > 0;
     static constexpr int kEpiWarps = NT == 192 ? 12 : 16;      // 3 or 4 per TMEM lane quarter
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
@@ -508,7 +524,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         }
         for (int s = 0; s < NS; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], L::kNoExt ? 1 : 1 + kTcEpiWarps);
+            mbar_init(&b_empty[s], (L::kNoExt || L::kEarlyB) ? 1 : 1 + kTcEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -704,7 +720,15 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             for (uint32_t t = 0; t < info.ntiles; ++t) {
                 const int st = static_cast<int>(st_idx), as = static_cast<int>(acc_idx);
                 if constexpr (L::kNoExt) mbar_wait_u32(smem_u32(&e_full[0]) + 8 * se_idx, se_phase);
-                else mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
+                else if constexpr (!L::kEarlyB) mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
+                // (early-released stages: the accumulator's completion implies the
+                // operands arrived; sizes come from gsz below)
+                const uint32_t* gsz = P.sizes + info.c0 + t * NT;
+                uint32_t pre0 = 0, pre1 = 0;
+                if constexpr (L::kEarlyB) {  // issue the size loads before the accumulator wait
+                    pre0 = __ldg(gsz + part * L::kColsPerWarp);
+                    pre1 = __ldg(gsz + part * L::kColsPerWarp + L::kColsPerWarp - 1);
+                }
                 mbar_wait_u32(accfull_u32 + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512) P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
@@ -714,8 +738,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 const uint32_t* sNpc = side_sz + NT;  // -pc pairs of the tile's columns
                 const int cw = part * L::kColsPerWarp;               // this warp's first column
                 const uint32_t wbase = info.c0 + t * NT + cw;
-                const uint32_t szw0 = tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw);
-                const uint32_t szw1 = tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw + L::kColsPerWarp - 1);
+                const uint32_t szw0 = L::kEarlyB ? pre0 : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw);
+                const uint32_t szw1 =
+                    L::kEarlyB ? pre1 : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cw + L::kColsPerWarp - 1);
                 // fast path: every group of this warp's range is inside all 32
                 // windows and of one column size (the bulk of the pair space)
                 const bool fast = szw0 == szw1 && wbase >= lo_max && wbase + L::kColsPerWarp <= hi_min;
@@ -736,7 +761,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         int dummy2[32];
                         tmem_ld32(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
                         e = m & (uni ? survivors32<true, KIND>(d2, cim1_2, dummy2, P.neg1)
-                                     : survivors_mixed<KIND, L::kKCT>(d2, pc2, maxham, si, stage, cl));
+                                     : (L::kEarlyB ? survivors_mixed_g<KIND>(d2, pc2, maxham, si, gsz, cl)
+                                                   : survivors_mixed<KIND, L::kKCT>(d2, pc2, maxham, si, stage, cl)));
                     }
                     // (without the level-2 GEMM, level-1 survivors are emitted and
                     // verify_pairs re-tests them against the level-2 sketch first)
@@ -796,7 +822,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         uint32_t d[16], d2[16];
                         tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cl, d);
                         if constexpr (K2 > 0) tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
-                        const uint32_t colsz = fast ? 0u : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cl + lane);
+                        const uint32_t colsz = fast ? 0u
+                                                    : (L::kEarlyB ? __ldg(gsz + cl + lane)
+                                                                  : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cl + lane));
                         tmem_wait_ld();
                         if constexpr (L::kNoExt) {  // D - pc_j per column
                             const uint4* np = reinterpret_cast<const uint4*>(sNpc + cl / 2);
@@ -875,8 +903,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         const uint32_t rm = low_mask(kh) & ~low_mask(kl);
                         if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
-                        const uint32_t sz0 = stage_size<L::kKCT>(stage, cl);
-                        uni = sz0 == stage_size<L::kKCT>(stage, cl + 31);
+                        const uint32_t sz0 = L::kEarlyB ? __ldg(gsz + cl) : stage_size<L::kKCT>(stage, cl);
+                        uni = sz0 == (L::kEarlyB ? __ldg(gsz + cl + 31) : stage_size<L::kKCT>(stage, cl + 31));
                         if (uni) {
                             if (sz0 != last_sz) {
                                 last_sz = sz0;
@@ -887,7 +915,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                             }
                             m = survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                         } else {
-                            m = survivors_mixed<KIND, L::kKCT>(d, pc, maxham, si, stage, cl);
+                            m = L::kEarlyB ? survivors_mixed_g<KIND>(d, pc, maxham, si, gsz, cl)
+                                           : survivors_mixed<KIND, L::kKCT>(d, pc, maxham, si, stage, cl);
                         }
                         m = bypass ? rm : (m & rm);
                     }
@@ -904,7 +933,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
                     mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
                     if constexpr (L::kNoExt) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
-                    else mbar_arrive_u32(bempty_u32 + 8 * st_idx);
+                    else if constexpr (!L::kEarlyB) mbar_arrive_u32(bempty_u32 + 8 * st_idx);
                 }
                 if (++st_idx == NS) {
                     st_idx = 0;
