@@ -1642,9 +1642,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     });
     const size_t free_b = free_at_first[device & 15];
     const uint64_t big = free_b >= (size_t(64) << 30) ? 1 : 0;
-    const uint64_t surv_cap =
+    uint64_t surv_cap =
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
-    const uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
+    uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
     uint2* d_surv = A.alloc<uint2>(surv_cap);
     uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
@@ -1671,13 +1671,16 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                                   : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
-    SB.ka = A.alloc<unsigned long long>(res_cap);
-    SB.va = A.alloc<uint32_t>(res_cap);
-    SB.kb = A.alloc<unsigned long long>(res_cap);
-    SB.vb = A.alloc<uint32_t>(res_cap);
-    const uint32_t max_tiles = static_cast<uint32_t>((res_cap + dev::kSortTile - 1) / dev::kSortTile);
-    SB.hist = A.alloc<uint32_t>(256ull * max_tiles);
-    SB.sums = A.alloc<uint32_t>((256ull * max_tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+    auto alloc_results = [&]() {
+        SB.ka = A.alloc<unsigned long long>(res_cap);
+        SB.va = A.alloc<uint32_t>(res_cap);
+        SB.kb = A.alloc<unsigned long long>(res_cap);
+        SB.vb = A.alloc<uint32_t>(res_cap);
+        const uint32_t max_tiles = static_cast<uint32_t>((res_cap + dev::kSortTile - 1) / dev::kSortTile);
+        SB.hist = A.alloc<uint32_t>(256ull * max_tiles);
+        SB.sums = A.alloc<uint32_t>((256ull * max_tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+    };
+    alloc_results();
     CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4, s));
     CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
     dev::Control h_ctl{};
@@ -1826,10 +1829,11 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     };
 
     uint64_t total_items = tl.item_base.back();
-    auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb, bool keep_survivors = false) {
+    auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb, bool keep_survivors = false,
+                             bool zero_counts = true) {
         if (!keep_survivors) CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
         CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
-        if (d_item_counts && ie > ib)
+        if (d_item_counts && ie > ib && zero_counts)
             CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (ie - ib) * tl.tile_rows * 4, s));
         if (ie <= ib) return;
         FP.item_begin = ib;
@@ -2043,30 +2047,64 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     free_delta8(ingest_d8, s);
 
     if (!done) {
-        // batches of work items sized so the survivors fit the buffer
+        // Survivor batches.  Grow the survivor / result buffers toward the first
+        // pass's survivor count while HBM allows (8 + 24 bytes per entry), then
+        // launch the filter over every remaining item with a soft survivor cap:
+        // its producers stop claiming items once the cap is passed, so each
+        // launch processes a prefix of the items, fills the buffer to about
+        // the cap and never overflows it (only if the last claims overshoot
+        // the margin is the launch rolled back and retried with a lower cap).
+        {
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            uint64_t want = surv_cap;
+            while (want < h_ctl.survivors && want < (uint64_t(1) << 30)) want <<= 1;
+            const uint64_t limit = static_cast<uint64_t>(0.35 * static_cast<double>(fr)) / 32;
+            while (want > surv_cap && want > limit) want >>= 1;
+            if (want > surv_cap && env_u64("SSJB_SURVIVOR_CAP", 0) == 0 && env_u64("SSJB_RESULT_CAP", 0) == 0) {
+                surv_cap = want;
+                res_cap = std::max(res_cap, surv_cap);
+                d_surv = A.alloc<uint2>(surv_cap);
+                alloc_results();
+                FP.surv = d_surv;
+                FP.surv_cap = surv_cap;
+                TP.surv = d_surv;
+                TP.surv_cap = surv_cap;
+                VP.surv = d_surv;
+                VP.res_keys = SB.ka;
+                VP.res_ov = SB.va;
+                VP.res_cap = res_cap;
+            }
+        }
+        uint64_t soft = std::max<uint64_t>(surv_cap / 2, 1);
+        uint64_t span = total_items;  // items per launch (halved only if the soft cap cannot help)
         uint64_t ib = 0;
-        uint64_t batch = std::max<uint64_t>(1, total_items * surv_cap / std::max<uint64_t>(h_ctl.survivors, 1) * 7 / 10);
+        if (d_item_counts && total_items)
+            CK(cudaMemsetAsync(d_item_counts, 0, total_items * tl.tile_rows * 4, s));
         while (ib < total_items) {
-            const uint64_t ie = std::min(total_items, ib + std::max<uint64_t>(batch, 1));
-            // rows touched by this batch (for rollback on overflow)
             const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
                                                       tl.item_base.begin() - 1);
-            const uint32_t te = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ie - 1) -
-                                                      tl.item_base.begin() - 1);
-            const uint32_t rb = tb * tl.tile_rows, re = std::min<uint32_t>(rows, (te + 1) * tl.tile_rows);
-            CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+            const uint32_t rb = tb * tl.tile_rows;  // rows this launch may touch: [rb, rows)
+            CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (rows - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+            FP.surv_soft = soft;
+            TP.surv_soft = soft;
             cudaEvent_t a = T.mark();
-            launch_filter(ib, ie, tb);
+            const uint64_t ie = std::min(total_items, ib + span);
+            launch_filter(ib, ie, tb, false, false);
             cudaEvent_t b = T.mark();
             CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             ms_filter += Timer::ms(a, b);
             const uint64_t S = h_ctl.survivors;
+            const uint64_t processed = std::min<uint64_t>(h_ctl.work_next, ie - ib);
             if (S > surv_cap) {
-                // overflow: roll the row counts back and retry a smaller batch
-                CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (re - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
-                batch = std::max<uint64_t>(1, (ie - ib) * surv_cap / S * 7 / 10);
-                if (batch >= ie - ib) batch = (ie - ib) / 2;
+                // the last claims overshot the margin: roll back this launch's
+                // row and item counts, retry with a lower cap
+                CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (rows - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
+                if (d_item_counts)
+                    CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (total_items - ib) * tl.tile_rows * 4, s));
+                if (soft > 1) soft = std::max<uint64_t>(soft / 4, 1);
+                else span = std::max<uint64_t>(1, std::min(span, processed) / 2);  // kernels without the soft cap
                 continue;
             }
             ++st.batches;
@@ -2084,12 +2122,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 ms_verify += Timer::ms(c0, c1);
                 res_count = h_ctl.results;
             }
-            // grow the next batch towards the capacity at the observed survivor rate
-            const uint64_t done_items = ie - ib;
-            ib = ie;
-            batch = S ? std::max<uint64_t>(1, static_cast<uint64_t>(double(done_items) * 0.7 * double(surv_cap) / double(S)))
-                      : total_items;
+            ib += processed;
         }
+        FP.surv_soft = 0;
+        TP.surv_soft = 0;
         cudaEvent_t r0 = T.mark();
         launch_counters();
         cudaEvent_t r1 = T.mark();

@@ -57,6 +57,7 @@ struct TcParams {
     uint32_t tiles_per_item;   // slots per item (>= ceil(kColChunk / NT))
     Control* ctl;
     unsigned long long surv_cap;
+    unsigned long long surv_soft;  // see claim_item (kernels.cuh)
     unsigned long long item_begin, item_end;
     uint32_t tile_begin, ntiles;
     uint32_t row_begin, row_end;
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             uint32_t iseq = 0, tseq = 0;
             // the next work item is claimed and looked up while the current one's
             // column tiles are still streaming (hides the atomic + table latency)
-            unsigned long long nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+            unsigned long long nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
             uint32_t nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
             for (;;) {
                 const int slot = iseq & 1;
@@ -598,12 +599,12 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     mbar_expect_tx(&b_full[st], L::kB);
                     tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
                     if (t == 0) {
-                        nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                        nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
                         nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
                     }
                 }
                 if (info.ntiles == 0) {
-                    nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                    nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
                     nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
                 }
                 ++iseq;

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             uint32_t iseq = 0, tseq = 0;
-            unsigned long long nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+            unsigned long long nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
             uint32_t nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
             for (;;) {
                 const int slot = iseq & 1;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                 tma_load_1d(sA + aslot * 2 * L::kA, P.opA + static_cast<uint64_t>(row0) * L::kRow, 2 * L::kA,
                             &a_full[aslot]);
                 mbar_arrive(&item_full[slot]);
-                nxt = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+                nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
                 nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;

@@ -33,6 +33,21 @@ struct Control {
     unsigned long long pad[6];
 };
 
+// Work-item claim of the persistent filters.  With a soft survivor cap the
+// producer stops claiming once the batch's survivors pass it, so a launch
+// always finishes with a prefix [item_begin, item_begin + work_next) of its
+// items processed (every claimed item is processed) and the survivor buffer
+// fills to about the cap instead of overflowing; the host resumes from there.
+__device__ __forceinline__ unsigned long long claim_item(Control* ctl, unsigned long long item_begin,
+                                                         unsigned long long item_end, unsigned long long soft) {
+    if (soft) {
+        unsigned long long cur;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(&ctl->survivors));
+        if (cur > soft) return item_end;
+    }
+    return item_begin + atomicAdd(&ctl->work_next, 1ull);
+}
+
 // ------------------------------------------------------------------ hashing
 // reference src/bitmap.hpp:30-36
 __device__ __forceinline__ uint32_t hash_token(uint32_t t, uint32_t width, int hash_mult, bool pow2) {
@@ -277,6 +292,7 @@ struct FilterParams {
     uint32_t* item_counts;       // survivors per (item, row-in-tile) for the rescan, or null
     Control* ctl;
     unsigned long long surv_cap;
+    unsigned long long surv_soft;  // stop claiming work items once this many survivors exist (0: never)
     unsigned long long item_begin, item_end;
     uint32_t tile_begin;         // tile index of item_begin's tile (search lower bound)
     uint32_t ntiles;
@@ -417,7 +433,7 @@ __global__ void __launch_bounds__(kRowTile) filter_kernel(FilterParams P) {
 
     for (;;) {
         if (tid == 0) {
-            unsigned long long it = P.item_begin + atomicAdd(&P.ctl->work_next, 1ull);
+            unsigned long long it = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
             uint32_t t = 0;
             if (it < P.item_end) {
                 uint32_t lo = P.tile_begin, hi = P.ntiles;  // largest t with item_base[t] <= it
