@@ -1777,6 +1777,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 
     std::vector<PairVec> runs;
     uint64_t res_count = 0;
+    uint64_t resume_item = 0;  // first work item the batch phase still has to filter
+    uint64_t fast_prefix = 0;  // items the first (soft-capped) pass filtered
     int idbits = 1;
     while ((uint64_t(1) << idbits) < n + 1) ++idbits;
     SB.count = &d_ctl->results;
@@ -1962,10 +1964,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                     launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
                 }
             }
-            if (!stream_filter) launch_filter(0, total_items, 0);  // one persistent launch after ingest
+            if (!stream_filter) {
+                FP.surv_soft = TP.surv_soft = std::max<uint64_t>(surv_cap / 2, 1);
+                launch_filter(0, total_items, 0);  // one persistent launch after ingest
+            }
         } else {
+            // soft survivor cap: a join whose survivors would overflow the buffer
+            // stops after an item prefix (kept, then continued in batches)
+            FP.surv_soft = TP.surv_soft = std::max<uint64_t>(surv_cap / 2, 1);
             launch_filter(0, total_items, 0);
         }
+        FP.surv_soft = TP.surv_soft = 0;
         cudaEvent_t b = T.mark();
         launch_verify();
         cudaEvent_t c1 = T.mark();
@@ -1987,7 +1996,25 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                          std::chrono::duration<double, std::milli>(t_launch - t_start).count(),
                          std::chrono::duration<double, std::milli>(t_enq - t_launch).count());
         h_ctl = hp->ctl;
-        if (h_ctl.survivors <= surv_cap) {
+        const bool multi_launch = streamed && env_u64("SSJB_STREAM", 1) >= 2;
+        const uint64_t fast_items = multi_launch ? total_items : std::min<uint64_t>(h_ctl.work_next, total_items);
+        const bool partial = fast_items < total_items;
+        fast_prefix = fast_items;
+        const bool switch_l2 = l2_auto && use_tc && !l2gemm && !fp4;
+        if (h_ctl.survivors <= surv_cap && partial && !switch_l2) {
+            // soft-capped: the item prefix [0, fast_items) is filtered and its
+            // survivors verified; keep its results and row/item counts, drop the
+            // counters computed from partial rows (recomputed at the end), and
+            // continue with the remaining items in batches
+            ms_filter = Timer::ms(a, b);
+            ms_verify = Timer::ms(b, c1);
+            st.batches = 1;
+            st.survivors = h_ctl.survivors;
+            res_count = h_ctl.results;
+            resume_item = fast_items;
+            CK(cudaMemsetAsync(&d_ctl->tested, 0, 4 * sizeof(unsigned long long), s));
+            CK(cudaMemsetAsync(&d_ctl->sat_rows, 0, sizeof(unsigned long long), s));
+        } else if (h_ctl.survivors <= surv_cap && !partial) {
             done = true;
             ms_filter = Timer::ms(a, b);
             ms_verify = Timer::ms(b, c1);
@@ -2003,7 +2030,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 flush_results(h_ctl.results);
             }
         } else {
-            // survivor buffer overflow: discard and redo in batches
+            // survivor buffer overflow, or a soft-capped level-1 pass that switches
+            // to the level-2 GEMM: discard and redo in batches
             CK(cudaMemsetAsync(d_rowcnt, 0, (rows + 1) * 4ull, s));
             CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));
             if (l2_auto && use_tc && !l2gemm && !fp4) {
@@ -2057,11 +2085,18 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         {
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
+            // survivors of the whole join, extrapolated from the first pass's prefix
+            const double est = static_cast<double>(h_ctl.survivors) * static_cast<double>(total_items) /
+                               static_cast<double>(std::max<uint64_t>(fast_prefix ? fast_prefix : total_items, 1));
             uint64_t want = surv_cap;
-            while (want < h_ctl.survivors && want < (uint64_t(1) << 30)) want <<= 1;
+            while (static_cast<double>(want) < est && want < (uint64_t(1) << 30)) want <<= 1;
             const uint64_t limit = static_cast<uint64_t>(0.35 * static_cast<double>(fr)) / 32;
             while (want > surv_cap && want > limit) want >>= 1;
             if (want > surv_cap && env_u64("SSJB_SURVIVOR_CAP", 0) == 0 && env_u64("SSJB_RESULT_CAP", 0) == 0) {
+                if (res_count) {  // the kept prefix's results leave the old buffer first
+                    flush_results(res_count);
+                    res_count = 0;
+                }
                 surv_cap = want;
                 res_cap = std::max(res_cap, surv_cap);
                 d_surv = A.alloc<uint2>(surv_cap);
@@ -2078,9 +2113,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
         uint64_t soft = std::max<uint64_t>(surv_cap / 2, 1);
         uint64_t span = total_items;  // items per launch (halved only if the soft cap cannot help)
-        uint64_t ib = 0;
-        if (d_item_counts && total_items)
-            CK(cudaMemsetAsync(d_item_counts, 0, total_items * tl.tile_rows * 4, s));
+        uint64_t ib = resume_item;
+        if (d_item_counts && total_items > ib)
+            CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (total_items - ib) * tl.tile_rows * 4, s));
         while (ib < total_items) {
             const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
                                                       tl.item_base.begin() - 1);
