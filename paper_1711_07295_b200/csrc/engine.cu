@@ -825,13 +825,13 @@ using BuildFn2 = void (*)(dev::BuildParams2);
 
 // Set/Xor sketches (and the level-2 Xor sketch in the same token pass) with
 // several lanes per record; null when the shape has no instantiation.
-BuildFn2 build_sub_fn(int words, int words2) {
+BuildFn2 build_sub_fn(int words, int words2, bool x) {
 #define SSJB_SUB(W)                                      \
     case W:                                              \
         switch (words2) {                                \
-            case 0: return dev::build_sketches_sub<W, 0>; \
-            case 4: return dev::build_sketches_sub<W, 4>; \
-            case 8: return dev::build_sketches_sub<W, 8>; \
+            case 0: return x ? dev::build_sketches_sub<W, 0, true> : dev::build_sketches_sub<W, 0, false>; \
+            case 4: return x ? dev::build_sketches_sub<W, 4, true> : dev::build_sketches_sub<W, 4, false>; \
+            case 8: return x ? dev::build_sketches_sub<W, 8, true> : dev::build_sketches_sub<W, 8, false>; \
         }                                                \
         break;
     switch (words) {
@@ -854,7 +854,7 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
                       int width2, int hash, cudaStream_t s, uint64_t& launches, uint32_t row0 = 0,
                       uint32_t row1 = UINT32_MAX) {
     if (method != Method::Set && method != Method::Xor) return false;
-    BuildFn2 fn = build_sub_fn(width / 64, bits2 ? width2 / 64 : 0);
+    BuildFn2 fn = build_sub_fn(width / 64, bits2 ? width2 / 64 : 0, method == Method::Xor);
     if (!fn) return false;
     row1 = std::min<uint32_t>(row1, static_cast<uint32_t>(rep.n));
     if (row1 <= row0) return true;

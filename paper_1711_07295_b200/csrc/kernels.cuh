@@ -198,7 +198,7 @@ struct BuildParams2 {
     uint64_t total_tokens; // tokens in the array (bound of the 16-byte loads)
 };
 
-template <int W, int W2>
+template <int W, int W2, bool XOR>
 __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
     const int lpr = 1 << P.lpr_log2;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -210,16 +210,20 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
     for (int w = 0; w < W; ++w) row[w] = 0;
 #pragma unroll
     for (int w = 0; w < (W2 > 0 ? W2 : 1); ++w) row2[w] = 0;
+    // widths are compile-time (64 W, 64 W2): the modulo of hash_token
+    // (reference src/bitmap.hpp:30-36) folds to a mask or a multiply-shift
     auto fold = [&](uint32_t t) {
-            const uint32_t h = hash_token(t, P.width, P.hash_mult, P.pow2);
+            const uint32_t hm = P.hash_mult ? static_cast<uint32_t>((static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull) >> 33)
+                                            : t;
+            const uint32_t h = hm % (64u * W);
             const uint64_t bit = 1ull << (h & 63);
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                const uint64_t m = (h >> 6) == uint32_t(w) ? bit : 0ull;
-                row[w] = P.method == 0 ? (row[w] | m) : (row[w] ^ m);
+                const uint64_t m = (W == 1 || (h >> 6) == uint32_t(w)) ? bit : 0ull;
+                row[w] = XOR ? (row[w] ^ m) : (row[w] | m);
             }
             if constexpr (W2 > 0) {
-                const uint32_t h2 = hash_token(t, P.width2, P.hash_mult, P.pow2_2);
+                const uint32_t h2 = hm % (64u * W2);
                 const uint64_t bit2 = 1ull << (h2 & 63);
 #pragma unroll
                 for (int w = 0; w < W2; ++w) row2[w] ^= (h2 >> 6) == uint32_t(w) ? bit2 : 0ull;
@@ -230,27 +234,40 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
         // lpr, four 128-bit loads in flight per lane before folding (a scalar
         // strided loop is bound by one load round trip per token)
         const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
-        for (uint64_t c = (b & ~uint64_t(3)) + 4ull * sub; c < e; c += 16ull * lpr) {
+        // 32-bit offsets relative to the record's first aligned chunk
+        const uint64_t a0 = b & ~uint64_t(3);
+        const uint32_t lo = static_cast<uint32_t>(b - a0), hi = static_cast<uint32_t>(e - a0);
+        const uint64_t rem = P.total_tokens - a0;
+        const uint32_t lim = rem > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(rem);
+        const uint32_t* base = P.tokens + a0;
+        for (uint32_t c = 4u * sub; c < hi; c += 16u * lpr) {
             uint4 v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint64_t cc = c + 4ull * lpr * u;
-                if (cc + 4 <= P.total_tokens) {
-                    v[u] = cc < e ? __ldg(reinterpret_cast<const uint4*>(P.tokens + cc)) : make_uint4(0, 0, 0, 0);
+                const uint32_t cc = c + 4u * lpr * u;
+                if (cc + 4 <= lim) {
+                    v[u] = cc < hi ? __ldg(reinterpret_cast<const uint4*>(base + cc)) : make_uint4(0, 0, 0, 0);
                 } else {
-                    v[u].x = cc < e ? P.tokens[cc] : 0u;
-                    v[u].y = cc + 1 < e ? P.tokens[cc + 1] : 0u;
-                    v[u].z = cc + 2 < e ? P.tokens[cc + 2] : 0u;
+                    v[u].x = cc < hi ? base[cc] : 0u;
+                    v[u].y = cc + 1 < hi ? base[cc + 1] : 0u;
+                    v[u].z = cc + 2 < hi ? base[cc + 2] : 0u;
                     v[u].w = 0u;
                 }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const uint64_t cc = c + 4ull * lpr * u;
-                const uint32_t t4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                const uint32_t cc = c + 4u * lpr * u;
+                if (cc >= lo && cc + 4 <= hi) {  // interior chunk: no per-token bounds
+                    fold(v[u].x);
+                    fold(v[u].y);
+                    fold(v[u].z);
+                    fold(v[u].w);
+                } else if (cc < hi) {
+                    const uint32_t t4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (cc + q >= b && cc + q < e) fold(t4[q]);
+                    for (int q = 0; q < 4; ++q)
+                        if (cc + q >= lo && cc + q < hi) fold(t4[q]);
+                }
             }
         }
     }
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, row[w], o);
-            row[w] = P.method == 0 ? (row[w] | v) : (row[w] ^ v);
+            row[w] = XOR ? (row[w] ^ v) : (row[w] | v);
         }
         if constexpr (W2 > 0) {
 #pragma unroll
