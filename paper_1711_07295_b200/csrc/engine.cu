@@ -3,6 +3,7 @@
 // identical to the reference's SSJ_ALGO_PAR_BITMAP (src/parallel_join.cpp:40-140)
 // or SSJ_ALGO_NAIVE (src/join.cpp:91-126).
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <atomic>
@@ -916,6 +917,13 @@ __global__ void pack_pairs(const unsigned long long* keys, const uint32_t* ov, P
 // fraction of the link rate).
 void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     constexpr size_t kChunk = size_t(64) << 20;
+    if (bytes >= (size_t(16) << 20)) {
+        // a fresh multi-GB result vector is first touched here: back it with
+        // transparent huge pages so the copy-out does not take a page fault per 4 KB
+        const uintptr_t a = (reinterpret_cast<uintptr_t>(dst) + (size_t(2) << 20) - 1) & ~((uintptr_t(2) << 20) - 1);
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~((uintptr_t(2) << 20) - 1);
+        if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    }
     if (bytes <= kChunk) {
         if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1772,7 +1780,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     if (W2 && !naive) {  // level-2 re-test of level-1 survivors before the merge
         VP.bits2 = d_bits2;
         VP.maxham = d_maxham;
-        VP.w2 = W2;
+        // (the level-2 GEMM emits level-2 survivors: no second test, which would
+        // cost two random 32-byte sketch loads per survivor)
+        VP.w2 = l2gemm ? 0 : W2;
     }
 
     std::vector<PairVec> runs;
@@ -2063,6 +2073,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 set_smem_once(reinterpret_cast<const void*>(tck.fn), tck.smem);
                 TP.opA = a1;
                 TP.opB = b1;
+                VP.w2 = 0;  // its survivors pass level 2 already
                 TP.bias = level1_acc_bias(W, 1);  // the variant-1 operands' biases
                 TP.bias2 = level2_acc_bias(W2, 1);
                 st.filter_kernel = 2;
