@@ -1784,6 +1784,18 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         // cost two random 32-byte sketch loads per survivor)
         VP.w2 = l2gemm ? 0 : W2;
     }
+    // level 3 (512-bit Xor) for the dense regime's large records, built on demand
+    auto enable_level3 = [&]() {
+        if (VP.bits3 || W2 != 4 || naive || env_u64("SSJB_L3", 1) == 0) return;
+        uint64_t* b3 = A.alloc<uint64_t>((n + kPadRows + 8) * 8);
+        launch_build_sub(*rep, b3, nullptr, Method::Xor, 512, 0, plan.bitmap.hash, s, st.launches);
+        VP.bits3 = b3;
+        VP.maxham = d_maxham;
+        VP.l3_min_sum = static_cast<uint32_t>(env_u64("SSJB_L3_MIN", 128));
+    };
+    // (tests: SSJB_L3_FORCE=1 enables level 3 from the first pass of any
+    // non-streamed join with level-2 sketches)
+    if (env_u64("SSJB_L3_FORCE", 0) != 0 && !streamed) enable_level3();
 
     std::vector<PairVec> runs;
     uint64_t res_count = 0;
@@ -2122,6 +2134,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 VP.res_cap = res_cap;
             }
         }
+        if (l2gemm) enable_level3();  // dense join: survivors in the billions, large records
         uint64_t soft = std::max<uint64_t>(surv_cap / 2, 1);
         uint64_t span = total_items;  // items per launch (halved only if the soft cap cannot help)
         uint64_t ib = resume_item;

@@ -868,6 +868,8 @@ struct VerifyParams {
     const int32_t* maxham;    // maxham[|r|+|s|] (with bits2)
     int w2;
     int warp_mode;            // 1: warp per pair when the survivors are few
+    const uint64_t* bits3;    // level-3 512-bit Xor sketches (dense joins), or null
+    uint32_t l3_min_sum;      // level 3 is tested when |r| + |s| >= this
 };
 
 // One thread per surviving pair: branch-free sorted merge with the
@@ -985,6 +987,22 @@ __global__ void verify_pairs(VerifyParams P) {
                 }
                 l2_ok = h <= P.maxham[na + nb];
                 if (!l2_ok) ia = na;  // skip the merge
+            }
+            if (l2_ok && P.bits3 && na + nb >= P.l3_min_sum) {
+                // level 3: the wider sketch still discriminates where the 256-bit
+                // one has saturated (large records); same sound bound
+                const ulonglong2* sj = reinterpret_cast<const ulonglong2*>(P.bits3 + static_cast<uint64_t>(j) * 8);
+                const ulonglong2* si = reinterpret_cast<const ulonglong2*>(P.bits3 + static_cast<uint64_t>(i) * 8);
+                int h = 0;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const ulonglong2 x = __ldg(sj + w), y = __ldg(si + w);
+                    h += __popcll(x.x ^ y.x) + __popcll(x.y ^ y.y);
+                }
+                if (h > P.maxham[na + nb]) {
+                    l2_ok = false;
+                    ia = na;  // skip the merge
+                }
             }
             merged = l2_ok;
             if (l2_ok && na <= kRegVerify && nb <= kRegVerify && na >= static_cast<uint32_t>(need) &&

@@ -214,3 +214,16 @@ def _c2(lib):
     if "c" not in _C2:
         _C2["c"] = D.c2(lib)
     return _C2["c"]
+
+
+@pytest.mark.parametrize("flavour", ["tc-l2gemm", "tc-i8"])
+def test_level3_verify_filter(lib, golden, colls, flavour, monkeypatch):
+    """Every fixture with the level-3 (512-bit Xor) re-test applied to every
+    survivor before the merge (dense joins enable it in their batch phase):
+    it may only drop pairs that cannot match."""
+    set_filter(monkeypatch, flavour)
+    monkeypatch.setenv("SSJB_L3_FORCE", "1")
+    monkeypatch.setenv("SSJB_L3_MIN", "0")
+    for e in golden["joins"]:
+        rep = S.join(colls(e["collection"]), options_of(lib, e))
+        assert_same(rep, e, flavour + "+l3")
