@@ -32,6 +32,9 @@
 namespace ssjb {
 namespace dev {
 
+#ifndef SSJB_SUSPEND_NS
+#define SSJB_SUSPEND_NS 8192u
+#endif
 constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
 constexpr int kTcLut = 1536;       // shared-memory copy of maxham[] (entries)
 constexpr int kKindI8 = 0;         // tcgen05 kind::i8, s32 accumulators
@@ -84,10 +87,11 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
 
 // Spin without a suspend hint (single-lane producer / MMA roles: wake-up
 // latency is on the critical path there).
-// try_wait suspend-time hint: a waiting warp is parked until the phase
+// try_wait suspend-time hint (8 us; a 1 ms hint stalled concurrent joins from
+// several host threads): a waiting warp is parked until the phase
 // completes (or this many ns pass) instead of re-issuing the probe, leaving
 // issue slots to the epilogue warps that share the SM sub-partitions
-constexpr uint32_t kSuspendNs = 1u << 20;
+constexpr uint32_t kSuspendNs = SSJB_SUSPEND_NS;
 
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
     asm volatile(
