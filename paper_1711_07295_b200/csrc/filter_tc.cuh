@@ -400,6 +400,55 @@ __device__ __forceinline__ uint32_t mask_col(int k) {
     return PERM ? static_cast<uint32_t>(2 * (k & 15) + (k >> 4)) : static_cast<uint32_t>(k);
 }
 
+// Both 32-column masks of a 64-column block in one emission (one prefix scan
+// instead of two): m0 covers columns base_col + [0, 32), m1 base_col + [32, 64).
+template <bool PERM>
+__device__ __forceinline__ void tc_emit64(uint32_t m0, uint32_t m1, uint32_t base_col, uint32_t row, uint2* q,
+                                          int& qlen, const TcParams& P, int lane) {
+    const int c = __popc(m0) + __popc(m1);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (total == 0) return;
+    const int excl = incl - c;
+    if (total > kTcQueue) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(total));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + excl;
+        while (m0) {
+            int k = __ffs(m0) - 1;
+            m0 &= m0 - 1;
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + mask_col<PERM>(k), row);
+            ++base;
+        }
+        while (m1) {
+            int k = __ffs(m1) - 1;
+            m1 &= m1 - 1;
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + 32 + mask_col<PERM>(k), row);
+            ++base;
+        }
+        return;
+    }
+    if (qlen + total > kTcQueue) tc_flush(q, qlen, P, lane);
+    int pos = qlen + excl;
+    while (m0) {
+        int k = __ffs(m0) - 1;
+        m0 &= m0 - 1;
+        q[pos++] = make_uint2(base_col + mask_col<PERM>(k), row);
+    }
+    while (m1) {
+        int k = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        q[pos++] = make_uint2(base_col + 32 + mask_col<PERM>(k), row);
+    }
+    qlen += total;
+    __syncwarp();
+}
+
 template <bool PERM = false>
 __device__ __forceinline__ void tc_emit(uint32_t m, uint32_t base_col, uint32_t row, uint2* q, int& qlen,
                                         const TcParams& P, int lane) {

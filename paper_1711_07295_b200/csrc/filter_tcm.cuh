@@ -63,8 +63,7 @@ __device__ __forceinline__ void tcm_block(TcmRow& R, uint32_t acc_col, const uin
             if (P.bias > 0) {  // non-negative accumulators: 3-instruction SWAR masks, permuted bits
                 if (!R.bypass) masks16_nonneg(d, R.cim1, m0, m1);
                 R.cnt += __popc(m0) + __popc(m1);
-                if (__any_sync(0xFFFFFFFFu, m0 != 0)) tc_emit<true>(m0, wbase, R.i, q, qlen, P, lane);
-                if (__any_sync(0xFFFFFFFFu, m1 != 0)) tc_emit<true>(m1, wbase + 32, R.i, q, qlen, P, lane);
+                tc_emit64<true>(m0, m1, wbase, R.i, q, qlen, P, lane);
                 return;
             }
             if (!R.bypass) masks16(d, c16, m0, m1);
