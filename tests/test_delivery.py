@@ -154,3 +154,19 @@ def test_golden_pairs_text(lib, golden, golden_arrays, tmp_path):
         if done >= 12:
             break
     assert done >= 5
+
+
+def test_delivery_with_empty_outputs(lib, tmp_path):
+    """No pairs at all (and an empty collection): no chunk is delivered, the
+    text file is empty, counters still match ssj_join's."""
+    for recs in ([[1, 2, 3], [4, 5, 6], [7, 8, 9, 10]], [], [[]] * 4):
+        coll = S.Collection.from_records(lib, recs)
+        opts = S.par_bitmap_options(lib, threshold=(9, 10), bits=64)
+        want = S.join(coll, opts)
+        assert len(want.pairs) == 0
+        rep, chunks = _stream(coll, opts, chunk_pairs=10)
+        assert chunks == [] and rep.counters == want.counters
+        assert S.join_count(coll, opts).counters == want.counters
+        path = str(tmp_path / "empty.txt")
+        S.join_write_pairs(coll, opts, path)
+        assert open(path).read() == ""
