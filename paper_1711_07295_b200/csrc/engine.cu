@@ -1551,7 +1551,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         if (!copy_streams[device & 15])
             CK(cudaStreamCreateWithFlags(&copy_streams[device & 15], cudaStreamNonBlocking));
         rep = upload_streamed(c, device, s, copy_streams[device & 15], tl.tile_rows,
-                              static_cast<int>(env_u64("SSJB_STREAM_CHUNKS", 4)), st.h2d_bytes, st.launches, ingest,
+                              static_cast<int>(env_u64("SSJB_STREAM_CHUNKS", 2)), st.h2d_bytes, st.launches, ingest,
                               ingest_t16, ingest_d8);
     } else if (!rep) {
         rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
