@@ -889,7 +889,6 @@ struct VerifyParams {
 // < required) only ever stops non-matching pairs, as in the reference's
 // verify (src/similarity.cpp:174-175).
 constexpr unsigned long long kWarpVerifyMax = 1ull << 15;
-constexpr int kRegVerify = 8;  // records up to this size are intersected in registers
 
 template <int W2>
 __device__ __forceinline__ void verify_warp_mode(const VerifyParams& P, unsigned long long count, int lane) {
@@ -1005,24 +1004,6 @@ __global__ void verify_pairs(VerifyParams P) {
                 }
             }
             merged = l2_ok;
-            if (l2_ok && na <= kRegVerify && nb <= kRegVerify && na >= static_cast<uint32_t>(need) &&
-                nb >= static_cast<uint32_t>(need)) {
-                // short records: all tokens in flight at once, all-pairs equality in
-                // registers (tokens are distinct within a record, so the count is
-                // the exact intersection) -- no chain of dependent merge loads
-                uint32_t a[kRegVerify], bt[kRegVerify];
-#pragma unroll
-                for (int k = 0; k < kRegVerify; ++k) {
-                    a[k] = k < static_cast<int>(na) ? __ldg(A + k) : 0u;
-                    bt[k] = k < static_cast<int>(nb) ? __ldg(B + k) : 0u;
-                }
-#pragma unroll
-                for (int x = 0; x < kRegVerify; ++x)
-#pragma unroll
-                    for (int y = 0; y < kRegVerify; ++y)
-                        o += (x < static_cast<int>(na)) & (y < static_cast<int>(nb)) & (a[x] == bt[y]);
-                ia = na;
-            }
             while (ia < na && ib < nb) {
                 const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
                 if (o + rest < need) break;
