@@ -943,7 +943,8 @@ void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         CK(cudaMemcpyAsync(stage[k & 1], static_cast<const uint8_t*>(src) + off, len, cudaMemcpyDeviceToHost, s));
         CK(cudaEventRecord(ev[k & 1], s));
     };
-    const unsigned nthreads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    static const unsigned max_threads = static_cast<unsigned>(env_u64("SSJB_D2H_THREADS", 32));  // host-memcpy bound: all cores
+    const unsigned nthreads = std::max(1u, std::min(max_threads, std::thread::hardware_concurrency()));
     issue(0);
     for (size_t k = 0; k < nchunks; ++k) {
         if (k + 1 < nchunks) issue(k + 1);
