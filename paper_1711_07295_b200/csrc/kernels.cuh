@@ -657,6 +657,15 @@ __global__ void find_saturated(const uint32_t* rowcnt, uint32_t nrows, uint32_t 
 
 constexpr int kRescanLut = 4096;  // maxham[] entries staged in shared memory
 
+__device__ __forceinline__ uint32_t warp_inclusive_sum(uint32_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
 // One warp per row whose survivor count reaches the capacity: locate the
 // capacity-th survivor in window order (the reference's saturation point,
 // src/parallel_join.cpp:83-94).  With per-item counts from the filter only the
@@ -682,30 +691,44 @@ __global__ void __launch_bounds__(256) rescan_saturated(RescanParams P) {
         }
         uint32_t start = j0, stop = i, seen = 0;
         if (P.item_counts) {
+            // the work item (then the filter tile) holding the capacity-th
+            // survivor: 32 items (tiles) per step, one per lane, located by a
+            // warp prefix sum and a ballot instead of a chain of dependent loads
             const uint32_t tile = r / P.tile_rows, t = r % P.tile_rows;
             const uint64_t ib = P.item_base[tile], ie = P.item_base[tile + 1];
-            for (uint64_t it = ib; it < ie; ++it) {
-                const uint32_t cc = P.item_counts[it * P.tile_rows + t];
-                if (seen + cc >= P.capacity) {
-                    const uint32_t c0 = P.tile_col_lo[tile] + static_cast<uint32_t>(it - ib) * kColChunk;
-                    start = max(j0, c0);
-                    stop = min(i, c0 + kColChunk);
-                    if (P.tile_counts) {  // narrow to the filter tile holding it
-                        for (uint32_t tt = 0; tt < P.tiles_per_item; ++tt) {
-                            uint32_t tc = 0;
-                            for (uint32_t pp = 0; pp < P.tile_parts; ++pp)
-                                tc += P.tile_counts[((it * P.tiles_per_item + tt) * 4 + pp) * P.tile_rows + t];
-                            if (seen + tc >= P.capacity) {
-                                start = max(j0, c0 + tt * P.tile_cols);
-                                stop = min(stop, c0 + (tt + 1) * P.tile_cols);
-                                break;
-                            }
-                            seen += tc;
-                        }
-                    }
-                    break;
+            for (uint64_t base = ib; base < ie; base += 32) {
+                const uint64_t it = base + lane;
+                const uint32_t cc = it < ie ? P.item_counts[it * P.tile_rows + t] : 0u;
+                const uint32_t inc = warp_inclusive_sum(cc, lane);
+                const uint32_t hit = __ballot_sync(0xFFFFFFFFu, seen + inc >= P.capacity);
+                if (!hit) {
+                    seen += __shfl_sync(0xFFFFFFFFu, inc, 31);
+                    continue;
                 }
-                seen += cc;
+                const int L = __ffs(hit) - 1;
+                seen += __shfl_sync(0xFFFFFFFFu, inc - cc, L);
+                const uint64_t itL = base + static_cast<uint64_t>(L);
+                const uint32_t c0 = P.tile_col_lo[tile] + static_cast<uint32_t>(itL - ib) * kColChunk;
+                start = max(j0, c0);
+                stop = min(i, c0 + kColChunk);
+                if (P.tile_counts) {  // narrow to the filter tile holding it (tiles_per_item <= 32)
+                    uint32_t tc = 0;
+                    if (static_cast<uint32_t>(lane) < P.tiles_per_item)
+                        for (uint32_t pp = 0; pp < P.tile_parts; ++pp)
+                            tc += P.tile_counts[((itL * P.tiles_per_item + lane) * 4 + pp) * P.tile_rows + t];
+                    const uint32_t inc2 = warp_inclusive_sum(tc, lane);
+                    // (slots past the item's last processed tile are not written, but
+                    // they only follow the crossing lane, so no prefix before it sees them)
+                    const uint32_t hit2 = __ballot_sync(
+                        0xFFFFFFFFu, static_cast<uint32_t>(lane) < P.tiles_per_item && seen + inc2 >= P.capacity);
+                    if (hit2) {
+                        const int L2 = __ffs(hit2) - 1;
+                        seen += __shfl_sync(0xFFFFFFFFu, inc2 - tc, L2);
+                        start = max(j0, c0 + static_cast<uint32_t>(L2) * P.tile_cols);
+                        stop = min(stop, c0 + static_cast<uint32_t>(L2 + 1) * P.tile_cols);
+                    }
+                }
+                break;
             }
         }
         uint64_t me[kMaxInlineWords];
