@@ -1887,7 +1887,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         // survivor count read on the device: no host round trip between K2 and K3
         VP.count_ptr = &d_ctl->survivors;
         VP.count_cap = surv_cap;
-        static const unsigned vmul = static_cast<unsigned>(env_u64("SSJB_VERIFY_GRID", 8));
+        static const unsigned vmul = static_cast<unsigned>(env_u64("SSJB_VERIFY_GRID", 32));  // latency-bound: more warps
         const unsigned vgrid = static_cast<unsigned>(sms) * vmul;
         if (VP.w2 == 4) dev::verify_pairs<4><<<vgrid, 256, 0, s>>>(VP);
         else if (VP.w2 == 8) dev::verify_pairs<8><<<vgrid, 256, 0, s>>>(VP);
