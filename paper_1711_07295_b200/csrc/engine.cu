@@ -1447,6 +1447,70 @@ double engine_time_build(const Collection& c, Method method, int width, int hash
     return reps > 0 ? total / reps : 0.0;
 }
 
+namespace {
+// Survivor and result buffers of a host thread's joins on one device, kept
+// across joins (grown, never shrunk): per-join stream-ordered allocations of
+// these multi-GB buffers from several threads at once make the memory pool
+// map fresh pages, stalling concurrent joins.
+struct JoinWorkspace {
+    int device = -1;
+    uint2* surv = nullptr;
+    uint64_t surv_cap = 0;
+    unsigned long long *ka = nullptr, *kb = nullptr;
+    uint32_t *va = nullptr, *vb = nullptr, *hist = nullptr, *sums = nullptr;
+    uint64_t res_cap = 0;
+    ~JoinWorkspace() { release(); }
+    void release() {
+        if (device < 0) return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaFree(surv);
+        cudaFree(ka);
+        cudaFree(kb);
+        cudaFree(va);
+        cudaFree(vb);
+        cudaFree(hist);
+        cudaFree(sums);
+        cudaSetDevice(cur);
+        surv = nullptr;
+        ka = kb = nullptr;
+        va = vb = hist = sums = nullptr;
+        surv_cap = res_cap = 0;
+    }
+    // (buffers may still be in use by the stream: callers synchronise it first)
+    void ensure(int dev, uint64_t scap, uint64_t rcap) {
+        device = dev;
+        if (scap > surv_cap) {
+            cudaFree(surv);
+            CK(cudaMalloc(&surv, scap * sizeof(uint2)));
+            surv_cap = scap;
+        }
+        if (rcap > res_cap) {
+            cudaFree(ka);
+            cudaFree(kb);
+            cudaFree(va);
+            cudaFree(vb);
+            cudaFree(hist);
+            cudaFree(sums);
+            const uint64_t tiles = (rcap + dev::kSortTile - 1) / dev::kSortTile;
+            CK(cudaMalloc(&ka, rcap * 8));
+            CK(cudaMalloc(&kb, rcap * 8));
+            CK(cudaMalloc(&va, rcap * 4));
+            CK(cudaMalloc(&vb, rcap * 4));
+            CK(cudaMalloc(&hist, 256ull * tiles * 4));
+            CK(cudaMalloc(&sums, ((256ull * tiles + dev::kScanBlock - 1) / dev::kScanBlock + 1) * 4));
+            res_cap = rcap;
+        }
+    }
+};
+
+JoinWorkspace& join_workspace(int device) {
+    static thread_local JoinWorkspace ws[16];
+    return ws[device & 15];
+}
+}  // namespace
+
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
     using Clock = std::chrono::steady_clock;
     set_device(device);
@@ -1654,7 +1718,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint64_t surv_cap =
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
     uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
-    uint2* d_surv = A.alloc<uint2>(surv_cap);
+    JoinWorkspace& WS = join_workspace(device);
+    const bool use_ws = env_u64("SSJB_WORKSPACE", 1) != 0;
+    if (use_ws) {
+        CK(cudaStreamSynchronize(s));  // the previous join on this stream is done with them
+        WS.ensure(device, surv_cap, res_cap);
+    }
+    uint2* d_surv = use_ws ? WS.surv : A.alloc<uint2>(surv_cap);
     uint32_t* d_rowcnt = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_rowsnap = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
@@ -1681,6 +1751,16 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     dev::Control* d_ctl = A.alloc<dev::Control>(1);
     SortBufs SB{};
     auto alloc_results = [&]() {
+        if (use_ws) {
+            WS.ensure(device, surv_cap, res_cap);
+            SB.ka = WS.ka;
+            SB.kb = WS.kb;
+            SB.va = WS.va;
+            SB.vb = WS.vb;
+            SB.hist = WS.hist;
+            SB.sums = WS.sums;
+            return;
+        }
         SB.ka = A.alloc<unsigned long long>(res_cap);
         SB.va = A.alloc<uint32_t>(res_cap);
         SB.kb = A.alloc<unsigned long long>(res_cap);
@@ -2123,7 +2203,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 }
                 surv_cap = want;
                 res_cap = std::max(res_cap, surv_cap);
-                d_surv = A.alloc<uint2>(surv_cap);
+                if (use_ws) CK(cudaStreamSynchronize(s));  // (regrown in place)
+                d_surv = use_ws ? (WS.ensure(device, surv_cap, res_cap), WS.surv) : A.alloc<uint2>(surv_cap);
                 alloc_results();
                 FP.surv = d_surv;
                 FP.surv_cap = surv_cap;
