@@ -1448,7 +1448,7 @@ double engine_time_build(const Collection& c, Method method, int width, int hash
 }
 
 namespace {
-// Survivor and result buffers of a host thread's joins on one device, kept
+// Survivor and result buffers of one join in flight on one device, kept
 // across joins (grown, never shrunk): per-join stream-ordered allocations of
 // these multi-GB buffers from several threads at once make the memory pool
 // map fresh pages, stalling concurrent joins.
@@ -1505,10 +1505,40 @@ struct JoinWorkspace {
     }
 };
 
-JoinWorkspace& join_workspace(int device) {
-    static thread_local JoinWorkspace ws[16];
-    return ws[device & 15];
+// Workspaces live in a per-device pool: a join leases one (a concurrent join
+// gets another), so short-lived host threads -- one per device in multi-GPU
+// joins -- reuse buffers across calls instead of re-allocating them.
+struct WorkspacePool {
+    std::mutex mu;
+    std::vector<std::unique_ptr<JoinWorkspace>> idle[16];
+};
+WorkspacePool& workspace_pool() {
+    static WorkspacePool* p = new WorkspacePool();  // leaked: outlives thread/static teardown
+    return *p;
 }
+
+struct WorkspaceLease {
+    int device;
+    cudaStream_t stream;
+    std::unique_ptr<JoinWorkspace> ws;
+    WorkspaceLease(int dev, cudaStream_t s) : device(dev), stream(s) {
+        WorkspacePool& P = workspace_pool();
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto& v = P.idle[dev & 15];
+        if (!v.empty()) {
+            ws = std::move(v.back());
+            v.pop_back();
+        } else {
+            ws = std::make_unique<JoinWorkspace>();
+        }
+    }
+    ~WorkspaceLease() {
+        cudaStreamSynchronize(stream);  // nothing queued may still use the buffers
+        WorkspacePool& P = workspace_pool();
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.idle[device & 15].push_back(std::move(ws));
+    }
+};
 }  // namespace
 
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
@@ -1718,7 +1748,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint64_t surv_cap =
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
     uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
-    JoinWorkspace& WS = join_workspace(device);
+    WorkspaceLease lease(device, s);
+    JoinWorkspace& WS = *lease.ws;
     const bool use_ws = env_u64("SSJB_WORKSPACE", 1) != 0;
     if (use_ws) {
         CK(cudaStreamSynchronize(s));  // the previous join on this stream is done with them
