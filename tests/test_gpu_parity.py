@@ -227,3 +227,21 @@ def test_level3_verify_filter(lib, golden, colls, flavour, monkeypatch):
     for e in golden["joins"]:
         rep = S.join(colls(e["collection"]), options_of(lib, e))
         assert_same(rep, e, flavour + "+l3")
+
+
+def test_concurrent_joins_from_threads(lib, golden, colls):
+    """Joins from four host threads at once (each on its own stream, sharing
+    collections, pinned replicas and the workspace pool) give every fixture's
+    exact result -- bench.py runs the sweep's joins two at a time."""
+    from concurrent.futures import ThreadPoolExecutor
+    cases = [e for e in golden["joins"] if e["options"]["algorithm"] == 6][:120]
+    work = [(colls(e["collection"]), options_of(lib, e)) for e in cases]  # (npz reads stay on this thread)
+    pinned = work[0][0]
+    S.pin_device(pinned)
+    try:
+        with ThreadPoolExecutor(max_workers=4) as pool:
+            reps = list(pool.map(lambda w: S.join(w[0], w[1]), work))
+    finally:
+        S.unpin_device(pinned)
+    for rep, e in zip(reps, cases):
+        assert_same(rep, e, "concurrent")
