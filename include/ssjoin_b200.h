@@ -46,6 +46,17 @@ ssj_status ssjb_partition_rows(const ssj_collection* coll, const ssj_join_option
 int ssjb_device_count(void);
 ssj_status ssjb_set_devices(int count);
 
+/* Row shards per GPU of one self-join (default: env SSJB_SHARDS_PER_DEVICE,
+ * else 1; 0 restores the default).  Values above 1 run the multi-GPU
+ * partition and shard merge on fewer devices -- the worker-count invariance
+ * check of reference tests/test_parallel.cpp:37-59 on a one-GPU host. */
+ssj_status ssjb_set_shards_per_device(int count);
+
+/* Frees the idle join workspaces (survivor / result buffers a dense join grew
+ * and the pool kept) of `device`, or of every device for -1.  Idle bytes kept
+ * per device are bounded by env SSJB_WORKSPACE_KEEP_MB (default: 1/4 of HBM). */
+ssj_status ssjb_trim(int device);
+
 typedef struct ssjb_stats {
     uint64_t window_pairs;   /* pair comparisons = counters.candidates */
     uint64_t survivors;      /* filter survivors verified on the GPU */

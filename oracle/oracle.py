@@ -44,6 +44,10 @@ def lib():
                                              C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
                                              C.c_size_t, C.c_size_t, C.POINTER(P),
                                              C.POINTER(C.c_size_t), C.POINTER(_Counters)]
+        L.oracle_par_bitmap_join_store.argtypes = [P, P, C.c_size_t, C.c_int64, C.c_int64, C.c_int,
+                                                   C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                                   C.c_size_t, C.c_size_t, P, C.POINTER(P),
+                                                   C.POINTER(C.c_size_t), C.POINTER(_Counters)]
         L.oracle_naive_join.argtypes = [P, P, C.c_size_t, C.c_int64, C.c_int64, C.POINTER(P),
                                         C.POINTER(C.c_size_t), C.POINTER(_Counters)]
         L.oracle_naive_join_sim.argtypes = [P, P, C.c_size_t, P, P, C.c_size_t, C.c_int, C.c_int,
@@ -98,6 +102,21 @@ def par_bitmap_join(tokens, offsets, p, q, bitmap_enabled=True, method=1, width=
                                       C.byref(cnt))
     if rc != 0:
         raise RuntimeError("oracle_par_bitmap_join failed")
+    return _take_pairs(ptr, n.value), {f: int(getattr(cnt, f)) for f in COUNTER_FIELDS}
+
+
+def par_bitmap_join_store(tokens, offsets, store, p, q, method=1, width=64, hash=0,
+                          cutoff=INT64_MAX, capacity=2048, row_begin=0, row_end=0):
+    """par_bitmap_join over rows [row_begin, row_end) with a prebuilt sketch
+    store (build_bitmaps of the whole collection): one build per join."""
+    t, o = _csr(tokens, offsets)
+    st = np.ascontiguousarray(store, dtype=np.uint64)
+    ptr, n, cnt = C.c_void_p(), C.c_size_t(), _Counters()
+    rc = lib().oracle_par_bitmap_join_store(t.ctypes.data, o.ctypes.data, len(o) - 1, p, q, 1, method, width,
+                                            hash, cutoff, capacity, row_begin, row_end, st.ctypes.data,
+                                            C.byref(ptr), C.byref(n), C.byref(cnt))
+    if rc != 0:
+        raise RuntimeError("oracle_par_bitmap_join_store failed")
     return _take_pairs(ptr, n.value), {f: int(getattr(cnt, f)) for f in COUNTER_FIELDS}
 
 

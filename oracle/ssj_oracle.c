@@ -156,17 +156,29 @@ int oracle_par_bitmap_join(const uint32_t* tokens, const uint64_t* offsets, size
                            int64_t q, int bitmap_enabled, int method, int width, int hash,
                            int64_t cutoff, int64_t capacity, size_t row_begin, size_t row_end,
                            oracle_pair** pairs, size_t* pair_count, oracle_counters* counters) {
+    return oracle_par_bitmap_join_store(tokens, offsets, n, p, q, bitmap_enabled, method, width, hash,
+                                        cutoff, capacity, row_begin, row_end, NULL, pairs, pair_count,
+                                        counters);
+}
+
+int oracle_par_bitmap_join_store(const uint32_t* tokens, const uint64_t* offsets, size_t n, int64_t p,
+                                 int64_t q, int bitmap_enabled, int method, int width, int hash,
+                                 int64_t cutoff, int64_t capacity, size_t row_begin, size_t row_end,
+                                 const uint64_t* prebuilt, oracle_pair** pairs, size_t* pair_count,
+                                 oracle_counters* counters) {
     memset(counters, 0, sizeof(*counters));
     *pairs = NULL;
     *pair_count = 0;
     if (capacity < 1) return -1;
     if (row_end == 0 || row_end > n) row_end = n;
     int nwords = width / 64;
-    uint64_t* store = NULL;
-    if (bitmap_enabled) {
-        store = (uint64_t*)calloc(n * (size_t)nwords + 1, sizeof(uint64_t));
-        if (!store) return -1;
-        oracle_build_bitmaps(tokens, offsets, n, method, width, hash, store);
+    uint64_t* owned = NULL;
+    const uint64_t* store = prebuilt;
+    if (bitmap_enabled && !store) {
+        owned = (uint64_t*)calloc(n * (size_t)nwords + 1, sizeof(uint64_t));
+        if (!owned) return -1;
+        oracle_build_bitmaps(tokens, offsets, n, method, width, hash, owned);
+        store = owned;
     }
     pair_vec out = {0, 0, 0};
     for (size_t i = row_begin; i < row_end; ++i) {
@@ -223,13 +235,13 @@ int oracle_par_bitmap_join(const uint32_t* tokens, const uint64_t* offsets, size
             }
         }
     }
-    free(store);
+    free(owned);
     qsort(out.data, out.size, sizeof(oracle_pair), pair_cmp);
     *pairs = out.data;
     *pair_count = out.size;
     return 0;
 oom:
-    free(store);
+    free(owned);
     free(out.data);
     return -1;
 }

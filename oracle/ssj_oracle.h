@@ -74,6 +74,15 @@ int oracle_par_bitmap_join(const uint32_t* tokens, const uint64_t* offsets, size
                            int64_t cutoff, int64_t capacity, size_t row_begin, size_t row_end,
                            oracle_pair** pairs, size_t* pair_count, oracle_counters* counters);
 
+/* The same join with a prebuilt sketch store (oracle_build_bitmaps of the
+ * whole collection at this method/width/hash; NULL: built here), so row blocks
+ * of one join share one build. */
+int oracle_par_bitmap_join_store(const uint32_t* tokens, const uint64_t* offsets, size_t n, int64_t p,
+                                 int64_t q, int bitmap_enabled, int method, int width, int hash,
+                                 int64_t cutoff, int64_t capacity, size_t row_begin, size_t row_end,
+                                 const uint64_t* prebuilt, oracle_pair** pairs, size_t* pair_count,
+                                 oracle_counters* counters);
+
 /* Brute-force self-join, reference src/join.cpp:91-126. */
 int oracle_naive_join(const uint32_t* tokens, const uint64_t* offsets, size_t n, int64_t p,
                       int64_t q, oracle_pair** pairs, size_t* pair_count,

@@ -127,6 +127,8 @@ _EXT_PROTOS = {
     "ssjb_partition_rows": (C.c_int, [P, C.POINTER(JoinOptions), C.c_int, P]),
     "ssjb_device_count": (C.c_int, []),
     "ssjb_set_devices": (C.c_int, [C.c_int]),
+    "ssjb_set_shards_per_device": (C.c_int, [C.c_int]),
+    "ssjb_trim": (C.c_int, [C.c_int]),
     "ssjb_report_stats": (C.c_int, [P, C.POINTER(Stats)]),
     "ssjb_build_bitmaps": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
     "ssjb_time_build": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -5,6 +5,9 @@
 #include <algorithm>
 #include <charconv>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -133,25 +136,102 @@ int configured_devices() {
     return std::max(1, d);
 }
 
-void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double total_s) {
+// ------------------------------------------------------- shard merge
+// Row shards of a self-join own disjoint, ascending id_s ranges (rows i are
+// id_s, reference src/parallel_join.cpp:61-136), and RS blocks own ascending
+// id_r ranges.  So the canonical (id_r, id_s) order of the union is, id_r by
+// id_r, shard 0's run, then shard 1's, ... -- no key comparisons beyond
+// finding each run's end.  The id_r space is cut into T slices of about equal
+// pair counts (a value binary search over the shards' lower bounds); each
+// host thread writes its slice at the offset given by the shards' lower
+// bounds: O(P) copying over all host threads, no growing intermediate.
+using Seq = std::pair<const ssjb::PairOut*, size_t>;
+
+size_t lower_id_r(const Seq& q, uint64_t v) {
+    return static_cast<size_t>(std::lower_bound(q.first, q.first + q.second, v,
+                                                [](const ssjb::PairOut& x, uint64_t j) { return x.id_r < j; }) -
+                               q.first);
+}
+
+void merge_shards(const std::vector<Seq>& seqs, ssjb::PairOut* out) {
     size_t total = 0;
-    for (auto& p : parts) total += p.pairs.size();
+    uint64_t max_id = 0;
+    for (const auto& q : seqs) {
+        total += q.second;
+        if (q.second) max_id = std::max<uint64_t>(max_id, q.first[q.second - 1].id_r);
+    }
+    if (!total) return;
+    const unsigned T = static_cast<unsigned>(
+        std::max<size_t>(1, std::min<size_t>(ssjb::host_threads(), total / (size_t(1) << 16))));
+    // cut[t]: first id_r of slice t (slice t = id_r in [cut[t], cut[t+1]))
+    std::vector<uint64_t> cut(T + 1);
+    cut[0] = 0;
+    cut[T] = max_id + 1;
+    for (unsigned t = 1; t < T; ++t) {
+        const size_t target = total * t / T;
+        uint64_t lo = cut[t - 1], hi = max_id + 1;  // smallest v with count(id_r < v) >= target
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            size_t c = 0;
+            for (const auto& q : seqs) c += lower_id_r(q, mid);
+            if (c >= target) hi = mid;
+            else lo = mid + 1;
+        }
+        cut[t] = lo;
+    }
+    auto slice = [&](unsigned t) {
+        const size_t G = seqs.size();
+        std::vector<size_t> at(G), end(G);
+        size_t dst = 0;
+        for (size_t g = 0; g < G; ++g) {
+            at[g] = lower_id_r(seqs[g], cut[t]);
+            end[g] = lower_id_r(seqs[g], cut[t + 1]);
+            dst += at[g];
+        }
+        ssjb::PairOut* o = out + dst;
+        for (;;) {
+            uint64_t r = UINT64_MAX;
+            for (size_t g = 0; g < G; ++g)
+                if (at[g] < end[g]) r = std::min<uint64_t>(r, seqs[g].first[at[g]].id_r);
+            if (r == UINT64_MAX) break;
+            for (size_t g = 0; g < G; ++g) {
+                const ssjb::PairOut* p = seqs[g].first;
+                size_t k = at[g];
+                while (k < end[g] && p[k].id_r == r) ++k;
+                if (k > at[g]) {
+                    std::memcpy(o, p + at[g], (k - at[g]) * sizeof(ssjb::PairOut));
+                    o += k - at[g];
+                    at[g] = k;
+                }
+            }
+        }
+    };
+    if (T == 1) {
+        slice(0);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(slice, t);
+    slice(0);
+    for (auto& x : th) x.join();
+}
+
+// total_s < 0: the join's total is measured from t0 after the merge
+void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double total_s,
+                 std::chrono::steady_clock::time_point t0 = {}) {
     if (parts.size() == 1) {
         rep.pairs = std::move(parts[0].pairs);
     } else {
-        // shards own disjoint id_s ranges; k-way merge by (id_r, id_s)
-        ssjb::PairVec merged;
-        merged.reserve(total);
+        std::vector<Seq> seqs;
+        size_t total = 0;
         for (auto& p : parts) {
-            ssjb::PairVec tmp;
-            tmp.reserve(merged.size() + p.pairs.size());
-            std::merge(merged.begin(), merged.end(), p.pairs.begin(), p.pairs.end(), std::back_inserter(tmp),
-                       [](const ssjb::PairOut& x, const ssjb::PairOut& y) {
-                           return x.id_r != y.id_r ? x.id_r < y.id_r : x.id_s < y.id_s;
-                       });
-            merged.swap(tmp);
+            seqs.emplace_back(p.pairs.data(), p.pairs.size());
+            total += p.pairs.size();
         }
+        ssjb::PairVec merged(total);
+        merge_shards(seqs, merged.data());
         rep.pairs = std::move(merged);
+        for (auto& p : parts) p.pairs = ssjb::PairVec();
     }
     ssj_counters& c = rep.counters;
     std::memset(&c, 0, sizeof c);
@@ -183,12 +263,97 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
         s.filter_kernel = p.stats.filter_kernel;
     }
     s.devices = static_cast<int>(parts.size());
+    if (total_s < 0) total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     rep.timings.total_s = total_s;
     rep.timings.verify_s = std::max(0.0, total_s - rep.timings.index_s - rep.timings.candidates_s);
 }
 
-// Runs rows [row_begin, row_end) split over `devices` GPUs (first_device..);
-// the engines' results per device (delivery: see JoinPlan::delivery).
+// Persistent host workers for per-device shard work.  The engine keeps
+// per-(host thread, device) CUDA resources (streams, event pools, pinned
+// staging), so shard work must run on long-lived threads: a batch of tasks
+// takes idle workers (spawning more only when every worker is busy, i.e. up
+// to the peak number of shards in flight) and the workers outlive the call.
+class DeviceWorkers {
+  public:
+    static DeviceWorkers& get() {
+        static DeviceWorkers* w = new DeviceWorkers();  // leaked: workers are detached
+        return *w;
+    }
+    // Runs every task, returns when all have finished (exceptions rethrown, first first).
+    void run_all(std::vector<std::function<void()>>& tasks) {
+        const size_t n = tasks.size();
+        std::vector<std::exception_ptr> errs(n);
+        std::mutex dmu;
+        std::condition_variable dcv;
+        size_t left = n;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (size_t k = 0; k < n; ++k) {
+                q_.push_back([&, k]() {
+                    try {
+                        tasks[k]();
+                    } catch (...) {
+                        errs[k] = std::current_exception();
+                    }
+                    std::lock_guard<std::mutex> l2(dmu);
+                    if (--left == 0) dcv.notify_all();
+                });
+            }
+            while (idle_ < q_.size()) {
+                std::thread([this]() { loop(); }).detach();
+                ++idle_;
+            }
+        }
+        cv_.notify_all();
+        std::unique_lock<std::mutex> lk(dmu);
+        dcv.wait(lk, [&]() { return left == 0; });
+        lk.unlock();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    }
+    size_t threads() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return spawned_;
+    }
+
+  private:
+    void loop() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            ++spawned_;
+        }
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&]() { return !q_.empty(); });
+                f = std::move(q_.front());
+                q_.pop_front();
+                --idle_;
+            }
+            f();
+            std::lock_guard<std::mutex> lk(mu_);
+            ++idle_;
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    size_t idle_ = 0, spawned_ = 0;
+};
+
+int g_shards_per_device = 0;  // 0: env SSJB_SHARDS_PER_DEVICE, else 1
+
+int shards_per_device() {
+    if (g_shards_per_device > 0) return g_shards_per_device;
+    const char* v = std::getenv("SSJB_SHARDS_PER_DEVICE");
+    return std::max(1, v && *v ? std::atoi(v) : 1);
+}
+
+// Runs rows [row_begin, row_end) split over `devices` GPUs (first_device..),
+// shards_per_device() row shards per GPU (more than one only as a test hook:
+// the multi-GPU partition and merge exercised on one device); the engines'
+// results per shard, in row order (delivery: see JoinPlan::delivery).
 std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
                                                size_t row_end, int devices, int first_device, int delivery) {
     if (coll.size() >= (size_t(1) << 31)) throw std::invalid_argument("collections above 2^31 records are not supported");
@@ -197,12 +362,13 @@ std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, con
     const int avail = ssjb::engine_device_count();
     if (avail <= 0) throw ssjb::DeviceError("no CUDA device available for the B200 join");
     devices = std::max(1, std::min(devices, avail - first_device));
-    std::vector<ssjb::EngineResult> parts(static_cast<size_t>(devices));
-    if (devices == 1) {
+    const int shards = devices * shards_per_device();
+    std::vector<ssjb::EngineResult> parts(static_cast<size_t>(shards));
+    if (shards == 1) {
         ssjb::engine_join(coll, whole, first_device, parts[0]);
     } else {
         // balanced contiguous row blocks of the range (window-pair prefix sums)
-        std::vector<uint64_t> bounds(static_cast<size_t>(devices) + 1);
+        std::vector<uint64_t> bounds(static_cast<size_t>(shards) + 1);
         {
             std::vector<double> pre(row_end - row_begin + 1, 0.0);
             for (size_t i = row_begin; i < row_end; ++i) {
@@ -210,30 +376,23 @@ std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, con
                 pre[i - row_begin + 1] = pre[i - row_begin] + (j0 < i ? double(i - j0) : 0.0) + 1.0;
             }
             bounds[0] = row_begin;
-            for (int g = 1; g < devices; ++g) {
-                const double target = pre.back() * g / devices;
+            for (int g = 1; g < shards; ++g) {
+                const double target = pre.back() * g / shards;
                 uint64_t b = row_begin + (std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
                 b = row_begin + ((b - row_begin) & ~uint64_t(127));  // 128-row tile boundaries
                 bounds[g] = std::max(b, bounds[g - 1]);
             }
-            bounds[devices] = row_end;
+            bounds[shards] = row_end;
         }
-        std::vector<std::thread> pool;
-        std::vector<std::exception_ptr> errs(static_cast<size_t>(devices));
-        for (int g = 0; g < devices; ++g) {
-            pool.emplace_back([&, g]() {
-                try {
-                    ssjb::JoinPlan p = ssjb::make_plan(coll, o, bounds[g], bounds[g + 1]);
-                    p.delivery = delivery;
-                    ssjb::engine_join(coll, p, first_device + g, parts[static_cast<size_t>(g)]);
-                } catch (...) {
-                    errs[static_cast<size_t>(g)] = std::current_exception();
-                }
+        std::vector<std::function<void()>> tasks;
+        for (int g = 0; g < shards; ++g) {
+            tasks.emplace_back([&, g]() {
+                ssjb::JoinPlan p = ssjb::make_plan(coll, o, bounds[g], bounds[g + 1]);
+                p.delivery = delivery;
+                ssjb::engine_join(coll, p, first_device + g % devices, parts[static_cast<size_t>(g)]);
             });
         }
-        for (auto& t : pool) t.join();
-        for (auto& e : errs)
-            if (e) std::rethrow_exception(e);
+        DeviceWorkers::get().run_all(tasks);
     }
     return parts;
 }
@@ -243,8 +402,7 @@ std::unique_ptr<ssj_report> run_gpu_join(const ssjb::Collection& coll, const ssj
     const auto t0 = std::chrono::steady_clock::now();
     auto parts = run_self_parts(coll, o, row_begin, row_end, devices, first_device, 0);
     auto rep = std::make_unique<ssj_report>();
-    const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(*rep, parts, total);
+    fill_report(*rep, parts, -1.0, t0);  // total_s includes the shard merge
     return rep;
 }
 
@@ -260,25 +418,17 @@ std::vector<ssjb::EngineResult> run_rs_parts(const ssjb::Collection& r, const ss
     devices = std::max(1, std::min(devices, avail));
     if (r.size() < static_cast<size_t>(devices) * 1024) devices = 1;
     std::vector<ssjb::EngineResult> parts(static_cast<size_t>(devices));
-    std::vector<std::thread> pool;
-    std::vector<std::exception_ptr> errs(static_cast<size_t>(devices));
+    std::vector<std::function<void()>> tasks;
     for (int g = 0; g < devices; ++g) {
         const size_t b = r.size() * static_cast<size_t>(g) / devices, e = r.size() * static_cast<size_t>(g + 1) / devices;
-        auto work = [&, g, b, e]() {
-            try {
-                ssjb::RsPlan p = ssjb::make_rs_plan(r, sc, o, b, e);
-                p.delivery = delivery;
-                ssjb::engine_join_rs(r, sc, p, g, parts[static_cast<size_t>(g)]);
-            } catch (...) {
-                errs[static_cast<size_t>(g)] = std::current_exception();
-            }
-        };
-        if (devices == 1) work();
-        else pool.emplace_back(work);
+        tasks.emplace_back([&, g, b, e]() {
+            ssjb::RsPlan p = ssjb::make_rs_plan(r, sc, o, b, e);
+            p.delivery = delivery;
+            ssjb::engine_join_rs(r, sc, p, g, parts[static_cast<size_t>(g)]);
+        });
     }
-    for (auto& t : pool) t.join();
-    for (auto& e : errs)
-        if (e) std::rethrow_exception(e);
+    if (devices == 1) tasks[0]();
+    else DeviceWorkers::get().run_all(tasks);
     return parts;
 }
 
@@ -286,24 +436,9 @@ std::unique_ptr<ssj_report> run_gpu_join_rs(const ssjb::Collection& r, const ssj
                                             const ssjb::Options& o, int devices) {
     const auto t0 = std::chrono::steady_clock::now();
     auto parts = run_rs_parts(r, sc, o, devices, 0);
-    devices = static_cast<int>(parts.size());
-    // blocks own ascending id_r ranges: concatenation is the canonical order
-    ssjb::PairVec all;
-    if (devices > 1) {
-        size_t count = 0;
-        for (auto& p : parts) count += p.pairs.size();
-        all.resize(count);
-        size_t at = 0;
-        for (auto& p : parts) {
-            if (!p.pairs.empty()) std::memcpy(all.data() + at, p.pairs.data(), p.pairs.size() * sizeof(ssjb::PairOut));
-            at += p.pairs.size();
-            p.pairs = ssjb::PairVec();
-        }
-    }
     auto rep = std::make_unique<ssj_report>();
-    const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(*rep, parts, total);
-    if (devices > 1) rep->pairs = std::move(all);
+    fill_report(*rep, parts, -1.0, t0);  // blocks own ascending id_r ranges (merge = concatenation)
+    const double total = rep->timings.total_s;
     rep->timings.index_s = rep->timings.candidates_s = 0;  // naive: all verify (src/join.cpp:124)
     rep->timings.verify_s = total;
     return rep;
@@ -344,33 +479,45 @@ void stream_parts(std::vector<ssjb::EngineResult>& parts, size_t n_ids, size_t c
             ja = jb;
             continue;
         }
-        std::vector<ssjb::PairVec> seqs;
+        // per part: its host run and its device runs (merged on the GPU) share
+        // id_s ranges, so they are merged by key; across parts (row shards /
+        // RS blocks) the id ranges are disjoint and ordered: merge_shards
+        std::vector<ssjb::PairVec> own;
+        std::vector<Seq> seqs;
         for (auto& p : parts) {
+            const ssjb::PairOut* lo = nullptr;
+            size_t cnt = 0;
             if (!p.pairs.empty()) {
-                auto lo = std::lower_bound(p.pairs.begin(), p.pairs.end(), ja,
-                                           [](const ssjb::PairOut& x, size_t j) { return x.id_r < j; });
-                auto hi = std::lower_bound(lo, p.pairs.end(), jb,
-                                           [](const ssjb::PairOut& x, size_t j) { return x.id_r < j; });
-                if (lo != hi) seqs.emplace_back(lo, hi);
+                const Seq all(p.pairs.data(), p.pairs.size());
+                const size_t a = lower_id_r(all, ja), b = lower_id_r(all, jb);
+                lo = p.pairs.data() + a;
+                cnt = b - a;
             }
-            if (p.runs) {
-                ssjb::PairVec v;
-                ssjb::runs_extract(*p.runs, static_cast<uint32_t>(ja), static_cast<uint32_t>(jb), v);
-                if (!v.empty()) seqs.push_back(std::move(v));
+            ssjb::PairVec v;
+            if (p.runs) ssjb::runs_extract(*p.runs, static_cast<uint32_t>(ja), static_cast<uint32_t>(jb), v);
+            if (!v.empty() && cnt) {
+                ssjb::PairVec m(v.size() + cnt);
+                std::merge(lo, lo + cnt, v.begin(), v.end(), m.begin(), key_less);
+                own.push_back(std::move(m));
+            } else if (!v.empty()) {
+                own.push_back(std::move(v));
+            } else if (cnt) {
+                seqs.emplace_back(lo, cnt);
+                continue;
+            } else {
+                continue;
             }
+            seqs.emplace_back(own.back().data(), own.back().size());
         }
-        while (seqs.size() > 1) {  // pairwise merges (a handful of sequences per chunk)
-            std::vector<ssjb::PairVec> next;
-            for (size_t k = 0; k + 1 < seqs.size(); k += 2) {
-                ssjb::PairVec m(seqs[k].size() + seqs[k + 1].size());
-                std::merge(seqs[k].begin(), seqs[k].end(), seqs[k + 1].begin(), seqs[k + 1].end(), m.begin(),
-                           key_less);
-                next.push_back(std::move(m));
-            }
-            if (seqs.size() & 1) next.push_back(std::move(seqs.back()));
-            seqs.swap(next);
+        if (seqs.size() == 1) {
+            sink(seqs[0].first, seqs[0].second);
+        } else if (!seqs.empty()) {
+            size_t cnt = 0;
+            for (const auto& q : seqs) cnt += q.second;
+            ssjb::PairVec m(cnt);
+            merge_shards(seqs, m.data());
+            sink(m.data(), m.size());
         }
-        if (!seqs.empty()) sink(seqs[0].data(), seqs[0].size());
         ja = jb;
     }
 }
@@ -741,6 +888,21 @@ SSJB_API ssj_status ssjb_set_devices(int count) {
     return guarded([&]() {
         if (count < 1) throw std::invalid_argument("device count must be >= 1");
         g_devices = count;
+        return SSJ_OK;
+    });
+}
+
+SSJB_API ssj_status ssjb_set_shards_per_device(int count) {
+    return guarded([&]() {
+        if (count < 0) throw std::invalid_argument("shards per device must be >= 0");
+        g_shards_per_device = count;
+        return SSJ_OK;
+    });
+}
+
+SSJB_API ssj_status ssjb_trim(int device) {
+    return guarded([&]() {
+        ssjb::engine_trim(device);
         return SSJ_OK;
     });
 }

@@ -1478,21 +1478,28 @@ struct JoinWorkspace {
         va = vb = hist = sums = nullptr;
         surv_cap = res_cap = 0;
     }
-    // (buffers may still be in use by the stream: callers synchronise it first)
+    uint64_t bytes() const { return surv_cap * sizeof(uint2) + res_cap * 24; }
+    // (buffers may still be in use by the stream: callers synchronise it first).
+    // Every pointer is nulled and its capacity zeroed as soon as it is freed, so
+    // a failed (throwing) allocation leaves an empty workspace, never a stale
+    // capacity over freed memory.
     void ensure(int dev, uint64_t scap, uint64_t rcap) {
         device = dev;
         if (scap > surv_cap) {
             cudaFree(surv);
+            surv = nullptr;
+            surv_cap = 0;
             CK(cudaMalloc(&surv, scap * sizeof(uint2)));
             surv_cap = scap;
         }
         if (rcap > res_cap) {
-            cudaFree(ka);
-            cudaFree(kb);
-            cudaFree(va);
-            cudaFree(vb);
-            cudaFree(hist);
-            cudaFree(sums);
+            for (void** p : {reinterpret_cast<void**>(&ka), reinterpret_cast<void**>(&kb),
+                             reinterpret_cast<void**>(&va), reinterpret_cast<void**>(&vb),
+                             reinterpret_cast<void**>(&hist), reinterpret_cast<void**>(&sums)}) {
+                cudaFree(*p);
+                *p = nullptr;
+            }
+            res_cap = 0;
             const uint64_t tiles = (rcap + dev::kSortTile - 1) / dev::kSortTile;
             CK(cudaMalloc(&ka, rcap * 8));
             CK(cudaMalloc(&kb, rcap * 8));
@@ -1517,11 +1524,31 @@ WorkspacePool& workspace_pool() {
     return *p;
 }
 
+// Idle workspace bytes kept per device (SSJB_WORKSPACE_KEEP_MB, default a
+// quarter of the device's HBM): a dense join grows its workspace to tens of
+// GB; beyond this budget a returned workspace is freed instead of pooled.
+uint64_t workspace_keep_bytes(int device) {
+    static uint64_t keep[16] = {};
+    static std::once_flag once[16];
+    std::call_once(once[device & 15], [device]() {
+        const uint64_t mb = env_u64("SSJB_WORKSPACE_KEEP_MB", 0);
+        size_t f = 0, t = 0;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        if (cudaMemGetInfo(&f, &t) != cudaSuccess) t = 0;
+        cudaSetDevice(cur);
+        keep[device & 15] = mb ? (mb << 20) : t / 4;
+    });
+    return keep[device & 15];
+}
+
 struct WorkspaceLease {
     int device;
     cudaStream_t stream;
     std::unique_ptr<JoinWorkspace> ws;
-    WorkspaceLease(int dev, cudaStream_t s) : device(dev), stream(s) {
+    int uncaught;
+    WorkspaceLease(int dev, cudaStream_t s) : device(dev), stream(s), uncaught(std::uncaught_exceptions()) {
         WorkspacePool& P = workspace_pool();
         std::lock_guard<std::mutex> lk(P.mu);
         auto& v = P.idle[dev & 15];
@@ -1534,12 +1561,33 @@ struct WorkspaceLease {
     }
     ~WorkspaceLease() {
         cudaStreamSynchronize(stream);  // nothing queued may still use the buffers
+        // a join that failed (e.g. an allocation inside ensure) returns nothing
+        // to the pool: its buffers are freed with it
+        if (std::uncaught_exceptions() > uncaught) {
+            ws->release();
+            return;
+        }
         WorkspacePool& P = workspace_pool();
         std::lock_guard<std::mutex> lk(P.mu);
-        P.idle[device & 15].push_back(std::move(ws));
+        auto& v = P.idle[device & 15];
+        uint64_t held = ws->bytes();
+        for (auto& w : v) held += w->bytes();
+        if (held > workspace_keep_bytes(device)) ws->release();  // keep the (empty) object
+        v.push_back(std::move(ws));
     }
 };
 }  // namespace
+
+// Frees every idle join workspace of `device` (all devices for -1).
+void engine_trim(int device) {
+    WorkspacePool& P = workspace_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (int d = 0; d < 16; ++d) {
+        if (device >= 0 && d != (device & 15)) continue;
+        for (auto& w : P.idle[d]) w->release();
+        P.idle[d].clear();
+    }
+}
 
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
     using Clock = std::chrono::steady_clock;
@@ -1745,6 +1793,16 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     });
     const size_t free_b = free_at_first[device & 15];
     const uint64_t big = free_b >= (size_t(64) << 30) ? 1 : 0;
+    // live free HBM for the optional large buffers below (queried only when a
+    // decision depends on it: earlier joins may hold pooled workspaces, pins)
+    size_t live_free_b = 0;
+    auto live_free = [&]() -> size_t {
+        if (!live_free_b) {
+            size_t f = 0, t = 0;
+            if (cudaMemGetInfo(&f, &t) == cudaSuccess) live_free_b = f;
+        }
+        return live_free_b;
+    };
     uint64_t surv_cap =
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
     uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
@@ -1765,7 +1823,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     const uint64_t ic_bytes = n_items * tl.tile_rows * 4;
     const bool keep_item_counts =
         !naive && (ic_bytes <= (uint64_t(1) << 30) ||
-                   (ic_bytes <= (uint64_t(16) << 30) && static_cast<double>(ic_bytes) <= 0.3 * double(free_b)));
+                   (ic_bytes <= (uint64_t(16) << 30) && static_cast<double>(ic_bytes) <= 0.3 * double(live_free())));
     uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * tl.tile_rows) : nullptr;
     // second level: per (item, filter tile, column part, row) counts written by the
     // tcgen05 epilogue (plain u16 stores, no memset: every slot of a processed
@@ -1776,7 +1834,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // (kept for the dense regime only -- the level-2 GEMM joins, where most rows
     // saturate; elsewhere the stores cost the filter more than the rescan saves)
     uint16_t* d_tile_counts = keep_item_counts && use_tc && l2gemm && !use_tc2 && tl.tile_rows == dev::kRowTile &&
-                                      tc_bytes <= std::min<uint64_t>(uint64_t(2) << 30, free_b / 5)
+                                      tc_bytes <= std::min<uint64_t>(uint64_t(2) << 30, live_free() / 5)
                                   ? A.alloc<uint16_t>(n_items * kTilesPerItem * 4 * dev::kRowTile)
                                   : nullptr;
     dev::Control* d_ctl = A.alloc<dev::Control>(1);

@@ -86,5 +86,6 @@ double engine_time_build(const Collection& c, Method method, int width, int hash
 void engine_pin(const Collection& c, int device);
 void engine_unpin(const Collection& c, int device);
 void engine_release_host(const Collection& c);  // undo host page registration
+void engine_trim(int device);                   // free idle join workspaces (-1: all devices)
 
 }  // namespace ssjb

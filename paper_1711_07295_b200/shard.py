@@ -44,19 +44,49 @@ def merge_counters(parts):
 
 def gather_to_root(pairs, counters, saturated, group=None):
     """Gather every rank's (pairs, counters, saturated) to rank 0 and merge.
+    Count-first: the pair counts and counters travel as one small int64
+    all-gather, then each rank's pairs go to rank 0 as one raw byte tensor
+    received in place into a preallocated buffer (no pickling).
     Returns (pairs, counters, saturated) on rank 0 and None elsewhere."""
+    import torch
     import torch.distributed as dist
+    from .ssjoin import PAIR_DTYPE
     rank = dist.get_rank()
     world = dist.get_world_size()
-    payload = (pairs.tobytes(), counters, int(saturated))
-    bucket = [None] * world if rank == 0 else None
-    dist.gather_object(payload, bucket, dst=0, group=group)
+    head = torch.tensor([len(pairs), int(saturated)] + [int(counters.get(k, 0)) for k in COUNTER_KEYS],
+                        dtype=torch.int64)
+    heads = [torch.zeros_like(head) for _ in range(world)]
+    dist.all_gather(heads, head, group=group)
     if rank != 0:
+        if len(pairs):
+            buf = np.ascontiguousarray(pairs).view(np.uint8)
+            dist.send(torch.from_numpy(buf), dst=0, group=group)
         return None
-    from .ssjoin import PAIR_DTYPE
-    runs = [np.frombuffer(b, dtype=PAIR_DTYPE) for b, _, _ in bucket]
-    merged_counters, sat = merge_counters([(c, s) for _, c, s in bucket])
-    return merge_runs(runs), merged_counters, sat
+    counts = [int(h[0]) for h in heads]
+    allp = np.empty(sum(counts), dtype=PAIR_DTYPE)
+    at = 0
+    for r, c in enumerate(counts):
+        if c == 0:
+            continue
+        dst = allp[at:at + c].view(np.uint8)
+        if r == 0:
+            dst[:] = np.ascontiguousarray(pairs).view(np.uint8)
+        else:
+            dist.recv(torch.from_numpy(dst), src=r, group=group)
+        at += c
+    merged_counters, sat = merge_counters(
+        [({k: int(h[2 + i]) for i, k in enumerate(COUNTER_KEYS)}, int(h[1])) for h in heads])
+    return merge_row_blocks(allp, counts), merged_counters, sat
+
+
+def merge_row_blocks(allp, counts):
+    """Canonical order of the concatenated results of ranks that own
+    ascending, disjoint row blocks (rows are id_s): within one id_r, rank r's
+    run precedes rank r+1's and each run is id_s-sorted, so a STABLE sort on
+    id_r alone is the merge."""
+    if sum(1 for c in counts if c) <= 1:
+        return allp
+    return allp[np.argsort(allp["id_r"], kind="stable")]
 
 
 def heap_merge(runs):

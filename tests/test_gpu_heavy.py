@@ -3,8 +3,11 @@ C4 ORKUT-shaped, C5 AOL-shaped; paper_1711_07295_b200/datasets.py).
 
 The CPU oracle cannot finish these joins in test time (C4: 4.7e11 window
 pairs, C5: 1.2e13), so each config is pinned three ways:
-  * against the reference's own full-size run where one is committed
-    (tests/golden/large.jsonl, C3: the unmodified reference, 8 threads);
+  * against the reference's own full-size runs (tests/golden/large.jsonl):
+    C3's PAR_BITMAP run (pairs + every counter, 8 threads), and for every
+    config the reference's exact PPJOIN run (``<config>_exact``: the full pair
+    list's count and sha256; every exact algorithm of the reference returns
+    the PAR_BITMAP pair list, tests/test_joins.cpp:62-112);
   * row-block samples: ssjb_join_rows over blocks spread across the
     collection vs the oracle on the same rows -- same pairs, same counters
     (reference src/parallel_join.cpp:61-136 is row-local, so a row block of
@@ -91,6 +94,13 @@ def test_heavy_config(lib, oracle, name):
         for k in COUNTERS:
             assert c[k] == g["counters"][k], k
         assert rep.saturated_records == g["saturated_records"]
+    # the reference's exact prefix-filter join: the full pair list
+    x = golden_large(name.split("_")[0] + "_exact")
+    assert x is not None or name == "C3", f"no full-size reference pairs for {name}"
+    if x is not None:
+        assert x["collection_sha256"] == hashlib.sha256(t.tobytes() + o.tobytes()).hexdigest()
+        assert len(pairs) == x["pair_count"]
+        assert hashlib.sha256(pairs.tobytes()).hexdigest() == x["pairs_sha256"]
 
     # size-independent properties
     assert c["candidates"] == D.window_pairs(o, p, q)
@@ -134,3 +144,25 @@ def test_heavy_config(lib, oracle, name):
     assert sum(x.saturated_records for x in parts) == rep.saturated_records
     print(f"{name}: n={n} window={c['candidates']:.3e} verified={c['verified']} matched={c['matched']} "
           f"saturated={rep.saturated_records} total_s={rep.timings['total_s']:.3f}")
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_heavy_sharded(lib, name):
+    """8 row shards through ssj_join (the multi-GPU partition + shard merge
+    on one device) reproduce the reference's full-size pair list; the merge
+    of 8 shards costs a small fraction of the join."""
+    coll, t, o = collection(lib, name)
+    _, mkopts, kw = CONFIGS[name]
+    g = golden_large(name + "_exact") or golden_large(name)
+    assert lib.ssjb_set_shards_per_device(8) == 0
+    try:
+        rep = S.join(coll, mkopts(lib, **kw))
+    finally:
+        lib.ssjb_set_shards_per_device(0)
+    assert rep.extra["devices"] == 8
+    assert len(rep.pairs) == g["pair_count"]
+    assert hashlib.sha256(rep.pairs.tobytes()).hexdigest() == g["pairs_sha256"]
+    if "counters" in g:
+        for k in COUNTERS:
+            assert rep.counters[k] == g["counters"][k], k
+    print(f"{name} 8 shards: total_s={rep.timings['total_s']:.3f}")

@@ -110,6 +110,31 @@ def test_row_shards_add_up(lib, golden, colls):
             assert sum(r.saturated_records for r in reps) == e["saturated_records"]
 
 
+@pytest.fixture
+def shards(lib):
+    """ssjb_set_shards_per_device for one test, restored afterwards."""
+    def set_(k):
+        assert lib.ssjb_set_shards_per_device(k) == capi.SSJ_OK
+    yield set_
+    lib.ssjb_set_shards_per_device(0)
+
+
+@pytest.mark.parametrize("count", [2, 4, 8])
+def test_shard_count_changes_nothing(lib, golden, colls, shards, count):
+    """Worker-count invariance through the drop-in path (reference
+    tests/test_parallel.cpp:37-59, tests/acceptance.cpp:297-336): ssj_join
+    split into 2/4/8 row shards -- the multi-GPU partition, per-shard engines
+    on persistent device workers, and the shard merge of capi.cpp -- returns
+    every fixture's bytes and counters unchanged."""
+    shards(count)
+    for e in golden["joins"]:
+        if e["options"]["algorithm"] != capi.SSJ_ALGO_PAR_BITMAP:
+            continue
+        rep = S.join(colls(e["collection"]), options_of(lib, e))
+        assert_same(rep, e, f"{count} shards")
+        assert rep.extra["devices"] == count
+
+
 @pytest.mark.parametrize("flavour", FILTERS)
 def test_random_collections_vs_oracle(lib, oracle, flavour, monkeypatch):
     set_filter(monkeypatch, flavour)
