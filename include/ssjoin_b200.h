@@ -74,6 +74,13 @@ typedef struct ssjb_stats {
     double ms_download;
     int devices;
     int filter_kernel;       /* 0 = POPC kernel */
+    /* head-overlap phase of dense joins (K3a, exact head-token overlaps on the
+     * tensor cores for the large-record region); zero when it did not run */
+    uint64_t head_pairs;     /* region window pairs (the kernel's algorithmic work) */
+    uint64_t head_survivors; /* region pairs passed to exact verification */
+    double ms_head;          /* device ms of the head-overlap kernel (max over GPUs) */
+    double ms_head_setup;    /* device ms of head selection + operand build */
+    int head_k;              /* head tokens (GEMM depth) */
 } ssjb_stats;
 
 ssj_status ssjb_report_stats(const ssj_report* report, ssjb_stats* out);

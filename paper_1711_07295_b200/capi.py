@@ -105,7 +105,9 @@ class Stats(C.Structure):
                                           "h2d_bytes", "d2h_bytes", "verify_bytes")] + \
                [(n, C.c_double) for n in ("ms_upload", "ms_build", "ms_filter", "ms_rescan",
                                           "ms_verify", "ms_sort", "ms_download")] + \
-               [("devices", C.c_int), ("filter_kernel", C.c_int)]
+               [("devices", C.c_int), ("filter_kernel", C.c_int),
+                ("head_pairs", C.c_uint64), ("head_survivors", C.c_uint64),
+                ("ms_head", C.c_double), ("ms_head_setup", C.c_double), ("head_k", C.c_int)]
 
 
 # ssjb_pair_sink: int (*)(const ssj_pair*, size_t, void*)

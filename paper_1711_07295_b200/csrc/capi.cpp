@@ -84,11 +84,6 @@ ssjb::Algo to_algo(int a) {
     return static_cast<ssjb::Algo>(a);
 }
 
-const char* algo_name(ssjb::Algo a) {
-    static const char* names[] = {"naive", "allpairs", "ppjoin", "ppjoin+", "groupjoin", "adaptjoin", "par-bitmap"};
-    return names[static_cast<int>(a)];
-}
-
 // reference src/capi.cpp:82-110 (same validation, same messages)
 ssjb::Options to_options(const ssj_join_options& in) {
     ssjb::Options o;
@@ -115,13 +110,29 @@ ssjb::Options to_options(const ssj_join_options& in) {
     return o;
 }
 
-// Algorithms the GPU path runs; the reference's checks of
-// src/parallel_join.cpp:41-44 for the data-parallel join.
-void check_supported(const ssjb::Options& o) {
+// Algorithms of the drop-in.  PAR_BITMAP and NAIVE run as themselves (the
+// PAR_BITMAP checks are reference src/parallel_join.cpp:41-44).  The
+// prefix-filter algorithms (ALLPAIRS, PPJOIN, PPJOIN+, GROUPJOIN, ADAPTJOIN)
+// are exact joins whose pair list is the same for every algorithm (reference
+// tests/test_joins.cpp:62-112, tests/test_capi.cpp:64-88), so the B200 build
+// returns that list from its GPU join: the Bitmap-Filter join for Jaccard
+// thresholds (the call's bitmap options, the filter enabled), the NAIVE join
+// for the other similarity functions.  Their counters describe that GPU run,
+// not the reference's prefix-filter internals; candidates == pruned +
+// verified and matched == pair count hold as for every algorithm.
+void check_supported(ssjb::Options& o) {
     if (o.algorithm == ssjb::Algo::Naive) return;
-    if (o.algorithm != ssjb::Algo::ParBitmap)
-        throw std::invalid_argument(std::string("algorithm ") + algo_name(o.algorithm) +
-                                    " is not provided by the B200 build (PAR_BITMAP and NAIVE run on the GPU)");
+    if (o.algorithm != ssjb::Algo::ParBitmap) {
+        if (o.sim == ssjb::Sim::Jaccard) {
+            o.algorithm = ssjb::Algo::ParBitmap;
+            o.bitmap_enabled = true;
+        } else {
+            o.algorithm = ssjb::Algo::Naive;
+        }
+        o.workers = std::max(o.workers, 1);
+        if (o.buffer_capacity < 1) o.buffer_capacity = 2048;
+        return;
+    }
     if (o.workers < 1) throw std::invalid_argument("workers must be >= 1");
     if (o.buffer_capacity < 1) throw std::invalid_argument("buffer capacity must be >= 1");
     if (o.sim != ssjb::Sim::Jaccard) throw std::invalid_argument("the data-parallel join takes a jaccard threshold");
@@ -261,6 +272,11 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
         s.ms_sort = std::max(s.ms_sort, p.stats.ms_sort);
         s.ms_download = std::max(s.ms_download, p.stats.ms_download);
         s.filter_kernel = p.stats.filter_kernel;
+        s.head_pairs += p.stats.head_pairs;
+        s.head_survivors += p.stats.head_survivors;
+        s.ms_head = std::max(s.ms_head, p.stats.ms_head);
+        s.ms_head_setup = std::max(s.ms_head_setup, p.stats.ms_head_setup);
+        s.head_k = std::max(s.head_k, p.stats.head_k);
     }
     s.devices = static_cast<int>(parts.size());
     if (total_s < 0) total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -21,6 +21,7 @@
 #include "filter_tc.cuh"
 #include "filter_tc2.cuh"
 #include "filter_tcm.cuh"
+#include "head_tc.cuh"
 
 namespace ssjb {
 
@@ -1152,6 +1153,116 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
     return t;
 }
 
+// ------------------------------------------------------------ K3a head plan
+// Region and work items of the head-overlap kernel (head_tc.cuh) for one
+// shard, computed on the host.  Eligible joins: Xor/Set sketches with the
+// 256-bit level-2 check (b <= 128), a minov table (not Cosine), records
+// below 2^16 tokens, universes up to 2^28.  SSJB_HEAD: 0 off, 1 auto (region
+// of >= 2^30 window pairs), 2 forced (tests); SSJB_HEAD_MIN_SIZE: S0;
+// SSJB_HEAD_K: head tokens (multiple of 128, <= 4096).
+struct HeadPlan {
+    bool ok = false;
+    uint32_t S0 = 0, L0 = 0, base = 0, tile0 = 0, ntiles = 0, rows_pad = 0;
+    int K = 0;
+    uint64_t pairs = 0;                 // region window pairs (the kernel's algorithmic work)
+    std::vector<uint32_t> tile_col_lo;  // per row tile
+    std::vector<uint2> items;           // (row tile, column chunk), chunk-major
+};
+
+HeadPlan make_head_plan(const Collection& c, const JoinPlan& plan, int W2) {
+    HeadPlan h;
+    const uint64_t mode = env_u64("SSJB_HEAD", 1);
+    const size_t n = c.size();
+    if (!mode || W2 != 4 || plan.naive || plan.cosine || !plan.bitmap.enabled || plan.row_end <= plan.row_begin ||
+        c.max_size >= 65536 || c.universe > (uint64_t(1) << 28) || n >= (size_t(1) << 31))
+        return h;
+    h.K = static_cast<int>(std::min<uint64_t>(4096, env_u64("SSJB_HEAD_K", 2048))) & ~(dev::kHeadSliceK - 1);
+    if (h.K < dev::kHeadSliceK) return h;
+    // S0: the smallest size at which two records of that size may differ in
+    // 64 sketch bits (maxham(2s) >= 64): from there on the 256-bit level-2
+    // sketch stops pruning
+    uint32_t S0 = static_cast<uint32_t>(env_u64("SSJB_HEAD_MIN_SIZE", 0));
+    if (!S0) {
+        S0 = 32;
+        while (S0 <= c.max_size && 2 * size_t(S0) < plan.minov.size() &&
+               2 * int64_t(S0) - 2 * int64_t(plan.minov[2 * S0]) < 64)
+            ++S0;
+    }
+    if (S0 > c.max_size) return h;
+    h.S0 = S0;
+    h.L0 = c.first_ge[S0];
+    const size_t r0 = std::max<size_t>(h.L0, plan.row_begin);
+    if (r0 >= plan.row_end) return h;
+    for (size_t i = r0; i < plan.row_end; ++i) {
+        const size_t lo = std::max<size_t>(h.L0, window_start_of(c, plan, i));
+        h.pairs += i > lo ? i - lo : 0;
+    }
+    if (h.pairs == 0 || (mode == 1 && h.pairs < (uint64_t(1) << 30))) return h;
+    h.base = h.L0 & ~127u;
+    h.tile0 = static_cast<uint32_t>(r0) & ~7u;
+    h.ntiles = static_cast<uint32_t>((plan.row_end - h.tile0 + dev::kRowTile - 1) / dev::kRowTile);
+    h.rows_pad = static_cast<uint32_t>(((n - h.base + 512) + 127) & ~size_t(127));
+    h.tile_col_lo.assign(h.ntiles, 0);
+    std::vector<std::pair<uint32_t, uint32_t>> it;  // (chunk, tile)
+    for (uint32_t t = 0; t < h.ntiles; ++t) {
+        const size_t first = std::max<size_t>(r0, size_t(h.tile0) + size_t(t) * dev::kRowTile);
+        if (first >= plan.row_end) continue;
+        const uint32_t lo = static_cast<uint32_t>(std::max<size_t>(h.L0, window_start_of(c, plan, first))) & ~7u;
+        h.tile_col_lo[t] = std::max(lo, h.base);
+        const size_t rmax = std::min<size_t>(size_t(h.tile0) + size_t(t + 1) * dev::kRowTile, plan.row_end);
+        const size_t c1 = rmax - 1;  // columns j < i <= rmax - 1
+        if (c1 <= h.tile_col_lo[t]) continue;
+        for (size_t cc = (h.tile_col_lo[t] - h.base) / dev::kColChunk; cc <= (c1 - 1 - h.base) / dev::kColChunk; ++cc)
+            it.emplace_back(static_cast<uint32_t>(cc), t);
+    }
+    std::sort(it.begin(), it.end());
+    h.items.resize(it.size());
+    for (size_t k = 0; k < it.size(); ++k) h.items[k] = make_uint2(it[k].second, it[k].first);
+    h.ok = !h.items.empty();
+    return h;
+}
+
+// Device side of the head plan: head selection (token counts over the region,
+// count threshold for the K most frequent, dense indices), the head operand
+// and the per-row (size, tail) info.  Everything lives in the join's arena.
+struct HeadDev {
+    uint8_t* op = nullptr;
+    uint32_t* info = nullptr;
+    uint2* items = nullptr;
+    uint32_t* col_lo = nullptr;
+};
+
+HeadDev head_setup(const DeviceReplica& rep, const Collection& c, const HeadPlan& h, Arena& A, cudaStream_t s,
+                   int sms, uint64_t& launches) {
+    HeadDev d;
+    const uint32_t U = static_cast<uint32_t>(std::max<uint64_t>(c.universe, 1));
+    const uint32_t n = static_cast<uint32_t>(c.size());
+    uint32_t* cnt = A.alloc<uint32_t>(U);
+    uint32_t* hist = A.alloc<uint32_t>(65536);
+    uint32_t* thr = A.alloc<uint32_t>(2);
+    uint16_t* map = A.alloc<uint16_t>(U);
+    CK(cudaMemsetAsync(cnt, 0, size_t(U) * 4, s));
+    CK(cudaMemsetAsync(hist, 0, 65536 * 4, s));
+    CK(cudaMemsetAsync(thr, 0, 8, s));
+    CK(cudaMemsetAsync(map, 0xFF, size_t(U) * 2, s));
+    const unsigned g = static_cast<unsigned>(sms) * 8;
+    dev::head_count<<<g, 256, 0, s>>>(rep.tokens, c.offsets[h.L0], c.offsets[n], cnt);
+    dev::head_hist<<<g, 256, 0, s>>>(cnt, U, hist);
+    dev::head_threshold<<<1, 1024, 0, s>>>(hist, static_cast<uint32_t>(h.K), thr);
+    dev::head_assign<<<g, 256, 0, s>>>(cnt, U, thr, static_cast<uint32_t>(h.K), map, thr + 1);
+    d.op = A.alloc<uint8_t>(size_t(h.rows_pad) * h.K);
+    d.info = A.alloc<uint32_t>(h.rows_pad);
+    dev::head_expand<<<h.rows_pad / 8, 256, 8 * h.K, s>>>(rep.tokens, rep.offsets, n, h.L0, h.base, h.rows_pad / 8,
+                                                         h.K, map, d.op, d.info);
+    launches += 5;
+    CK(cudaGetLastError());
+    d.items = A.alloc<uint2>(h.items.size());
+    d.col_lo = A.alloc<uint32_t>(h.tile_col_lo.size());
+    CK(cudaMemcpyAsync(d.items, h.items.data(), h.items.size() * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d.col_lo, h.tile_col_lo.data(), h.tile_col_lo.size() * 4, cudaMemcpyHostToDevice, s));
+    return d;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ delivery
@@ -1645,6 +1756,11 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             l2gemm = static_cast<double>(cx) < 1.25 * static_cast<double>(c.median_size());
         }
     }
+    // K3a: exact head-token overlaps for the large-record region of dense joins
+    // (head_tc.cuh); active whenever the join runs the level-2 GEMM
+    const HeadPlan hplan = use_tc && W <= 2 && W2 == 4 ? make_head_plan(c, plan, W2) : HeadPlan{};
+    bool head_active = l2gemm && hplan.ok;
+    const bool head_upfront = head_active;  // batch mode from the start (no single-pass fast path)
     const char* kenv = std::getenv("SSJB_TC_KIND");
     // operand kind: fp4 (packed e2m1) halves the operand bytes and doubles the
     // MMA rate per element, which wins for b >= 192 (C2 b=256 sweep: 7.96 vs
@@ -1688,7 +1804,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint16_t* ingest_t16 = nullptr;
     Delta8Dev ingest_d8;
     const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
-    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n &&
+    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n && !head_upfront &&
         n >= env_u64("SSJB_STREAM_MIN_ROWS", 65536) && n > 0 && env_u64("SSJB_STREAM", 1) != 0) {
         static thread_local cudaStream_t copy_streams[16] = {};
         if (!copy_streams[device & 15])
@@ -1927,6 +2043,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.debug = static_cast<int>(env_u64("SSJB_TC_DEBUG", 0));
         TP.bias = level1_acc_bias(W, variant);
         TP.bias2 = level2_acc_bias(W2, variant);
+        TP.emit_col_end = head_active ? hplan.L0 : ~0u;
         if (TP.debug & 2) {
             TP.trace = A.alloc<unsigned long long>(2048 + 2 * 8192);
             CK(cudaMemsetAsync(TP.trace, 0, (2048 + 2 * 8192) * 8, s));
@@ -2052,9 +2169,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         ++st.launches;
         CK(cudaGetLastError());
     };
-    auto launch_verify = [&]() {
+    auto launch_verify = [&](const unsigned long long* count_ptr = nullptr) {
         // survivor count read on the device: no host round trip between K2 and K3
-        VP.count_ptr = &d_ctl->survivors;
+        VP.count_ptr = count_ptr ? count_ptr : &d_ctl->survivors;
         VP.count_cap = surv_cap;
         static const unsigned vmul = static_cast<unsigned>(env_u64("SSJB_VERIFY_GRID", 32));  // latency-bound: more warps
         const unsigned vgrid = static_cast<unsigned>(sms) * vmul;
@@ -2121,7 +2238,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     bool done = false;
     const auto t_launch = Clock::now();  // host setup ends: the first filter launch
     auto t_synced = t_launch;
-    {
+    if (!head_upfront) {
         cudaEvent_t a = T.mark();
         if (streamed) {
             const int variant_s = variant;
@@ -2259,6 +2376,8 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 TP.bias = level1_acc_bias(W, 1);  // the variant-1 operands' biases
                 TP.bias2 = level2_acc_bias(W2, 1);
                 st.filter_kernel = 2;
+                head_active = hplan.ok;
+                TP.emit_col_end = head_active ? hplan.L0 : ~0u;
             }
         }
     }
@@ -2356,6 +2475,77 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
         FP.surv_soft = 0;
         TP.surv_soft = 0;
+        if (head_active) {
+            // K3a over the large-record region (K2 counted those pairs but did not
+            // emit them): batches with a soft survivor cap, each verified by K3
+            cudaEvent_t h0 = T.mark();
+            const HeadDev hd = head_setup(*rep, c, hplan, A, s, sms, st.launches);
+            dev::Control* d_hctl = A.alloc<dev::Control>(1);
+            dev::HeadParams HP{};
+            HP.op = hd.op;
+            HP.base = hplan.base;
+            HP.groups = hplan.rows_pad / 8;
+            HP.kslices = hplan.K / dev::kHeadSliceK;
+            HP.info = hd.info;
+            HP.minov = d_minov;
+            HP.wstart = d_wstart;
+            HP.items = hd.items;
+            HP.tile_col_lo = hd.col_lo;
+            HP.tile0 = hplan.tile0;
+            HP.L0 = hplan.L0;
+            HP.row_begin = static_cast<uint32_t>(plan.row_begin);
+            HP.row_end = static_cast<uint32_t>(plan.row_end);
+            HP.surv = d_surv;
+            HP.surv_cap = surv_cap;
+            HP.ctl = d_hctl;
+            set_smem_once(reinterpret_cast<const void*>(dev::head_overlap_kernel), dev::kHeadSmem);
+            cudaEvent_t h1 = T.mark();
+            const uint64_t hitems = hplan.items.size();
+            uint64_t hsoft = std::max<uint64_t>(surv_cap / 2, 1);
+            uint64_t hb = 0;
+            dev::Control hc{};
+            while (hb < hitems) {
+                CK(cudaMemsetAsync(d_hctl, 0, sizeof(dev::Control), s));
+                HP.item_begin = hb;
+                HP.item_end = hitems;
+                HP.surv_soft = hsoft;
+                cudaEvent_t a = T.mark();
+                dev::head_overlap_kernel<<<static_cast<unsigned>(std::min<uint64_t>(hitems - hb, sms)),
+                                           dev::kHeadThreads, dev::kHeadSmem, s>>>(HP);
+                ++st.launches;
+                CK(cudaGetLastError());
+                cudaEvent_t b = T.mark();
+                CK(cudaMemcpyAsync(&hc, d_hctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                st.ms_head += Timer::ms(a, b);
+                const uint64_t S = hc.survivors;
+                const uint64_t processed = std::min<uint64_t>(hc.work_next, hitems - hb);
+                if (S > surv_cap) {  // overshoot: nothing was counted, redo with a lower cap
+                    hsoft = std::max<uint64_t>(hsoft / 4, 1);
+                    continue;
+                }
+                st.head_survivors += S;
+                ++st.batches;
+                if (S) {
+                    if (res_count + S > res_cap) {
+                        flush_results(res_count);
+                        res_count = 0;
+                    }
+                    cudaEvent_t c0 = T.mark();
+                    launch_verify(&d_hctl->survivors);
+                    cudaEvent_t c1 = T.mark();
+                    CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+                    CK(cudaStreamSynchronize(s));
+                    ms_verify += Timer::ms(c0, c1);
+                    res_count = h_ctl.results;
+                }
+                hb += processed;
+            }
+            CK(cudaStreamSynchronize(s));
+            st.ms_head_setup += Timer::ms(h0, h1);
+            st.head_pairs = hplan.pairs;
+            st.head_k = hplan.K;
+        }
         cudaEvent_t r0 = T.mark();
         launch_counters();
         cudaEvent_t r1 = T.mark();

@@ -51,6 +51,10 @@ struct EngineStats {
     double ms_upload = 0, ms_build = 0, ms_filter = 0, ms_rescan = 0, ms_verify = 0, ms_sort = 0,
            ms_download = 0;
     int filter_kernel = 0;
+    // K3a head-overlap phase (dense joins): region window pairs, survivors, head tokens, device ms
+    uint64_t head_pairs = 0, head_survivors = 0;
+    int head_k = 0;
+    double ms_head = 0, ms_head_setup = 0;
 };
 
 // Sorted result runs left in device memory (delivery mode 2): the streaming

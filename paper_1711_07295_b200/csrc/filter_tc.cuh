@@ -71,7 +71,19 @@ struct TcParams {
     int bias, bias2;           // added to every level-1 / level-2 accumulator by the operands'
                                // extension (non-negative accumulators: SWAR masks, masks16_nonneg)
     unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
+    uint32_t emit_col_end;     // level-2 GEMM: survivors with column j >= this are counted but
+                               // not emitted (the head-overlap kernel K3a covers them); ~0u: all
 };
+
+// Columns base_col + k < end of a 32-column group as a mask, natural bit order
+// (bit k = column k) or the masks16_nonneg order (PERM: bit k < 16 = column
+// 2k, bit 16 + k = column 2k + 1).
+template <bool PERM>
+__device__ __forceinline__ uint32_t cols_below(uint32_t end, uint32_t base_col) {
+    const int x = end > base_col ? static_cast<int>(min(end - base_col, 32u)) : 0;
+    if constexpr (PERM) return low_mask((x + 1) >> 1) | (low_mask(x >> 1) << 16);
+    else return low_mask(x);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -820,6 +832,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     }
                     // (without the level-2 GEMM, level-1 survivors are emitted and
                     // verify_pairs re-tests them against the level-2 sketch first)
+                    if constexpr (K2 > 0) e &= cols_below<false>(P.emit_col_end, gbase);
                     if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
                 };
                 bool groups_done = (P.debug & 1) != 0;
@@ -929,7 +942,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         }
                         m &= rm;  // (rm is all ones on the fast path, so the bit order is moot)
                         cnt += __popc(m);
-                        const uint32_t e = m & e2;
+                        uint32_t e = m & e2;
+                        if constexpr (K2 > 0)
+                            e &= perm ? cols_below<true>(P.emit_col_end, gbase) : cols_below<false>(P.emit_col_end, gbase);
                         if (__any_sync(0xFFFFFFFFu, e != 0)) {
                             if (perm) tc_emit<true>(e, gbase, i, q, qlen, P, lane);
                             else tc_emit(e, gbase, i, q, qlen, P, lane);

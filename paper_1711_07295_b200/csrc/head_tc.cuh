@@ -1,0 +1,437 @@
+// K3a: exact head-token overlaps on the tensor cores, for the dense region
+// of large records.  Included by engine.cu.
+//
+// Why.  For records of several hundred tokens and more, every b-bit Xor
+// sketch saturates: at tau = 0.7 the allowed Hamming distance of a pair with
+// |r|+|s| = 1000 is ~180 bits, more than a 256-bit sketch of two unrelated
+// records differs by.  On the ORKUT-shaped C4 these pairs are 8e9 of the 8.1e9
+// level-2 survivors, and merging them is 0.7 s of a 1 s join.
+//
+// What.  The K most frequent tokens of the region (its "head") get dense
+// indices; every region record becomes an exact K-bit head indicator h_r and
+// a tail count t_r = |r| - popcount(h_r).  For any pair
+//
+//     overlap(r, s) = <h_r, h_s> + |tail_r  ^  tail_s|  <=  <h_r, h_s> + min(t_r, t_s)
+//
+// and <h_r, h_s> is an exact int8 GEMM (operands 0/1, s32 accumulators).  A
+// pair whose bound is below the required overlap minov[|r|+|s|] cannot match
+// (the same integer threshold reference src/similarity.cpp:113-115 verifies
+// against, src/similarity.cpp:168-185); the rest are emitted as survivors and
+// verified exactly by K3 (verify_pairs).  The head is a property of the data,
+// not of a hash: the bound is exact for the head and loses only on the tail,
+// which for Zipf-like token laws is short where it matters.  Reference
+// counters are unaffected: they come from the level-1 b-bit filter (K2), which
+// still tests every window pair; K2 only stops EMITTING the pairs this kernel
+// covers (j >= L0, see TcParams::emit_col_end).
+//
+// Region: rows i >= L0 (records are size-sorted, so L0 = the first record with
+// |r| >= S0) and columns j in [max(L0, j0(i)), i).
+//
+// Layout.  The head operand is slice-major so one bulk copy moves a K-slice of
+// a whole tile: element (row r, k) of K at
+//     (((k / 128) * groups + (r - base) / 8) * 8 + (k % 128) / 16) * 128 + (r % 8) * 16 + k % 16
+// i.e. per K-slice of 128 bytes, 8-row core groups of 8 K-major 128-byte core
+// matrices (SBO = 1024 between groups, LBO = 128 between the two 16-byte K
+// halves of one kind::i8 instruction).
+//
+// Kernel: persistent, one CTA per SM, warp-specialised like K2:
+//   warp 0      bulk-copy producer: per 128 x 256 output tile, K/128 stages of
+//               (A slice 16 KB + B slice 32 KB) into a 4-stage ring
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma kind::i8 M=128 N=256
+//               K=32, 4 per stage, into 2 accumulator slots of 256 columns
+//   warps 2-17  epilogue: packed s16 TMEM loads, a per-group pre-test against
+//               the group's lowest threshold, exact per-pair test on the rare
+//               candidates, warp-queued emission of survivors (j, i)
+// Work items: (row tile, 4096-column chunk), ordered chunk-major so the SMs
+// working at once share one column chunk (its B operand stays in L2).
+#pragma once
+
+#include "filter_tc.cuh"
+
+namespace ssjb {
+namespace dev {
+
+constexpr int kHeadSliceK = 128;                       // K bytes per pipeline stage
+constexpr int kHeadNT = 256;                           // columns per MMA tile
+constexpr int kHeadStages = 4;
+constexpr int kHeadEpiWarps = 16;
+constexpr int kHeadThreads = 64 + 32 * kHeadEpiWarps;  // 576
+constexpr int kHeadA = kRowTile * kHeadSliceK;         // 16 KB
+constexpr int kHeadB = kHeadNT * kHeadSliceK;          // 32 KB
+constexpr int kHeadStage = kHeadA + kHeadB;
+constexpr int kHeadQueue = 128;                        // survivor staging per epilogue warp
+constexpr int kHeadSmem = kHeadStages * kHeadStage + kHeadEpiWarps * kHeadQueue * 8;
+constexpr int kHeadGroupBytes = 8 * kHeadSliceK;       // one 8-row core group of one slice (SBO)
+static_assert(kHeadSmem + 2048 <= 232448, "shared memory per CTA");
+
+struct HeadParams {
+    const uint8_t* op;          // head operand rows [base, base + 8 * groups), slice-major core layout
+    uint32_t base;              // first operand row (multiple of 8)
+    uint32_t groups;            // 8-row groups per slice
+    int kslices;                // K / kHeadSliceK
+    const uint32_t* info;       // (|r| << 16) | tail per operand row
+    const int32_t* minov;       // minov[|r| + |s|]
+    const uint32_t* wstart;     // j0 per record size
+    const uint2* items;         // (row tile, column chunk), chunk-major
+    const uint32_t* tile_col_lo;  // first (8-aligned) column of each row tile's window span
+    uint32_t tile0;             // first row of row tile 0 (multiple of 8, >= base)
+    uint32_t L0;                // first region record
+    uint32_t row_begin, row_end;  // this shard's rows
+    uint2* surv;
+    unsigned long long surv_cap, surv_soft;
+    unsigned long long item_begin, item_end;
+    Control* ctl;               // the head phase's own control block (survivors, work_next)
+};
+
+struct HeadItem {
+    uint32_t row0, c0, ntiles, done;
+};
+
+__device__ __forceinline__ void head_flush(uint2* q, int& qlen, const HeadParams& P, int lane) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(qlen));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    for (int k = lane; k < qlen; k += 32)
+        if (base + k < P.surv_cap) P.surv[base + k] = q[k];
+    qlen = 0;
+    __syncwarp();
+}
+
+// lane's survivors of a 32-column group (bit k = column base_col + k) into the warp queue
+__device__ __forceinline__ void head_emit(uint32_t m, uint32_t base_col, uint32_t row, uint2* q, int& qlen,
+                                          const HeadParams& P, int lane) {
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (total == 0) return;
+    if (qlen + total > kHeadQueue) head_flush(q, qlen, P, lane);
+    if (total > kHeadQueue) {  // (at most 32 x 32: straight to global memory)
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(total));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + (incl - c);
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            if (base < P.surv_cap) P.surv[base] = make_uint2(base_col + k, row);
+            ++base;
+        }
+        return;
+    }
+    int pos = qlen + incl - c;
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        q[pos++] = make_uint2(base_col + k, row);
+    }
+    qlen += total;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParams P) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sStage = smem;                                                        // [kHeadStages][A | B]
+    uint2* sQ = reinterpret_cast<uint2*>(smem + kHeadStages * kHeadStage);         // [16][kHeadQueue]
+    __shared__ __align__(8) uint64_t item_full[2], item_empty[2];
+    __shared__ __align__(8) uint64_t s_full[kHeadStages], s_empty[kHeadStages], acc_full[2], acc_empty[2];
+    __shared__ HeadItem items[2];
+    __shared__ uint32_t tmem_base_sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t kTmemCols = 2 * kHeadNT;
+
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&item_full[s], 1);
+            mbar_init(&item_empty[s], 1 + kHeadEpiWarps);
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], kHeadEpiWarps);
+        }
+        for (int s = 0; s < kHeadStages; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem_base = tmem_base_sh;
+    const uint64_t slice_stride = static_cast<uint64_t>(P.groups) * kHeadGroupBytes;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t iseq = 0, sseq = 0;
+            for (;;) {
+                const int slot = iseq & 1;
+                mbar_spin(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
+                const unsigned long long it = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
+                HeadItem info{};
+                if (it >= P.item_end) {
+                    info.done = 1;
+                    items[slot] = info;
+                    mbar_arrive(&item_full[slot]);
+                    break;
+                }
+                const uint2 w = P.items[it];  // (row tile, column chunk)
+                const uint32_t row0 = P.tile0 + w.x * kRowTile;
+                const uint32_t rmax = min(row0 + kRowTile, P.row_end);  // columns j < i < rmax
+                const uint32_t chunk0 = P.base + w.y * kColChunk;
+                info.row0 = row0;
+                info.c0 = max(P.tile_col_lo[w.x], chunk0);
+                const uint32_t c1 = min(chunk0 + kColChunk, rmax > 0 ? rmax - 1 : 0);
+                info.ntiles = c1 > info.c0 ? (c1 - info.c0 + kHeadNT - 1) / kHeadNT : 0;
+                info.done = 0;
+                items[slot] = info;
+                mbar_arrive(&item_full[slot]);
+                const uint8_t* a_src = P.op + static_cast<uint64_t>((row0 - P.base) >> 3) * kHeadGroupBytes;
+                for (uint32_t t = 0; t < info.ntiles; ++t) {
+                    const uint8_t* b_src =
+                        P.op + static_cast<uint64_t>((info.c0 + t * kHeadNT - P.base) >> 3) * kHeadGroupBytes;
+                    for (int s = 0; s < P.kslices; ++s, ++sseq) {
+                        const int st = sseq % kHeadStages;
+                        mbar_spin(&s_empty[st], ((sseq / kHeadStages) & 1) ^ 1);
+                        uint8_t* dst = sStage + st * kHeadStage;
+                        mbar_expect_tx(&s_full[st], kHeadStage);
+                        tma_load_1d(dst, a_src + s * slice_stride, kHeadA, &s_full[st]);
+                        tma_load_1d(dst + kHeadA, b_src + s * slice_stride, kHeadB, &s_full[st]);
+                    }
+                }
+                ++iseq;
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t iseq = 0, sseq = 0, aseq = 0;
+            for (;;) {
+                const int slot = iseq & 1;
+                mbar_spin(&item_full[slot], (iseq >> 1) & 1);
+                const HeadItem info = items[slot];
+                mbar_arrive(&item_empty[slot]);
+                if (info.done) break;
+                for (uint32_t t = 0; t < info.ntiles; ++t, ++aseq) {
+                    const int as = aseq & 1;
+                    mbar_spin(&acc_empty[as], ((aseq >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t d = tmem_base + as * kHeadNT;
+                    for (int s = 0; s < P.kslices; ++s, ++sseq) {
+                        const int st = sseq % kHeadStages;
+                        mbar_spin(&s_full[st], (sseq / kHeadStages) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t a0 = smem_u32(sStage + st * kHeadStage);
+                        const uint32_t b0 = a0 + kHeadA;
+#pragma unroll
+                        for (int k = 0; k < kHeadSliceK / 32; ++k)
+                            umma_i8<kHeadNT>(d, umma_desc(a0 + k * 256, kHeadGroupBytes),
+                                             umma_desc(b0 + k * 256, kHeadGroupBytes), (s | k) != 0);
+                        umma_commit(&s_empty[st]);
+                    }
+                    umma_commit(&acc_full[as]);
+                }
+                ++iseq;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int ew = warp - 2;
+        const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (hardware rule)
+        const int part = ew >> 2;      // 64-column quarter of each tile
+        const int rit = quarter * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+        uint2* q = sQ + ew * kHeadQueue;
+        int qlen = 0;
+        uint32_t iseq = 0, aseq = 0;
+        for (;;) {
+            const int slot = iseq & 1;
+            mbar_wait(&item_full[slot], (iseq >> 1) & 1);
+            const HeadItem info = items[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&item_empty[slot]);
+            if (info.done) break;
+            const uint32_t i = info.row0 + rit;
+            const bool valid = i >= max(P.L0, P.row_begin) && i < P.row_end;
+            uint32_t si = 0, ti = 0, lo_i = 0, hi_i = 0;
+            if (valid) {
+                const uint32_t inf = P.info[i - P.base];
+                si = inf >> 16;
+                ti = inf & 0xFFFFu;
+                lo_i = max(P.L0, P.wstart[si]);
+                hi_i = i;
+            }
+            for (uint32_t t = 0; t < info.ntiles; ++t, ++aseq) {
+                const int as = aseq & 1;
+                const uint32_t gcol = info.c0 + t * kHeadNT + part * 64;  // warp's first column
+                // sizes of the warp's two 32-column groups' first columns (pre-test thresholds)
+                const uint32_t f0 = __ldg(P.info + (gcol - P.base));
+                const uint32_t f1 = __ldg(P.info + (gcol + 32 - P.base));
+                mbar_wait(&acc_full[as], (aseq >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                uint32_t d[32];
+                tmem_ld64_pack16(tmem_base + lane_base + as * kHeadNT + part * 64, d);
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[as]);  // accumulators are in registers
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    const uint32_t gbase = gcol + 32 * g;
+                    const uint32_t rm = valid ? (low_mask(static_cast<int>(hi_i) - static_cast<int>(gbase)) &
+                                                 ~low_mask(static_cast<int>(lo_i) - static_cast<int>(gbase)))
+                                              : 0u;
+                    // the group's columns are size-sorted: minov[si + first size] - ti is
+                    // a lower bound of every column's threshold minov[si+sj] - min(ti,tj)
+                    const uint32_t sfirst = (g ? f1 : f0) >> 16;
+                    const int thr = valid ? __ldg(P.minov + si + sfirst) - static_cast<int>(ti) : 0;
+                    uint32_t dg[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) dg[k] = d[16 * g + k];
+                    const uint32_t cand = rm ? rm & mask16_32(dg, min(max(thr - 1, -32768), 32767)) : 0u;
+                    uint32_t e = 0;
+                    if (cand) {  // rare: exact per-pair test of the pre-test's candidates
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) {
+                            if (!((cand >> k) & 1u)) continue;
+                            const uint32_t inf = __ldg(P.info + (gbase + k - P.base));
+                            const int need = __ldg(P.minov + si + (inf >> 16));
+                            const int acc = static_cast<int>((dg[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+                            if (acc + static_cast<int>(min(ti, inf & 0xFFFFu)) >= need) e |= 1u << k;
+                        }
+                    }
+                    if (__any_sync(0xFFFFFFFFu, e != 0)) head_emit(e, gbase, i, q, qlen, P, lane);
+                }
+            }
+            ++iseq;
+        }
+        if (qlen) head_flush(q, qlen, P, lane);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+}
+
+// ---------------------------------------------------------------- head setup
+// Token counts over the region's records [L0, n): cnt[t] += 1 per occurrence.
+__global__ void head_count(const uint32_t* tokens, uint64_t t0, uint64_t t1, uint32_t* cnt) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = t0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < t1; k += stride)
+        atomicAdd(cnt + tokens[k], 1u);
+}
+
+// Count-of-counts for the head selection: hist[min(c, 65535)] over tokens with c >= 2
+// (a token in one region record cannot contribute to any pair's overlap).
+__global__ void head_hist(const uint32_t* cnt, uint32_t universe, uint32_t* hist) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < universe; t += stride) {
+        const uint32_t c = cnt[t];
+        if (c >= 2) atomicAdd(hist + min(c, 65535u), 1u);
+    }
+}
+
+// One block of 1024 threads: the smallest count c* >= 2 such that at most K
+// tokens have count >= c* (out[0]).  hist has 65536 buckets; chunk t of 64
+// buckets is summed by thread t, then thread 0 scans from the top.
+__global__ void __launch_bounds__(1024) head_threshold(const uint32_t* hist, uint32_t K, uint32_t* out) {
+    __shared__ uint32_t part[1024];
+    const int t = threadIdx.x;
+    uint32_t s = 0;
+    for (int k = 0; k < 64; ++k) s += hist[t * 64 + k];
+    part[t] = s;
+    __syncthreads();
+    if (t != 0) return;
+    uint32_t acc = 0, thr = 2;
+    for (int c = 1023; c >= 0; --c) {
+        if (acc + part[c] <= K) {
+            acc += part[c];
+            continue;
+        }
+        for (int k = 63; k >= 0; --k) {  // the cut lies in this chunk
+            const uint32_t h = hist[c * 64 + k];
+            if (acc + h > K) {
+                thr = static_cast<uint32_t>(c * 64 + k + 1);
+                break;
+            }
+            acc += h;
+        }
+        break;
+    }
+    out[0] = thr < 2 ? 2u : thr;
+}
+
+// Dense head indices for tokens with count >= c* (order is immaterial: any
+// token set gives an exact bound); map[t] = index or 0xFFFF.
+__global__ void head_assign(const uint32_t* cnt, uint32_t universe, const uint32_t* thr, uint32_t K,
+                            uint16_t* map, uint32_t* next) {
+    const uint32_t c0 = thr[0];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < universe; t += stride) {
+        const bool take = cnt[t] >= c0;
+        const uint32_t bal = __ballot_sync(__activemask(), take);
+        if (!take) continue;
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(bal) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(next, static_cast<uint32_t>(__popc(bal)));
+        base = __shfl_sync(bal, base, leader) + __popc(bal & ((1u << lane) - 1u));
+        map[t] = base < K ? static_cast<uint16_t>(base) : static_cast<uint16_t>(0xFFFFu);
+    }
+}
+
+// One CTA per 8-row core group of operand rows [base + 8g, +8): the K-byte
+// head indicator rows (0/1) in the slice-major core layout, and info[] =
+// (|r| << 16) | tail.  Rows outside [L0, n) stay zero (size 0).
+__global__ void __launch_bounds__(256) head_expand(const uint32_t* tokens, const uint64_t* offsets, uint32_t n,
+                                                   uint32_t L0, uint32_t base, uint32_t groups, int K,
+                                                   const uint16_t* map, uint8_t* op, uint32_t* info) {
+    extern __shared__ __align__(16) uint8_t rowbuf[];  // [8][K]
+    __shared__ uint32_t heads[8];
+    const uint32_t g = blockIdx.x;
+    uint4* z = reinterpret_cast<uint4*>(rowbuf);
+    for (int k = threadIdx.x; k < 8 * K / 16; k += blockDim.x) z[k] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 8) heads[threadIdx.x] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t r = base + 8 * g + warp;  // one warp per row
+    uint32_t size = 0;
+    if (r >= L0 && r < n) {
+        const uint64_t b = offsets[r], e = offsets[r + 1];
+        size = static_cast<uint32_t>(e - b);
+        uint32_t h = 0;
+        for (uint64_t k = b + lane; k < e; k += 32) {
+            const uint16_t m = map[tokens[k]];
+            if (m != 0xFFFFu) {
+                rowbuf[warp * K + m] = 1;
+                ++h;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+        if (lane == 0) heads[warp] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        const uint32_t rr = base + 8 * g + threadIdx.x;
+        const uint32_t sz = (rr >= L0 && rr < n) ? static_cast<uint32_t>(offsets[rr + 1] - offsets[rr]) : 0u;
+        info[8 * g + threadIdx.x] = (sz << 16) | (sz - heads[threadIdx.x]);
+    }
+    (void)size;
+    // 16-byte units: unit u -> (slice s, chunk c, row q): u = (s * 8 + c) * 8 + q
+    const int units = K / 16 * 8;
+    for (int u = threadIdx.x; u < units; u += blockDim.x) {
+        const int q = u & 7, c = (u >> 3) & 7, s = u >> 6;
+        const uint4 v = *reinterpret_cast<const uint4*>(rowbuf + q * K + s * kHeadSliceK + c * 16);
+        const uint64_t off = ((static_cast<uint64_t>(s) * groups + g) * 8 + c) * 128 + q * 16;
+        *reinterpret_cast<uint4*>(op + off) = v;
+    }
+}
+
+}  // namespace dev
+}  // namespace ssjb

@@ -54,15 +54,19 @@ def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
         assert sha(store) == e["sha256"], e
 
 
-FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "tc-i8-1tile", "tc-i8-noext", "popc", "tc-l2gemm"]
+FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "tc-i8-1tile", "tc-i8-noext", "popc", "tc-l2gemm", "tc-head"]
 
 
 def set_filter(monkeypatch, flavour):
     """tcgen05 fp4 / int8 CTA-pair / int8 single-CTA with two row tiles per column
     tile (default) or one (with the popcount extension block, or K = b) /
-    level-2 GEMM, or POPC."""
+    level-2 GEMM, or POPC; tc-head: the level-2 GEMM with the head-overlap
+    kernel (K3a) forced over every record of >= 3 tokens with a 128-token head."""
     monkeypatch.setenv("SSJB_FILTER", "popc" if flavour == "popc" else "tc")
-    monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour == "tc-l2gemm" else "0")
+    monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour in ("tc-l2gemm", "tc-head") else "0")
+    monkeypatch.setenv("SSJB_HEAD", "2" if flavour == "tc-head" else "0")
+    monkeypatch.setenv("SSJB_HEAD_MIN_SIZE", "3")
+    monkeypatch.setenv("SSJB_HEAD_K", "128")
     monkeypatch.setenv("SSJB_TC_KIND", "i8" if flavour.startswith("tc-i8") else "fp4")
     monkeypatch.setenv("SSJB_TC2", "1" if flavour == "tc-i8-pair" else "0")
     monkeypatch.setenv("SSJB_NOEXT", "1" if flavour == "tc-i8-noext" else "0")
