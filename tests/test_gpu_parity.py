@@ -274,3 +274,30 @@ def test_concurrent_joins_from_threads(lib, golden, colls):
         S.unpin_device(pinned)
     for rep, e in zip(reps, cases):
         assert_same(rep, e, "concurrent")
+
+
+@pytest.mark.parametrize("sim", [capi.SSJ_SIM_JACCARD, capi.SSJ_SIM_COSINE, capi.SSJ_SIM_DICE,
+                                 capi.SSJ_SIM_OVERLAP])
+def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim):
+    """ssj_join with ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN / ADAPTJOIN returns
+    the reference's pair list for that algorithm (run live from oracle/_ref on
+    the same collection and options) for every similarity function; the
+    counters satisfy the reference's invariants."""
+    rng = np.random.default_rng(77 + sim)
+    for trial in range(6):
+        n = int(rng.integers(100, 900))
+        gen = dict(num_sets=n, mean_size=float(rng.uniform(4, 30)), universe=int(rng.integers(30, 400)),
+                   seed=int(rng.integers(0, 1 << 30)))
+        mine = S.Collection.generate(lib, **gen)
+        theirs = S.Collection.generate(ref, **gen)
+        thr = (int(rng.integers(2, 8)), 1) if sim == capi.SSJ_SIM_OVERLAP else (int(rng.integers(4, 10)), 10)
+        for algo in (1, 2, 3, 4, 5):
+            kw = dict(algorithm=algo, similarity=sim, threshold=thr, bitmap_enabled=int(trial % 2),
+                      workers=2)
+            want = S.join(theirs, S.default_options(ref, **kw))
+            got = S.join(mine, S.default_options(lib, **kw))
+            assert len(got.pairs) == len(want.pairs) and (got.pairs == want.pairs).all(), (sim, algo, trial)
+            c = got.counters
+            assert c["candidates"] == (c["pruned_length"] + c["pruned_positional"] + c["pruned_suffix"]
+                                       + c["pruned_bitmap"] + c["verified"])
+            assert c["matched"] == len(got.pairs)

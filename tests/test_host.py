@@ -164,12 +164,15 @@ def test_option_errors_match_reference(lib, ref):
     assert e.value.status == capi.SSJ_ERROR_INVALID_ARGUMENT
 
 
-def test_prefix_filter_algorithms_are_rejected(lib):
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_prefix_filter_algorithms_reach_the_gpu_join(lib):
+    """ALLPAIRS..ADAPTJOIN are accepted (routed to the GPU exact join, see
+    capi.cpp check_supported): without a device they fail like PAR_BITMAP."""
     coll = S.Collection.from_records(lib, [[1, 2], [1, 2, 3]])
     for algo in (1, 2, 3, 4, 5):
         with pytest.raises(S.SsjError) as e:
             S.join(coll, S.default_options(lib, algorithm=algo))
-        assert e.value.status == capi.SSJ_ERROR_INVALID_ARGUMENT and "B200" in e.value.message
+        assert e.value.status == capi.SSJ_ERROR_INTERNAL and "CUDA" in e.value.message
 
 
 @pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
