@@ -1127,9 +1127,10 @@ struct Tiling {
     std::vector<uint64_t> item_base;  // ntiles + 1
     std::vector<uint32_t> col_lo;     // ntiles
     std::vector<uint32_t> item_tile;  // tile of each work item
+    std::vector<uint32_t> order;      // claim order -> item id (column-chunk-major), empty: identity
 };
 
-Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows) {
+Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows, bool ordered = false) {
     Tiling t;
     t.tile_rows = tile_rows;
     const size_t rows = plan.row_end - plan.row_begin;
@@ -1150,7 +1151,34 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
     for (uint32_t k = 0; k < t.ntiles; ++k)
         std::fill(t.item_tile.begin() + static_cast<ptrdiff_t>(t.item_base[k]),
                   t.item_tile.begin() + static_cast<ptrdiff_t>(t.item_base[k + 1]), k);
+    if (ordered && !t.item_tile.empty()) {
+        // claim order: items by the 4096-column bucket of their first column
+        // (counting sort, stable in tile order), so the CTAs working at once
+        // stream the same column operands from L2
+        const size_t nb = c.size() / dev::kColChunk + 2;
+        std::vector<uint64_t> at(nb + 1, 0);
+        auto bucket = [&](uint32_t k, uint64_t item) {
+            return std::min<size_t>(nb - 1, (t.col_lo[k] + (item - t.item_base[k]) * dev::kColChunk) / dev::kColChunk);
+        };
+        for (uint32_t k = 0; k < t.ntiles; ++k)
+            for (uint64_t it = t.item_base[k]; it < t.item_base[k + 1]; ++it) ++at[bucket(k, it) + 1];
+        for (size_t b = 0; b < nb; ++b) at[b + 1] += at[b];
+        t.order.resize(t.item_tile.size());
+        for (uint32_t k = 0; k < t.ntiles; ++k)
+            for (uint64_t it = t.item_base[k]; it < t.item_base[k + 1]; ++it)
+                t.order[at[bucket(k, it)]++] = static_cast<uint32_t>(it);
+    }
     return t;
+}
+
+// Zeroes the per-(item, row) survivor counts of the items at claim positions
+// [k0, k1) of a column-chunk-major order (the items a batch has not processed).
+__global__ void zero_item_counts(const uint32_t* order, uint64_t k0, uint64_t k1, uint32_t* counts,
+                                 uint32_t tile_rows) {
+    const uint64_t total = (k1 - k0) * tile_rows;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total; x += stride)
+        counts[static_cast<uint64_t>(order[k0 + x / tile_rows]) * tile_rows + x % tile_rows] = 0;
 }
 
 // ------------------------------------------------------------ K3a head plan
@@ -1163,7 +1191,9 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
 struct HeadPlan {
     bool ok = false;
     uint32_t S0 = 0, L0 = 0, base = 0, tile0 = 0, ntiles = 0, rows_pad = 0;
-    int K = 0;
+    int K = 0;                          // head tokens (GEMM depth in elements)
+    int kind = dev::kKindF4;            // operand kind: kKindF4 (mxf4, K/2 bytes per row) or kKindI8
+    int row_bytes() const { return kind == dev::kKindF4 ? K / 2 : K; }
     uint64_t pairs = 0;                 // region window pairs (the kernel's algorithmic work)
     std::vector<uint32_t> tile_col_lo;  // per row tile
     std::vector<uint2> items;           // (row tile, column chunk), chunk-major
@@ -1176,8 +1206,12 @@ HeadPlan make_head_plan(const Collection& c, const JoinPlan& plan, int W2) {
     if (!mode || W2 != 4 || plan.naive || plan.cosine || !plan.bitmap.enabled || plan.row_end <= plan.row_begin ||
         c.max_size >= 65536 || c.universe > (uint64_t(1) << 28) || n >= (size_t(1) << 31))
         return h;
-    h.K = static_cast<int>(std::min<uint64_t>(4096, env_u64("SSJB_HEAD_K", 2048))) & ~(dev::kHeadSliceK - 1);
-    if (h.K < dev::kHeadSliceK) return h;
+    const char* kenv = std::getenv("SSJB_HEAD_KIND");
+    h.kind = kenv && std::string(kenv) == "i8" ? dev::kKindI8 : dev::kKindF4;
+    // K: a multiple of one 128-byte pipeline slice (128 int8 / 256 e2m1 elements)
+    const int kq = h.kind == dev::kKindF4 ? 2 * dev::kHeadSliceK : dev::kHeadSliceK;
+    h.K = static_cast<int>(std::min<uint64_t>(4096, env_u64("SSJB_HEAD_K", 4096))) / kq * kq;
+    if (h.K < kq) return h;
     // S0: the smallest size at which two records of that size may differ in
     // 64 sketch bits (maxham(2s) >= 64): from there on the 256-bit level-2
     // sketch stops pruning
@@ -1246,14 +1280,21 @@ HeadDev head_setup(const DeviceReplica& rep, const Collection& c, const HeadPlan
     CK(cudaMemsetAsync(thr, 0, 8, s));
     CK(cudaMemsetAsync(map, 0xFF, size_t(U) * 2, s));
     const unsigned g = static_cast<unsigned>(sms) * 8;
-    dev::head_count<<<g, 256, 0, s>>>(rep.tokens, c.offsets[h.L0], c.offsets[n], cnt);
+    // sample: about 2^24 region tokens (every stride-th region record)
+    const uint64_t region_tokens = c.offsets[n] - c.offsets[h.L0];
+    const uint32_t stride = static_cast<uint32_t>(std::max<uint64_t>(1, region_tokens >> 24));
+    dev::head_count<<<g, 256, 0, s>>>(rep.tokens, rep.offsets, h.L0, n, stride, cnt);
     dev::head_hist<<<g, 256, 0, s>>>(cnt, U, hist);
     dev::head_threshold<<<1, 1024, 0, s>>>(hist, static_cast<uint32_t>(h.K), thr);
     dev::head_assign<<<g, 256, 0, s>>>(cnt, U, thr, static_cast<uint32_t>(h.K), map, thr + 1);
-    d.op = A.alloc<uint8_t>(size_t(h.rows_pad) * h.K);
+    d.op = A.alloc<uint8_t>(size_t(h.rows_pad) * h.row_bytes());
     d.info = A.alloc<uint32_t>(h.rows_pad);
-    dev::head_expand<<<h.rows_pad / 8, 256, 8 * h.K, s>>>(rep.tokens, rep.offsets, n, h.L0, h.base, h.rows_pad / 8,
-                                                         h.K, map, d.op, d.info);
+    if (h.kind == dev::kKindF4)
+        dev::head_expand<dev::kKindF4><<<h.rows_pad / 8, 256, 8 * h.row_bytes(), s>>>(
+            rep.tokens, rep.offsets, n, h.L0, h.base, h.rows_pad / 8, h.K, map, d.op, d.info);
+    else
+        dev::head_expand<dev::kKindI8><<<h.rows_pad / 8, 256, 8 * h.row_bytes(), s>>>(
+            rep.tokens, rep.offsets, n, h.L0, h.base, h.rows_pad / 8, h.K, map, d.op, d.info);
     launches += 5;
     CK(cudaGetLastError());
     d.items = A.alloc<uint2>(h.items.size());
@@ -1783,11 +1824,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint64_t* d_item_base = nullptr;
     uint32_t* d_col_lo = nullptr;
     uint32_t* d_item_tile = nullptr;
+    uint32_t* d_item_order = nullptr;
+    // column-chunk-major claim order for collections whose operands exceed L2
+    // (tcgen05 single-CTA kernels; per-chunk streamed filter launches keep item order)
+    const bool item_ordered = use_tc && !use_tc2 && n >= env_u64("SSJB_ORDER_MIN_ROWS", 262144) &&
+                              env_u64("SSJB_STREAM", 1) < 2 && env_u64("SSJB_ITEM_ORDER", 1) != 0;
     auto set_tiling = [&](uint32_t tile_rows) {
-        tl = make_tiling(c, plan, tile_rows);
+        tl = make_tiling(c, plan, tile_rows, item_ordered);
         stage.add(&d_item_base, tl.item_base.data(), tl.item_base.size() * 8);
         stage.add(&d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4);
         stage.add(&d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4);
+        if (!tl.order.empty()) stage.add(&d_item_order, tl.order.data(), tl.order.size() * 4);
         stage.flush(A, s, st.h2d_bytes);
     };
     set_tiling(use_tc2 || use_tcm ? 2 * dev::kRowTile : dev::kRowTile);
@@ -2026,6 +2073,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.wstart = d_wstart;
         TP.item_base = d_item_base;
         TP.item_tile = d_item_tile;
+        TP.item_order = item_ordered ? d_item_order : nullptr;
         TP.tile_col_lo = d_col_lo;
         TP.surv = d_surv;
         TP.rowcnt = d_rowcnt;
@@ -2359,6 +2407,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                     total_items = n_items = tl.item_base.back();
                     TP.item_base = d_item_base;
                     TP.item_tile = d_item_tile;
+                    TP.item_order = item_ordered ? d_item_order : nullptr;
                     TP.tile_col_lo = d_col_lo;
                     TP.ntiles = tl.ntiles;
                     if (d_item_counts && n_items * tl.tile_rows * 4 <= ic_bytes) {
@@ -2428,12 +2477,25 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         uint64_t soft = std::max<uint64_t>(surv_cap / 2, 1);
         uint64_t span = total_items;  // items per launch (halved only if the soft cap cannot help)
         uint64_t ib = resume_item;
-        if (d_item_counts && total_items > ib)
-            CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (total_items - ib) * tl.tile_rows * 4, s));
+        const bool ordered = use_tc && TP.item_order != nullptr;
+        // the counts of the items a batch has not processed: claim positions [k0, total)
+        auto zero_unprocessed = [&](uint64_t k0) {
+            if (!d_item_counts || total_items <= k0) return;
+            if (ordered) {
+                const uint64_t cnt = (total_items - k0) * tl.tile_rows;
+                zero_item_counts<<<static_cast<unsigned>(std::min<uint64_t>((cnt + 255) / 256, uint64_t(sms) * 16)), 256,
+                                   0, s>>>(TP.item_order, k0, total_items, d_item_counts, tl.tile_rows);
+                ++st.launches;
+                CK(cudaGetLastError());
+            } else {
+                CK(cudaMemsetAsync(d_item_counts + k0 * tl.tile_rows, 0, (total_items - k0) * tl.tile_rows * 4, s));
+            }
+        };
+        zero_unprocessed(ib);
         while (ib < total_items) {
             const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
                                                       tl.item_base.begin() - 1);
-            const uint32_t rb = tb * tl.tile_rows;  // rows this launch may touch: [rb, rows)
+            const uint32_t rb = ordered ? 0u : tb * tl.tile_rows;  // rows this launch may touch: [rb, rows)
             CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (rows - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
             FP.surv_soft = soft;
             TP.surv_soft = soft;
@@ -2450,8 +2512,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 // the last claims overshot the margin: roll back this launch's
                 // row and item counts, retry with a lower cap
                 CK(cudaMemcpyAsync(d_rowcnt + rb, d_rowsnap + rb, (rows - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
-                if (d_item_counts)
-                    CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (total_items - ib) * tl.tile_rows * 4, s));
+                zero_unprocessed(ib);
                 if (soft > 1) soft = std::max<uint64_t>(soft / 4, 1);
                 else span = std::max<uint64_t>(1, std::min(span, processed) / 2);  // kernels without the soft cap
                 continue;
@@ -2485,7 +2546,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             HP.op = hd.op;
             HP.base = hplan.base;
             HP.groups = hplan.rows_pad / 8;
-            HP.kslices = hplan.K / dev::kHeadSliceK;
+            HP.kslices = hplan.row_bytes() / dev::kHeadSliceK;
             HP.info = hd.info;
             HP.minov = d_minov;
             HP.wstart = d_wstart;
@@ -2498,20 +2559,28 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             HP.surv = d_surv;
             HP.surv_cap = surv_cap;
             HP.ctl = d_hctl;
-            set_smem_once(reinterpret_cast<const void*>(dev::head_overlap_kernel), dev::kHeadSmem);
+            using HL8 = dev::HeadLayout<dev::kKindI8>;
+            using HL4 = dev::HeadLayout<dev::kKindF4>;
+            const bool hf4 = hplan.kind == dev::kKindF4;
+            const void* hfn = hf4 ? reinterpret_cast<const void*>(dev::head_overlap_kernel<dev::kKindF4>)
+                                  : reinterpret_cast<const void*>(dev::head_overlap_kernel<dev::kKindI8>);
+            set_smem_once(hfn, hf4 ? HL4::kSmem : HL8::kSmem);
             cudaEvent_t h1 = T.mark();
             const uint64_t hitems = hplan.items.size();
             uint64_t hsoft = std::max<uint64_t>(surv_cap / 2, 1);
+            uint64_t hspan = hitems;  // items per launch: halved when even a soft cap of 1 overshoots
             uint64_t hb = 0;
             dev::Control hc{};
             while (hb < hitems) {
                 CK(cudaMemsetAsync(d_hctl, 0, sizeof(dev::Control), s));
+                const uint64_t he = std::min(hitems, hb + hspan);
                 HP.item_begin = hb;
-                HP.item_end = hitems;
+                HP.item_end = he;
                 HP.surv_soft = hsoft;
                 cudaEvent_t a = T.mark();
-                dev::head_overlap_kernel<<<static_cast<unsigned>(std::min<uint64_t>(hitems - hb, sms)),
-                                           dev::kHeadThreads, dev::kHeadSmem, s>>>(HP);
+                const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>(he - hb, sms));
+                if (hf4) dev::head_overlap_kernel<dev::kKindF4><<<hgrid, HL4::kThreads, HL4::kSmem, s>>>(HP);
+                else dev::head_overlap_kernel<dev::kKindI8><<<hgrid, HL8::kThreads, HL8::kSmem, s>>>(HP);
                 ++st.launches;
                 CK(cudaGetLastError());
                 cudaEvent_t b = T.mark();
@@ -2519,9 +2588,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 CK(cudaStreamSynchronize(s));
                 st.ms_head += Timer::ms(a, b);
                 const uint64_t S = hc.survivors;
-                const uint64_t processed = std::min<uint64_t>(hc.work_next, hitems - hb);
-                if (S > surv_cap) {  // overshoot: nothing was counted, redo with a lower cap
-                    hsoft = std::max<uint64_t>(hsoft / 4, 1);
+                const uint64_t processed = std::min<uint64_t>(hc.work_next, he - hb);
+                if (S > surv_cap) {  // overshoot: nothing was counted; redo with a lower cap / fewer items
+                    if (hsoft > 1) hsoft = std::max<uint64_t>(hsoft / 4, 1);
+                    else hspan = std::max<uint64_t>(1, std::min(hspan, std::max<uint64_t>(processed, 2)) / 2);
                     continue;
                 }
                 st.head_survivors += S;

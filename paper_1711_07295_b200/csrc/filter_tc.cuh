@@ -73,7 +73,21 @@ struct TcParams {
     unsigned long long* trace; // CTA 0 event timestamps (pipeline probe), or null
     uint32_t emit_col_end;     // level-2 GEMM: survivors with column j >= this are counted but
                                // not emitted (the head-overlap kernel K3a covers them); ~0u: all
+    const uint32_t* item_order;  // claim index -> work item id (column-chunk-major), or null: identity
 };
+
+constexpr unsigned long long kNoItem = ~0ull;
+
+// Next work item of a persistent tcgen05 filter: the claim index (prefix
+// semantics of claim_item) mapped through P.item_order to an item id, or
+// kNoItem when the launch has none left.  The column-chunk-major order makes
+// the CTAs working at once read the same column operands, which then stay in
+// L2 instead of being re-read from HBM by every row tile of a wide window.
+__device__ __forceinline__ unsigned long long claim_tc(const TcParams& P) {
+    const unsigned long long k = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
+    if (k >= P.item_end) return kNoItem;
+    return P.item_order ? static_cast<unsigned long long>(P.item_order[k]) : k;
+}
 
 // Columns base_col + k < end of a 32-column group as a mask, natural bit order
 // (bit k = column k) or the masks16_nonneg order (PERM: bit k < 16 = column
@@ -617,15 +631,15 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             uint32_t iseq = 0, tseq = 0;
             // the next work item is claimed and looked up while the current one's
             // column tiles are still streaming (hides the atomic + table latency)
-            unsigned long long nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
-            uint32_t nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+            unsigned long long nxt = claim_tc(P);
+            uint32_t nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
             for (;;) {
                 const int slot = iseq & 1;
                 mbar_spin(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
                 const unsigned long long it = nxt;
                 TcItem info{};
                 info.item = it;
-                if (it >= P.item_end) {
+                if (it == kNoItem) {
                     info.done = 1;
                     items[slot] = info;
                     mbar_arrive(&item_full[slot]);
@@ -664,13 +678,13 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     mbar_expect_tx(&b_full[st], L::kB);
                     tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
                     if (t == 0) {
-                        nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
-                        nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+                        nxt = claim_tc(P);
+                        nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
                     }
                 }
                 if (info.ntiles == 0) {
-                    nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
-                    nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+                    nxt = claim_tc(P);
+                    nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
                 }
                 ++iseq;
             }

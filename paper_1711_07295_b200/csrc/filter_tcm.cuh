@@ -157,15 +157,15 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             uint32_t iseq = 0, tseq = 0;
-            unsigned long long nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
-            uint32_t nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+            unsigned long long nxt = claim_tc(P);
+            uint32_t nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
             for (;;) {
                 const int slot = iseq & 1;
                 mbar_spin(&item_empty[slot], ((iseq >> 1) & 1) ^ 1);
                 const unsigned long long it = nxt;
                 TcItem info{};
                 info.item = it;
-                if (it >= P.item_end) {
+                if (it == kNoItem) {
                     info.done = 1;
                     items[slot] = info;
                     mbar_arrive(&item_full[slot]);
@@ -187,8 +187,8 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                 tma_load_1d(sA + aslot * 2 * L::kA, P.opA + static_cast<uint64_t>(row0) * L::kRow, 2 * L::kA,
                             &a_full[aslot]);
                 mbar_arrive(&item_full[slot]);
-                nxt = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
-                nxt_tile = nxt < P.item_end ? P.item_tile[nxt] : 0u;
+                nxt = claim_tc(P);
+                nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);

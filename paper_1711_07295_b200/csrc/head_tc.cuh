@@ -52,17 +52,28 @@ namespace ssjb {
 namespace dev {
 
 constexpr int kHeadSliceK = 128;                       // K bytes per pipeline stage
-constexpr int kHeadNT = 256;                           // columns per MMA tile
 constexpr int kHeadStages = 4;
-constexpr int kHeadEpiWarps = 16;
-constexpr int kHeadThreads = 64 + 32 * kHeadEpiWarps;  // 576
-constexpr int kHeadA = kRowTile * kHeadSliceK;         // 16 KB
-constexpr int kHeadB = kHeadNT * kHeadSliceK;          // 32 KB
-constexpr int kHeadStage = kHeadA + kHeadB;
 constexpr int kHeadQueue = 128;                        // survivor staging per epilogue warp
-constexpr int kHeadSmem = kHeadStages * kHeadStage + kHeadEpiWarps * kHeadQueue * 8;
 constexpr int kHeadGroupBytes = 8 * kHeadSliceK;       // one 8-row core group of one slice (SBO)
-static_assert(kHeadSmem + 2048 <= 232448, "shared memory per CTA");
+
+// Per operand kind: int8 (0/1 bytes, s32 accumulators, N = 256, two slots =
+// all 512 TMEM columns) or mxf4 (packed e2m1 1.0 codes, unit block scales,
+// f32 accumulators, twice the elements per byte and per instruction; N = 192
+// so two slots leave TMEM room for the scale factors).
+template <int KIND>
+struct HeadLayout {
+    static constexpr int NT = KIND == kKindF4 ? 192 : 256;   // columns per MMA tile
+    static constexpr int kEpiWarps = NT / 16;                // 64 columns x 32 rows each
+    static constexpr int kThreads = 64 + 32 * kEpiWarps;
+    static constexpr int kA = kRowTile * kHeadSliceK;         // 16 KB
+    static constexpr int kB = NT * kHeadSliceK;
+    static constexpr int kStage = kA + kB;
+    static constexpr int kSmem = kHeadStages * kStage + kEpiWarps * kHeadQueue * 8;
+    static constexpr uint32_t kSfCol = 2 * NT;               // fp4: A scales, then B scales (+32)
+    static constexpr uint32_t kTmemCols = 512;
+    static_assert(kSmem + 2048 <= 232448, "shared memory per CTA");
+    static_assert(KIND == kKindI8 || 2 * NT + 128 <= 512, "TMEM: accumulators + scale factors");
+};
 
 struct HeadParams {
     const uint8_t* op;          // head operand rows [base, base + 8 * groups), slice-major core layout
@@ -132,16 +143,21 @@ __device__ __forceinline__ void head_emit(uint32_t m, uint32_t base_col, uint32_
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParams P) {
+template <int KIND>
+__global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_kernel(HeadParams P) {
+    using L = HeadLayout<KIND>;
+    constexpr int kHeadNT = L::NT;
+    constexpr int kHeadEpiWarps = L::kEpiWarps;
+    constexpr int kHeadA = L::kA, kHeadB = L::kB, kHeadStage = L::kStage;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sStage = smem;                                                        // [kHeadStages][A | B]
-    uint2* sQ = reinterpret_cast<uint2*>(smem + kHeadStages * kHeadStage);         // [16][kHeadQueue]
+    uint2* sQ = reinterpret_cast<uint2*>(smem + kHeadStages * kHeadStage);         // [warps][kHeadQueue]
     __shared__ __align__(8) uint64_t item_full[2], item_empty[2];
     __shared__ __align__(8) uint64_t s_full[kHeadStages], s_empty[kHeadStages], acc_full[2], acc_empty[2];
     __shared__ HeadItem items[2];
     __shared__ uint32_t tmem_base_sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kTmemCols = 2 * kHeadNT;
+    constexpr uint32_t kTmemCols = L::kTmemCols;
 
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -165,6 +181,18 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem_base = tmem_base_sh;
+    if constexpr (KIND == kKindF4) {
+        // unit block scales (ue8m0 127 = 1.0) for every A and B scale slot the MMA may read
+        if (warp >= 2 && warp < 6) {
+            const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+#pragma unroll
+            for (int c = 0; c < 128; c += 32) tmem_fill32(tmem_base + lanes + L::kSfCol + c, 0x7F7F7F7Fu);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
     const uint64_t slice_stride = static_cast<uint64_t>(P.groups) * kHeadGroupBytes;
 
     if (warp == 0) {
@@ -231,9 +259,15 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
                         const uint32_t a0 = smem_u32(sStage + st * kHeadStage);
                         const uint32_t b0 = a0 + kHeadA;
 #pragma unroll
-                        for (int k = 0; k < kHeadSliceK / 32; ++k)
-                            umma_i8<kHeadNT>(d, umma_desc(a0 + k * 256, kHeadGroupBytes),
-                                             umma_desc(b0 + k * 256, kHeadGroupBytes), (s | k) != 0);
+                        for (int k = 0; k < kHeadSliceK / 32; ++k) {
+                            const uint64_t da = umma_desc(a0 + k * 256, kHeadGroupBytes);
+                            const uint64_t db = umma_desc(b0 + k * 256, kHeadGroupBytes);
+                            if constexpr (KIND == kKindI8)
+                                umma_i8<kHeadNT>(d, da, db, (s | k) != 0);
+                            else
+                                umma_f4<kHeadNT>(d, da, db, (s | k) != 0, tmem_base + L::kSfCol,
+                                                 tmem_base + L::kSfCol + 32);
+                        }
                         umma_commit(&s_empty[st]);
                     }
                     umma_commit(&acc_full[as]);
@@ -276,8 +310,18 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
                 const uint32_t f1 = __ldg(P.info + (gcol + 32 - P.base));
                 mbar_wait(&acc_full[as], (aseq >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                uint32_t d[32];
-                tmem_ld64_pack16(tmem_base + lane_base + as * kHeadNT + part * 64, d);
+                // the warp's 64 accumulator columns: packed s16 pairs (int8: values <= K)
+                // or two loads of 32 f32 values (mxf4)
+                uint32_t d[KIND == kKindI8 ? 32 : 64];
+                if constexpr (KIND == kKindI8) {
+                    uint32_t (&d32)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+                    tmem_ld64_pack16(tmem_base + lane_base + as * kHeadNT + part * 64, d32);
+                } else {
+                    uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(d);
+                    uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(d + 32);
+                    tmem_ld32(tmem_base + lane_base + as * kHeadNT + part * 64, lo);
+                    tmem_ld32(tmem_base + lane_base + as * kHeadNT + part * 64 + 32, hi);
+                }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[as]);  // accumulators are in registers
@@ -291,10 +335,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
                     // a lower bound of every column's threshold minov[si+sj] - min(ti,tj)
                     const uint32_t sfirst = (g ? f1 : f0) >> 16;
                     const int thr = valid ? __ldg(P.minov + si + sfirst) - static_cast<int>(ti) : 0;
-                    uint32_t dg[16];
+                    uint32_t cand = 0;
+                    if constexpr (KIND == kKindI8) {
+                        uint32_t dg[16];
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) dg[k] = d[16 * g + k];
-                    const uint32_t cand = rm ? rm & mask16_32(dg, min(max(thr - 1, -32768), 32767)) : 0u;
+                        for (int k = 0; k < 16; ++k) dg[k] = d[16 * g + k];
+                        cand = rm ? rm & mask16_32(dg, min(max(thr - 1, -32768), 32767)) : 0u;
+                    } else if (rm) {
+                        // exact integers in f32, all >= 0: compare the bit patterns as ints
+                        const int key = thr <= 0 ? INT_MIN : __float_as_int(static_cast<float>(thr));
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) cand |= (static_cast<int>(d[32 * g + k]) >= key ? 1u : 0u) << k;
+                        cand &= rm;
+                    }
                     uint32_t e = 0;
                     if (cand) {  // rare: exact per-pair test of the pre-test's candidates
 #pragma unroll
@@ -302,7 +355,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
                             if (!((cand >> k) & 1u)) continue;
                             const uint32_t inf = __ldg(P.info + (gbase + k - P.base));
                             const int need = __ldg(P.minov + si + (inf >> 16));
-                            const int acc = static_cast<int>((dg[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+                            int acc;
+                            if constexpr (KIND == kKindI8) acc = static_cast<int>((d[16 * g + (k >> 1)] >> (16 * (k & 1))) & 0xFFFFu);
+                            else acc = static_cast<int>(__uint_as_float(d[32 * g + k]));
                             if (acc + static_cast<int>(min(ti, inf & 0xFFFFu)) >= need) e |= 1u << k;
                         }
                     }
@@ -319,21 +374,39 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_overlap_kernel(HeadParam
 }
 
 // ---------------------------------------------------------------- head setup
-// Token counts over the region's records [L0, n): cnt[t] += 1 per occurrence.
-__global__ void head_count(const uint32_t* tokens, uint64_t t0, uint64_t t1, uint32_t* cnt) {
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t k = t0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < t1; k += stride)
-        atomicAdd(cnt + tokens[k], 1u);
+// Token counts over every stride-th record of the region [L0, n), one warp
+// per record: cnt[t] += 1 per occurrence.  The head only has to be a good
+// guess of the frequent tokens (any head set gives an exact bound), so a
+// sample of the region's records is enough.
+__global__ void head_count(const uint32_t* tokens, const uint64_t* offsets, uint32_t L0, uint32_t n, uint32_t stride,
+                           uint32_t* cnt) {
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);; w += warps) {
+        const uint64_t r = L0 + static_cast<uint64_t>(w) * stride;
+        if (r >= n) break;
+        const uint64_t b = offsets[r], e = offsets[r + 1];
+        for (uint64_t k = b + lane; k < e; k += 32) atomicAdd(cnt + tokens[k], 1u);
+    }
 }
 
 // Count-of-counts for the head selection: hist[min(c, 65535)] over tokens with c >= 2
 // (a token in one region record cannot contribute to any pair's overlap).
-__global__ void head_hist(const uint32_t* cnt, uint32_t universe, uint32_t* hist) {
+// Small counts (the contended buckets) go through a per-block histogram.
+__global__ void __launch_bounds__(256) head_hist(const uint32_t* cnt, uint32_t universe, uint32_t* hist) {
+    __shared__ uint32_t sh[1024];
+    for (int k = threadIdx.x; k < 1024; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < universe; t += stride) {
         const uint32_t c = cnt[t];
-        if (c >= 2) atomicAdd(hist + min(c, 65535u), 1u);
+        if (c < 2) continue;
+        if (c < 1024) atomicAdd(sh + c, 1u);
+        else atomicAdd(hist + min(c, 65535u), 1u);
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 1024; k += blockDim.x)
+        if (sh[k]) atomicAdd(hist + k, sh[k]);
 }
 
 // One block of 1024 threads: the smallest count c* >= 2 such that at most K
@@ -385,30 +458,33 @@ __global__ void head_assign(const uint32_t* cnt, uint32_t universe, const uint32
     }
 }
 
-// One CTA per 8-row core group of operand rows [base + 8g, +8): the K-byte
-// head indicator rows (0/1) in the slice-major core layout, and info[] =
-// (|r| << 16) | tail.  Rows outside [L0, n) stay zero (size 0).
+// One CTA per 8-row core group of operand rows [base + 8g, +8): the head
+// indicator rows in the slice-major core layout -- int8 (one byte 0/1 per
+// head token, K bytes) or mxf4 (e2m1 1.0 = 0x2 per head token, two per byte
+// low nibble first, K/2 bytes) -- and info[] = (|r| << 16) | tail.  Rows
+// outside [L0, n) stay zero (size 0).
+template <int KIND>
 __global__ void __launch_bounds__(256) head_expand(const uint32_t* tokens, const uint64_t* offsets, uint32_t n,
                                                    uint32_t L0, uint32_t base, uint32_t groups, int K,
                                                    const uint16_t* map, uint8_t* op, uint32_t* info) {
-    extern __shared__ __align__(16) uint8_t rowbuf[];  // [8][K]
+    extern __shared__ __align__(16) uint8_t rowbuf[];  // [8][RB]
     __shared__ uint32_t heads[8];
+    const int RB = KIND == kKindI8 ? K : K / 2;         // operand bytes per row
     const uint32_t g = blockIdx.x;
     uint4* z = reinterpret_cast<uint4*>(rowbuf);
-    for (int k = threadIdx.x; k < 8 * K / 16; k += blockDim.x) z[k] = make_uint4(0, 0, 0, 0);
+    for (int k = threadIdx.x; k < 8 * RB / 16; k += blockDim.x) z[k] = make_uint4(0, 0, 0, 0);
     if (threadIdx.x < 8) heads[threadIdx.x] = 0;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = base + 8 * g + warp;  // one warp per row
-    uint32_t size = 0;
     if (r >= L0 && r < n) {
         const uint64_t b = offsets[r], e = offsets[r + 1];
-        size = static_cast<uint32_t>(e - b);
         uint32_t h = 0;
         for (uint64_t k = b + lane; k < e; k += 32) {
-            const uint16_t m = map[tokens[k]];
+            const uint32_t m = map[tokens[k]];
             if (m != 0xFFFFu) {
-                rowbuf[warp * K + m] = 1;
+                if constexpr (KIND == kKindI8) rowbuf[warp * RB + m] = 1;
+                else atomicOr(reinterpret_cast<uint32_t*>(rowbuf + warp * RB) + (m >> 3), 0x2u << (4 * (m & 7)));
                 ++h;
             }
         }
@@ -422,12 +498,11 @@ __global__ void __launch_bounds__(256) head_expand(const uint32_t* tokens, const
         const uint32_t sz = (rr >= L0 && rr < n) ? static_cast<uint32_t>(offsets[rr + 1] - offsets[rr]) : 0u;
         info[8 * g + threadIdx.x] = (sz << 16) | (sz - heads[threadIdx.x]);
     }
-    (void)size;
     // 16-byte units: unit u -> (slice s, chunk c, row q): u = (s * 8 + c) * 8 + q
-    const int units = K / 16 * 8;
+    const int units = RB / 16 * 8;
     for (int u = threadIdx.x; u < units; u += blockDim.x) {
         const int q = u & 7, c = (u >> 3) & 7, s = u >> 6;
-        const uint4 v = *reinterpret_cast<const uint4*>(rowbuf + q * K + s * kHeadSliceK + c * 16);
+        const uint4 v = *reinterpret_cast<const uint4*>(rowbuf + q * RB + s * kHeadSliceK + c * 16);
         const uint64_t off = ((static_cast<uint64_t>(s) * groups + g) * 8 + c) * 128 + q * 16;
         *reinterpret_cast<uint4*>(op + off) = v;
     }

@@ -54,19 +54,26 @@ def test_sketch_kernel_matches_reference_stores(lib, golden, colls):
         assert sha(store) == e["sha256"], e
 
 
-FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "tc-i8-1tile", "tc-i8-noext", "popc", "tc-l2gemm", "tc-head"]
+FILTERS = ["tc-fp4", "tc-i8-pair", "tc-i8", "tc-i8-1tile", "tc-i8-noext", "popc", "tc-l2gemm", "tc-head",
+           "tc-head-i8"]
 
 
 def set_filter(monkeypatch, flavour):
     """tcgen05 fp4 / int8 CTA-pair / int8 single-CTA with two row tiles per column
     tile (default) or one (with the popcount extension block, or K = b) /
-    level-2 GEMM, or POPC; tc-head: the level-2 GEMM with the head-overlap
-    kernel (K3a) forced over every record of >= 3 tokens with a 128-token head."""
+    level-2 GEMM, or POPC; tc-head / tc-head-i8: the level-2 GEMM with the
+    head-overlap kernel (K3a, mxf4 / int8 operands) forced over every record
+    of >= 3 tokens with a 256 / 128-token head."""
+    head = flavour.startswith("tc-head")
     monkeypatch.setenv("SSJB_FILTER", "popc" if flavour == "popc" else "tc")
-    monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour in ("tc-l2gemm", "tc-head") else "0")
-    monkeypatch.setenv("SSJB_HEAD", "2" if flavour == "tc-head" else "0")
+    monkeypatch.setenv("SSJB_L2GEMM", "1" if flavour == "tc-l2gemm" or head else "0")
+    monkeypatch.setenv("SSJB_HEAD", "2" if head else "0")
     monkeypatch.setenv("SSJB_HEAD_MIN_SIZE", "3")
-    monkeypatch.setenv("SSJB_HEAD_K", "128")
+    monkeypatch.setenv("SSJB_HEAD_KIND", "i8" if flavour == "tc-head-i8" else "fp4")
+    monkeypatch.setenv("SSJB_HEAD_K", "128" if flavour == "tc-head-i8" else "256")
+    # column-chunk-major work-item claim order (default only above 262144 rows)
+    ordered = flavour in ("tc-i8", "tc-l2gemm", "tc-head", "tc-head-i8", "tc-fp4")
+    monkeypatch.setenv("SSJB_ORDER_MIN_ROWS", "1" if ordered else "1000000000")
     monkeypatch.setenv("SSJB_TC_KIND", "i8" if flavour.startswith("tc-i8") else "fp4")
     monkeypatch.setenv("SSJB_TC2", "1" if flavour == "tc-i8-pair" else "0")
     monkeypatch.setenv("SSJB_NOEXT", "1" if flavour == "tc-i8-noext" else "0")
@@ -185,8 +192,13 @@ def test_naive_vs_oracle(lib, oracle):
         assert rep.counters["candidates"] == cnt["candidates"] == rep.counters["verified"]
 
 
-def test_survivor_and_result_overflow_batches(lib, golden, colls, monkeypatch):
-    """Tiny survivor/result buffers force many filter batches and result runs."""
+@pytest.mark.parametrize("flavour", ["default", "tc-head"])
+def test_survivor_and_result_overflow_batches(lib, golden, colls, monkeypatch, flavour):
+    """Tiny survivor/result buffers force many filter batches and result runs
+    (tc-head: level-2 GEMM batches in column-chunk-major claim order, then
+    head-overlap batches)."""
+    if flavour != "default":
+        set_filter(monkeypatch, flavour)
     monkeypatch.setenv("SSJB_SURVIVOR_CAP", str(1 << 19))
     monkeypatch.setenv("SSJB_RESULT_CAP", str(1 << 19))
     for e in golden["joins"]:

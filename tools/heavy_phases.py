@@ -26,7 +26,8 @@ for name in names:
     print(json.dumps({"config": name, "gen_s": round(gen, 2), "wall_s": round(wall, 3),
                       "window": r.counters["candidates"], "verified": r.counters["verified"],
                       "matched": r.counters["matched"], "saturated": r.saturated_records,
-                      "survivors_emitted": x["survivors"], "batches": x["batches"], "kernel": x["filter_kernel"],
+                      "survivors_emitted": x["survivors"], "head_survivors": x.get("head_survivors"),
+                      "head_k": x.get("head_k"), "batches": x["batches"], "kernel": x["filter_kernel"],
                       "ms": {k[3:]: round(x[k], 2) for k in x if k.startswith("ms_")},
                       "timings": r.timings}), flush=True)
     del coll

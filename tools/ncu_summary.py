@@ -3,8 +3,9 @@
 into profiles/: one markdown table of the key per-launch metrics and a JSON
 file bench.py reads for `roofline.traffic` (dram read+write bytes per launch).
 
-    python tools/ncu_summary.py gpurun_out/filter_tc.ncu-rep profiles/r01_filter_tc_ncu
+    python tools/ncu_summary.py gpurun_out/filter_tc.ncu-rep profiles/r01_filter_tc_ncu [kernel-regex]
 """
+import re
 import csv
 import io
 import json
@@ -32,7 +33,7 @@ def to_bytes(v, unit):
     return float(v) * scale
 
 
-def main(rep, out_prefix):
+def main(rep, out_prefix, pattern=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -42,6 +43,8 @@ def main(rep, out_prefix):
     lines = ["| # | kernel | " + " | ".join(f"{label} ({units[i]})" for i, _, label in cols) + " |",
              "|---|---|" + "---|" * len(cols)]
     per_launch = []
+    if pattern:
+        data = [r for r in data if re.search(pattern, r[ki])]
     for n, r in enumerate(data):
         lines.append(f"| {n} | `{r[ki][:60]}` | " + " | ".join(r[i] for i, _, _ in cols) + " |")
         rd = to_bytes(r[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
@@ -58,4 +61,4 @@ def main(rep, out_prefix):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)

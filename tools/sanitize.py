@@ -29,7 +29,9 @@ FLAVOURS = {
     "fp4": dict(SSJB_FILTER="tc", SSJB_TC_KIND="fp4", SSJB_L2GEMM="0", SSJB_HEAD="0"),
     "l2gemm": dict(SSJB_FILTER="tc", SSJB_TC_KIND="i8", SSJB_L2GEMM="1", SSJB_HEAD="0"),
     "head": dict(SSJB_FILTER="tc", SSJB_TC_KIND="i8", SSJB_L2GEMM="1", SSJB_HEAD="2", SSJB_HEAD_MIN_SIZE="3",
-                 SSJB_HEAD_K="128"),
+                 SSJB_HEAD_K="256", SSJB_HEAD_KIND="fp4", SSJB_ORDER_MIN_ROWS="1"),
+    "head_i8": dict(SSJB_FILTER="tc", SSJB_TC_KIND="i8", SSJB_L2GEMM="1", SSJB_HEAD="2", SSJB_HEAD_MIN_SIZE="3",
+                    SSJB_HEAD_K="128", SSJB_HEAD_KIND="i8", SSJB_ORDER_MIN_ROWS="1"),
     "popc": dict(SSJB_FILTER="popc", SSJB_L2GEMM="0", SSJB_HEAD="0"),
 }
 
