@@ -81,6 +81,7 @@ typedef struct ssjb_stats {
     double ms_head;          /* device ms of the head-overlap kernel (max over GPUs) */
     double ms_head_setup;    /* device ms of head selection + operand build */
     int head_k;              /* head tokens (GEMM depth) */
+    double ms_merge;         /* host ms merging the row shards' sorted runs (multi-shard joins) */
 } ssjb_stats;
 
 ssj_status ssjb_report_stats(const ssj_report* report, ssjb_stats* out);

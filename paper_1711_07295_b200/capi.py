@@ -107,7 +107,8 @@ class Stats(C.Structure):
                                           "ms_verify", "ms_sort", "ms_download")] + \
                [("devices", C.c_int), ("filter_kernel", C.c_int),
                 ("head_pairs", C.c_uint64), ("head_survivors", C.c_uint64),
-                ("ms_head", C.c_double), ("ms_head_setup", C.c_double), ("head_k", C.c_int)]
+                ("ms_head", C.c_double), ("ms_head_setup", C.c_double), ("head_k", C.c_int),
+                ("ms_merge", C.c_double)]
 
 
 # ssjb_pair_sink: int (*)(const ssj_pair*, size_t, void*)

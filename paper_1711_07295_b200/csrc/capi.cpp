@@ -239,15 +239,19 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
             seqs.emplace_back(p.pairs.data(), p.pairs.size());
             total += p.pairs.size();
         }
+        const auto m0 = std::chrono::steady_clock::now();
         ssjb::PairVec merged(total);
         merge_shards(seqs, merged.data());
         rep.pairs = std::move(merged);
+        rep.stats.ms_merge = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - m0).count();
         for (auto& p : parts) p.pairs = ssjb::PairVec();
     }
     ssj_counters& c = rep.counters;
     std::memset(&c, 0, sizeof c);
     ssjb_stats& s = rep.stats;
+    const double ms_merge = s.ms_merge;
     std::memset(&s, 0, sizeof s);
+    s.ms_merge = ms_merge;
     for (auto& p : parts) {
         c.candidates += p.candidates;
         c.bitmap_tested += p.bitmap_tested;

@@ -102,7 +102,7 @@ struct TableStage {
         if (total > cap) {
             if (host) cudaFreeHost(host);
             cap = std::max(total, size_t(1) << 20);
-            CK(cudaMallocHost(reinterpret_cast<void**>(&host), cap));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&host), cap, cudaHostAllocPortable));
         }
         uint8_t* dev = A.alloc<uint8_t>(total);
         size_t off = 0;
@@ -206,24 +206,26 @@ bool build_delta8(const Collection& c) {
 }
 
 void register_host(const Collection& c) {
-    // Page-lock the arrays that are uploaded so every upload is a pinned DMA;
+    // Page-lock the arrays that are uploaded so every upload is a pinned DMA
+    // (portable: pinned for every device's context -- multi-GPU joins upload
+    // the same collection to each device);
     // tokens of a universe <= 65536 travel as a delta-coded byte stream (dense
     // universes) or a 16-bit copy, built once here.
     if (c.host_registered) return;
     if (narrow_tokens(c) && c.universe <= 65535 && env_u64("SSJB_DELTA8", 1) != 0 && build_delta8(c)) {
         c.use_delta8 = true;
-        cudaHostRegister(c.tokens8.data(), c.tokens8.size(), cudaHostRegisterDefault);
-        cudaHostRegister(c.exc_start.data(), c.exc_start.size() * 4, cudaHostRegisterDefault);
-        if (!c.exc_val.empty()) cudaHostRegister(c.exc_val.data(), c.exc_val.size() * 2, cudaHostRegisterDefault);
+        cudaHostRegister(c.tokens8.data(), c.tokens8.size(), cudaHostRegisterPortable);
+        cudaHostRegister(c.exc_start.data(), c.exc_start.size() * 4, cudaHostRegisterPortable);
+        if (!c.exc_val.empty()) cudaHostRegister(c.exc_val.data(), c.exc_val.size() * 2, cudaHostRegisterPortable);
     } else if (narrow_tokens(c)) {
         c.tokens16.assign(c.tokens.begin(), c.tokens.end());
-        cudaHostRegister(c.tokens16.data(), c.tokens16.size() * sizeof(uint16_t), cudaHostRegisterDefault);
+        cudaHostRegister(c.tokens16.data(), c.tokens16.size() * sizeof(uint16_t), cudaHostRegisterPortable);
     } else if (!c.tokens.empty()) {
         cudaHostRegister(const_cast<uint32_t*>(c.tokens.data()), c.tokens.size() * sizeof(uint32_t),
-                         cudaHostRegisterDefault);
+                         cudaHostRegisterPortable);
     }
     cudaHostRegister(const_cast<uint64_t*>(c.offsets.data()), c.offsets.size() * sizeof(uint64_t),
-                     cudaHostRegisterDefault);
+                     cudaHostRegisterPortable);
     cudaGetLastError();  // registration is an optimisation; ignore failures
     c.host_registered = true;
 }
@@ -297,7 +299,7 @@ namespace {
 __global__ void sizes_from_offsets(const uint64_t* off, uint32_t* sizes, size_t n) {
     size_t r = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (r < n) sizes[r] = static_cast<uint32_t>(off[r + 1] - off[r]);
-    else if (r < n + kPadRows) sizes[r] = n ? static_cast<uint32_t>(off[n] - off[n - 1]) : 0u;
+    else if (r < n + kPadRows + 8) sizes[r] = n ? static_cast<uint32_t>(off[n] - off[n - 1]) : 0u;
 }
 
 __global__ void widen_tokens(const uint16_t* in, uint32_t* out, size_t n) {
@@ -451,12 +453,12 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     if (resident) {
         CK(cudaMalloc(&rep->tokens, tok_bytes));
         CK(cudaMalloc(&rep->offsets, (n + 1) * sizeof(uint64_t)));
-        CK(cudaMalloc(&rep->sizes, (n + kPadRows) * sizeof(uint32_t)));
+        CK(cudaMalloc(&rep->sizes, (n + kPadRows + 8) * sizeof(uint32_t)));
     } else {
         rep->stream = stream;
         CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->tokens), tok_bytes, stream));
         CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->offsets), (n + 1) * sizeof(uint64_t), stream));
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows) * sizeof(uint32_t), stream));
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows + 8) * sizeof(uint32_t), stream));
     }
     rep->device = device;
     rep->n = n;
@@ -490,7 +492,7 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     }
     rep->bytes = tok_h2d + (n + 1) * sizeof(uint64_t);
     h2d += rep->bytes;
-    const size_t tot = n + kPadRows;
+    const size_t tot = n + kPadRows + 8;  // (n_pad = n + kPadRows rounded up to 8 rows)
     sizes_from_offsets<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(rep->offsets, rep->sizes, n);
     ++launches;
     CK(cudaGetLastError());
@@ -534,7 +536,7 @@ std::shared_ptr<DeviceReplica> upload_streamed(const Collection& c, int device, 
     rep->stream = stream;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->tokens), tok_bytes, stream));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->offsets), (n + 1) * sizeof(uint64_t), stream));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows) * sizeof(uint32_t), stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows + 8) * sizeof(uint32_t), stream));
     const bool delta8 = c.use_delta8;
     const bool narrow = !delta8 && narrow_tokens(c);
     t16 = nullptr;
@@ -545,7 +547,7 @@ std::shared_ptr<DeviceReplica> upload_streamed(const Collection& c, int device, 
     rep->n = n;
     rep->tokens_total = T;
     CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
-    sizes_from_offsets<<<static_cast<unsigned>((n + kPadRows + 255) / 256), 256, 0, stream>>>(rep->offsets,
+    sizes_from_offsets<<<static_cast<unsigned>((n + kPadRows + 8 + 255) / 256), 256, 0, stream>>>(rep->offsets,
                                                                                               rep->sizes, n);
     ++launches;
     CK(cudaGetLastError());
@@ -934,7 +936,7 @@ void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     static thread_local cudaEvent_t ev[2];
     if (!stage[0]) {
         for (int b = 0; b < 2; ++b) {
-            CK(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), kChunk, cudaHostAllocPortable));
             CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
         }
     }
@@ -1078,7 +1080,7 @@ __global__ void small_sort_pack(const unsigned long long* keys, const uint32_t* 
 
 SmallPack* host_small_pack() {
     static thread_local SmallPack* p = nullptr;
-    if (!p) CK(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(SmallPack)));
+    if (!p) CK(cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof(SmallPack), cudaHostAllocPortable));
     return p;
 }
 

@@ -515,6 +515,21 @@ struct TcItem {
     uint32_t tile, c0, c1, ntiles, done;
 };
 
+// An epilogue warp's copy of a published work item: lane 0 alone reads the
+// shared slot and broadcasts it, so the lane that releases the slot (its
+// mbarrier arrive) is the only one that read it.
+__device__ __forceinline__ TcItem warp_item(const TcItem& slot, int lane) {
+    TcItem v{};
+    if (lane == 0) v = slot;
+    v.item = __shfl_sync(0xFFFFFFFFu, v.item, 0);
+    v.tile = __shfl_sync(0xFFFFFFFFu, v.tile, 0);
+    v.c0 = __shfl_sync(0xFFFFFFFFu, v.c0, 0);
+    v.c1 = __shfl_sync(0xFFFFFFFFu, v.c1, 0);
+    v.ntiles = __shfl_sync(0xFFFFFFFFu, v.ntiles, 0);
+    v.done = __shfl_sync(0xFFFFFFFFu, v.done, 0);
+    return v;
+}
+
 // KIND: operand kind; KA: level-1 operand bytes per row; K2: level-2 GEMM
 // operand bytes (0: none); W2: level-2 Xor sketch words for the POPC check
 // (used when K2 == 0); NS: B stages; NT: columns per MMA tile.
@@ -534,7 +549,13 @@ struct TcLayout {
     // with the tile -- with only two 59 KB stages fitting, a stage's lifetime
     // (copy + MMAs + epilogue) otherwise paces the pipeline
     static constexpr bool kEarlyB = K2 > 0;
-    static constexpr int kEpiWarps = NT == 192 ? 12 : 16;      // 3 or 4 per TMEM lane quarter
+    // epilogue warps (4 per column part, one per TMEM lane quarter): 64 columns
+    // each for the level-2 GEMM's 128-column tiles (the per-tile fixed cost of a
+    // warp -- barrier waits, column sizes, thresholds -- paid by 8 warps, not 16)
+#ifndef SSJB_L2_EPI_WARPS
+#define SSJB_L2_EPI_WARPS 16
+#endif
+    static constexpr int kEpiWarps = NT == 192 ? 12 : ((K2 > 0 && NT == 128) ? SSJB_L2_EPI_WARPS : 16);
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
     static constexpr int kRow = KA + K2 + (kNoExt ? 0 : 16);   // operand row: L1 | L2 | size chunk
@@ -753,7 +774,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         for (;;) {
             const int slot = iseq & 1;
             mbar_wait(&item_full[slot], (iseq >> 1) & 1);
-            const TcItem info = items[slot];
+            const TcItem info = warp_item(items[slot], lane);
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (info.done) break;
@@ -850,7 +871,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (__any_sync(0xFFFFFFFFu, e != 0)) tc_emit(e, gbase, i, q, qlen, P, lane);
                 };
                 bool groups_done = (P.debug & 1) != 0;
-                if constexpr (KIND == kKindI8 && L::kColsPerWarp == 64) {
+                if constexpr (KIND == kKindI8 && L::kColsPerWarp == 64 && K2 == 0) {
                     // interior fast path: the warp's 64 columns in ONE packed TMEM
                     // load (one load latency per tile instead of two)
                     if (fast && !groups_done) {

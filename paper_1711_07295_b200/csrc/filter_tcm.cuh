@@ -248,7 +248,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
         for (;;) {
             const int slot = iseq & 1;
             mbar_wait(&item_full[slot], (iseq >> 1) & 1);
-            const TcItem info = items[slot];
+            const TcItem info = warp_item(items[slot], lane);
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (info.done) break;

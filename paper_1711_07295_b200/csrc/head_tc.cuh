@@ -98,6 +98,17 @@ struct HeadItem {
     uint32_t row0, c0, ntiles, done;
 };
 
+// lane 0 reads the published item and broadcasts it (see warp_item, filter_tc.cuh)
+__device__ __forceinline__ HeadItem warp_head_item(const HeadItem& slot, int lane) {
+    HeadItem v{};
+    if (lane == 0) v = slot;
+    v.row0 = __shfl_sync(0xFFFFFFFFu, v.row0, 0);
+    v.c0 = __shfl_sync(0xFFFFFFFFu, v.c0, 0);
+    v.ntiles = __shfl_sync(0xFFFFFFFFu, v.ntiles, 0);
+    v.done = __shfl_sync(0xFFFFFFFFu, v.done, 0);
+    return v;
+}
+
 __device__ __forceinline__ void head_flush(uint2* q, int& qlen, const HeadParams& P, int lane) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(qlen));
@@ -288,7 +299,7 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
         for (;;) {
             const int slot = iseq & 1;
             mbar_wait(&item_full[slot], (iseq >> 1) & 1);
-            const HeadItem info = items[slot];
+            const HeadItem info = warp_head_item(items[slot], lane);
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (info.done) break;

@@ -167,4 +167,7 @@ def test_heavy_sharded(lib, name):
     if "counters" in g:
         for k in COUNTERS:
             assert rep.counters[k] == g["counters"][k], k
-    print(f"{name} 8 shards: total_s={rep.timings['total_s']:.3f} (first call {first_s:.3f})")
+    # the shard merge (all host threads, O(pairs)) is a small part of the join
+    assert rep.extra["ms_merge"] < 0.25 * rep.timings["total_s"] * 1e3, rep.extra
+    print(f"{name} 8 shards: total_s={rep.timings['total_s']:.3f} (first call {first_s:.3f}) "
+          f"merge_ms={rep.extra['ms_merge']:.1f}")
