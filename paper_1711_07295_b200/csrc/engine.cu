@@ -663,7 +663,7 @@ struct TcKernel {
 template <int KIND, int KA, int K2, int W2, int NS, int NT>
 TcKernel tc_kernel() {
     using L = dev::TcLayout<KIND, KA, K2, W2, NS, NT>;
-    return TcKernel{dev::filter_tc_kernel<KIND, KA, K2, W2, NS, NT>, L::kBytes, L::kThreads, NT, L::kEpiWarps / 4};
+    return TcKernel{dev::filter_tc_kernel<KIND, KA, K2, W2, NS, NT>, L::kBytes, L::kThreads, NT, L::kParts};
 }
 
 // Tensor-core filter instantiations: level-1 width b = 64*words.
@@ -2750,6 +2750,208 @@ void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& pla
     double ms_verify = 0;
     dev::Control h_ctl{};
     uint64_t verify_bytes = 0;
+    // Filtered path (round 2): length window + Xor-sketch bound on R x S tiles,
+    // then exact verification of the survivors only.  Sound for every
+    // similarity function whose required overlap depends on |r|+|s| (not
+    // Cosine); NAIVE's counters are unchanged (candidates = verified = |R||S|).
+    // SSJB_RS_FILTER: 0 off, 1 auto (|R||S| >= 2^24), 2 forced.
+    const uint64_t rs_mode = env_u64("SSJB_RS_FILTER", 1);
+    const bool filtered = !plan.cosine && rs_mode != 0 && (rs_mode == 2 || total >= (uint64_t(1) << 24)) &&
+                          plan.delivery != 2 && R.max_size < (uint32_t(1) << 30);
+    if (filtered) {
+        const int words = std::max(R.median_size(), Sc.median_size()) > 64 ? 2 : 1;
+        const uint32_t nR = static_cast<uint32_t>(R.size()), nS32 = static_cast<uint32_t>(nS);
+        uint64_t* bits_r = A.alloc<uint64_t>((size_t(nR) + kPadRows + 8) * words);
+        uint64_t* bits_s = &R == &Sc ? bits_r : A.alloc<uint64_t>((size_t(nS32) + kPadRows + 8) * words);
+        if (!launch_build_sub(*repR, bits_r, nullptr, Method::Xor, 64 * words, 0, 0, s, st.launches))
+            launch_build(*repR, bits_r, Method::Xor, 64 * words, 0, s, st.launches);
+        if (bits_s != bits_r && !launch_build_sub(*repS, bits_s, nullptr, Method::Xor, 64 * words, 0, 0, s, st.launches))
+            launch_build(*repS, bits_s, Method::Xor, 64 * words, 0, s, st.launches);
+        // per R size x: the S index window of sizes y with minov[x+y] <= min(x, y)
+        // (an overlap never exceeds the smaller record; minov steps by <= 1, so
+        // the admissible y form one interval)
+        const uint32_t mr = R.max_size, ms = Sc.max_size;
+        std::vector<uint32_t> lo(mr + 1), hi(mr + 1);
+        auto ok = [&](uint32_t x, uint32_t y) { return plan.minov[x + y] <= static_cast<int32_t>(std::min(x, y)); };
+        for (uint32_t x = 0; x <= mr; ++x) {
+            const uint32_t ym = std::min(x, ms);
+            lo[x] = hi[x] = nS32;
+            if (!ok(x, ym)) continue;  // no admissible size
+            // y <= x: y - minov[x+y] is nondecreasing -> first admissible y by bisection
+            uint32_t a = 0, b = ym;
+            while (a < b) {
+                const uint32_t m = (a + b) / 2;
+                if (ok(x, m)) b = m;
+                else a = m + 1;
+            }
+            const uint32_t ylo = a;
+            // y >= x: minov[x+y] <= x holds on a prefix of [x, ms]
+            uint32_t yhi = ms;
+            if (x < ms) {
+                a = x;
+                b = ms;
+                while (a < b) {
+                    const uint32_t m = (a + b + 1) / 2;
+                    if (ok(x, m)) a = m;
+                    else b = m - 1;
+                }
+                yhi = a;
+            }
+            lo[x] = Sc.first_ge[ylo];
+            hi[x] = std::max(lo[x], Sc.first_ge[yhi + 1]);
+        }
+        std::vector<int32_t> maxham(plan.minov.size());
+        for (size_t S = 0; S < maxham.size(); ++S) maxham[S] = static_cast<int32_t>(S) - 2 * plan.minov[S];
+        // work items: (R row tile, S column chunk) over each tile's window union
+        std::vector<uint2> items;
+        const uint32_t ntiles = static_cast<uint32_t>((rows + dev::kRowTile - 1) / dev::kRowTile);
+        for (uint32_t t = 0; t < ntiles; ++t) {
+            const size_t a = plan.r_begin + size_t(t) * dev::kRowTile;
+            const size_t b = std::min<size_t>(a + dev::kRowTile, plan.r_end);
+            uint32_t wlo = nS32, whi = 0;  // union of the rows' windows (empty ones excluded)
+            for (size_t r = a; r < b; ++r) {
+                const uint32_t x = R.rec_size(r);
+                if (hi[x] > lo[x]) {
+                    wlo = std::min(wlo, lo[x]);
+                    whi = std::max(whi, hi[x]);
+                }
+            }
+            if (whi <= wlo) continue;
+            for (uint32_t cc = wlo / dev::kColChunk; cc <= (whi - 1) / dev::kColChunk; ++cc) items.push_back(make_uint2(t, cc));
+        }
+        uint32_t *d_lo = nullptr, *d_hi = nullptr;
+        int32_t* d_maxham = nullptr;
+        uint2* d_items = nullptr;
+        TableStage fs;
+        fs.add(&d_lo, lo.data(), lo.size() * 4);
+        fs.add(&d_hi, hi.data(), hi.size() * 4);
+        fs.add(&d_maxham, maxham.data(), maxham.size() * 4);
+        if (!items.empty()) fs.add(&d_items, items.data(), items.size() * sizeof(uint2));
+        fs.flush(A, s, st.h2d_bytes);
+        const uint64_t surv_cap = std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << 26), 1u << 20);
+        uint2* d_surv = A.alloc<uint2>(surv_cap);
+        dev::RsFilterParams FP{};
+        FP.bits_r = bits_r;
+        FP.bits_s = bits_s;
+        FP.sizes_r = repR->sizes;
+        FP.sizes_s = repS->sizes;
+        FP.s_lo = d_lo;
+        FP.s_hi = d_hi;
+        FP.maxham = d_maxham;
+        FP.items = d_items;
+        FP.r_begin = static_cast<uint32_t>(plan.r_begin);
+        FP.r_end = static_cast<uint32_t>(plan.r_end);
+        FP.n_s = nS32;
+        FP.words = words;
+        FP.surv = d_surv;
+        FP.surv_cap = surv_cap;
+        FP.ctl = d_ctl;
+        dev::VerifyRsPairsParams RP{};
+        RP.ta = repR->tokens;
+        RP.oa = repR->offsets;
+        RP.tb = repS->tokens;
+        RP.ob = repS->offsets;
+        RP.need = VP.need;
+        RP.surv = d_surv;
+        RP.count_ptr = &d_ctl->survivors;
+        RP.count_cap = surv_cap;
+        RP.res_keys = SB.ka;
+        RP.res_ov = SB.va;
+        RP.res_cap = res_cap;
+        RP.ctl = d_ctl;
+        uint64_t res_count = 0, survivors = 0;
+        auto flush = [&]() {  // sort + pack + download the result buffer as one run
+            if (!res_count) return;
+            const bool inb = sort_results(SB, res_count, idbits, s, st.launches);
+            PairOut* packed = A.alloc<PairOut>(res_count);
+            pack_pairs<<<static_cast<unsigned>((res_count + 255) / 256), 256, 0, s>>>(
+                inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va, packed, res_count);
+            ++st.launches;
+            CK(cudaGetLastError());
+            counted += res_count;
+            if (plan.delivery == 0) {
+                PairVec run(res_count);
+                d2h_staged(run.data(), packed, res_count * sizeof(PairOut), s);
+                st.d2h_bytes += res_count * sizeof(PairOut);
+                runs.push_back(std::move(run));
+            }
+            CK(cudaStreamSynchronize(s));
+            CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
+            res_count = 0;
+        };
+        uint64_t soft = std::max<uint64_t>(surv_cap / 2, 1), span = items.size(), ib = 0;
+        const uint64_t nitems = items.size();
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::rs_filter, dev::kRowTile, 0));
+        while (ib < nitems) {
+            const uint64_t ie = std::min(nitems, ib + span);
+            CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
+            CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
+            FP.item_begin = ib;
+            FP.item_end = ie;
+            FP.surv_soft = soft;
+            cudaEvent_t a = T.mark();
+            dev::rs_filter<<<static_cast<unsigned>(std::min<uint64_t>(ie - ib, uint64_t(sms) * std::max(per_sm, 1))),
+                             dev::kRowTile, 0, s>>>(FP);
+            ++st.launches;
+            CK(cudaGetLastError());
+            cudaEvent_t b = T.mark();
+            CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            st.ms_filter += Timer::ms(a, b);
+            const uint64_t S = h_ctl.survivors;
+            const uint64_t processed = std::min<uint64_t>(h_ctl.work_next, ie - ib);
+            if (S > surv_cap) {  // overshoot: nothing counted yet, retry with a lower cap / fewer items
+                if (soft > 1) soft = std::max<uint64_t>(soft / 4, 1);
+                else span = std::max<uint64_t>(1, std::min(span, std::max<uint64_t>(processed, 2)) / 2);
+                continue;
+            }
+            ++st.batches;
+            survivors += S;
+            if (S) {
+                if (res_count + S > res_cap) flush();
+                cudaEvent_t c0 = T.mark();
+                dev::verify_rs_pairs<<<static_cast<unsigned>(std::min<uint64_t>((S + 255) / 256, uint64_t(sms) * 16)),
+                                       256, 0, s>>>(RP);
+                ++st.launches;
+                CK(cudaGetLastError());
+                cudaEvent_t c1 = T.mark();
+                CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                ms_verify += Timer::ms(c0, c1);
+                if (h_ctl.results > res_cap) throw DeviceError("RS result buffer overflow");
+                res_count = h_ctl.results;
+            }
+            ib += processed;
+        }
+        flush();
+        verify_bytes = h_ctl.verify_bytes;
+        st.survivors = survivors;
+        // runs are each sorted; batches follow the item order, which a row tile's
+        // chunks may straddle: merge
+        PairVec merged;
+        for (auto& r : runs) {
+            if (merged.empty()) {
+                merged = std::move(r);
+                continue;
+            }
+            PairVec tmp(merged.size() + r.size());
+            std::merge(merged.begin(), merged.end(), r.begin(), r.end(), tmp.begin(),
+                       [](const PairOut& x, const PairOut& y) {
+                           return x.id_r != y.id_r ? x.id_r < y.id_r : x.id_s < y.id_s;
+                       });
+            merged.swap(tmp);
+        }
+        out.pairs = std::move(merged);
+        out.matched = counted;
+        st.verify_bytes = verify_bytes;
+        st.ms_upload = Timer::ms(e0, e_up);
+        st.ms_verify = ms_verify;
+        out.index_s = 0;
+        out.candidates_s = 0;
+        out.verify_s = std::chrono::duration<double>(Clock::now() - t_start).count();
+        return;
+    }
     while (k0 < total) {
         const uint64_t k1 = std::min(total, k0 + std::max<uint64_t>(batch, 1));
         CK(cudaMemsetAsync(d_ctl, 0, sizeof(dev::Control), s));

@@ -35,6 +35,9 @@ namespace dev {
 #ifndef SSJB_SUSPEND_NS
 #define SSJB_SUSPEND_NS 8192u
 #endif
+#ifndef SSJB_EARLY_ACC
+#define SSJB_EARLY_ACC 1
+#endif
 constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
 constexpr int kTcLut = 1536;       // shared-memory copy of maxham[] (entries)
 constexpr int kKindI8 = 0;         // tcgen05 kind::i8, s32 accumulators
@@ -552,12 +555,19 @@ struct TcLayout {
     // epilogue warps (4 per column part, one per TMEM lane quarter): 64 columns
     // each for the level-2 GEMM's 128-column tiles (the per-tile fixed cost of a
     // warp -- barrier waits, column sizes, thresholds -- paid by 8 warps, not 16)
-#ifndef SSJB_L2_EPI_WARPS
-#define SSJB_L2_EPI_WARPS 16
+    static constexpr int kEpiWarps = NT == 192 ? 12 : 16;
+    // level-2 GEMM kernel: the epilogue is latency-bound per warp, so its 16
+    // warps form two sets that take alternate tiles (the two accumulator
+    // slots) -- each warp has two tile intervals for 64 columns instead of one
+    // for 32 (SSJB_L2_EPI_SETS=1: every warp on every tile)
+#ifndef SSJB_L2_EPI_SETS
+#define SSJB_L2_EPI_SETS 2
 #endif
-    static constexpr int kEpiWarps = NT == 192 ? 12 : ((K2 > 0 && NT == 128) ? SSJB_L2_EPI_WARPS : 16);
+    static constexpr int kSets = (K2 > 0 && NT == 128) ? SSJB_L2_EPI_SETS : 1;
+    static constexpr int kSetWarps = kEpiWarps / kSets;      // warps per tile
+    static constexpr int kParts = kSetWarps / 4;             // column parts per tile
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
-    static constexpr int kColsPerWarp = NT * 4 / kEpiWarps;
+    static constexpr int kColsPerWarp = NT * 4 / kSetWarps;
     static constexpr int kRow = KA + K2 + (kNoExt ? 0 : 16);   // operand row: L1 | L2 | size chunk
     static constexpr int kKCT = kRow / 16;                     // 16-byte chunks per row
     static constexpr int kSbo = kKCT * 128;                    // stride between 8-row core groups
@@ -578,6 +588,7 @@ struct TcLayout {
     static_assert(kBytes + 1024 + 4 * kTcLut + 512 <= 232448, "shared memory per CTA");
     static_assert(KIND == kKindI8 || kAccCols + 128 <= 512, "TMEM: accumulators + scale factors");
     static_assert(kAccCols <= 512 && kAccSlots >= 2, "TMEM");
+    static_assert(kSets == 1 || (kEarlyB && kAccSlots % kSets == 0), "epilogue sets need early B release");
 };
 
 template <int KIND, int KA, int K2, int W2, int NS, int NT>
@@ -617,7 +628,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         }
         for (int s = 0; s < L::kAccSlots; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], kTcEpiWarps);
+            mbar_init(&acc_empty[s], L::kSetWarps);
         }
         for (int s = 0; s < L::NE; ++s) {
             mbar_init(&e_full[s], 1);
@@ -696,8 +707,12 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         tma_load_1d(side, P.sizes + col, NT * 4, &e_full[se]);
                         tma_load_1d(side + NT * 4, P.npc2 + col / 2, NT * 2, &e_full[se]);
                     }
-                    mbar_expect_tx(&b_full[st], L::kB);
-                    tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
+                    if ((P.debug & 8) && tseq >= NS) {  // (probe bit 8: stale B stages, no copies)
+                        mbar_arrive(&b_full[st]);
+                    } else {
+                        mbar_expect_tx(&b_full[st], L::kB);
+                        tma_load_1d(dst, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
+                    }
                     if (t == 0) {
                         nxt = claim_tc(P);
                         nxt_tile = nxt != kNoItem ? P.item_tile[nxt] : 0u;
@@ -745,7 +760,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if constexpr (K2 > 0) {
                         const uint32_t d2 = tmem_base + L::kL2Col + as * NT;
 #pragma unroll
-                        for (int s = 0; s < K2 / 32; ++s)
+                        for (int s = 0; s < ((P.debug & 4) ? 1 : K2 / 32); ++s)  // (probe bit 4: one L2 MMA)
                             umma_i8<NT>(d2, umma_desc(a0 + KA * 8 + s * 256, L::kSbo),
                                         umma_desc(b0 + KA * 8 + s * 256, L::kSbo), s > 0);
                     }
@@ -760,7 +775,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         // ------------------------------------------------------------ epilogue
         const int ew = warp - 2;
         const int quarter = warp & 3;          // TMEM lanes 32*quarter .. +31 (hardware rule)
-        const int part = ew >> 2;              // this warp's column range of each tile
+        const int eset = ew / L::kSetWarps;    // the tiles (accumulator slots) this warp takes
+        const int part = (ew % L::kSetWarps) >> 2;  // this warp's column range of each tile
         const int rit = quarter * 32 + lane;   // row in tile
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         uint2* q = sQ + ew * kTcQueue;
@@ -819,12 +835,30 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
             uint32_t last_sz = 0xFFFFFFFFu;  // cim1 cache: sizes are sorted, so it rarely changes
             int cim1 = 0, cim1_2 = 0, cim1_key = 0;
             for (uint32_t t = 0; t < info.ntiles; ++t) {
+                if constexpr (L::kSets > 1) {
+                    if (static_cast<int>(acc_idx % L::kSets) != eset) {  // the other set's tile
+                        if (++st_idx == NS) {
+                            st_idx = 0;
+                            st_phase ^= 1u;
+                        }
+                        if (++acc_idx == L::kAccSlots) {
+                            acc_idx = 0;
+                            acc_phase ^= 1u;
+                        }
+                        continue;
+                    }
+                }
                 const int st = static_cast<int>(st_idx), as = static_cast<int>(acc_idx);
                 if constexpr (L::kNoExt) mbar_wait_u32(smem_u32(&e_full[0]) + 8 * se_idx, se_phase);
                 else if constexpr (!L::kEarlyB) mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
                 // (early-released stages: the accumulator's completion implies the
                 // operands arrived; sizes come from gsz below)
                 const uint32_t* gsz = P.sizes + info.c0 + t * NT;
+                // level-2 GEMM kernel, one 32-column group per warp: the packed
+                // group loads are the warp's only TMEM reads of the tile, so the slot
+                // is released as soon as they land (SSJB_EARLY_ACC=0: at tile end)
+                constexpr bool kEarlyAcc = K2 > 0 && KIND == kKindI8 && L::kColsPerWarp == 32 && SSJB_EARLY_ACC;
+                bool acc_released = false;
                 uint32_t pre0 = 0, pre1 = 0;
                 if constexpr (L::kEarlyB) {  // issue the size loads before the accumulator wait
                     pre0 = __ldg(gsz + part * L::kColsPerWarp);
@@ -928,6 +962,14 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                                                     : (L::kEarlyB ? __ldg(gsz + cl + lane)
                                                                   : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cl + lane));
                         tmem_wait_ld();
+                        if constexpr (kEarlyAcc) {
+                            // the warp's only group is in registers: hand the accumulator
+                            // slot back to the MMA issuer before the masks and emission
+                            asm volatile("tcgen05.fence::before_thread_sync;");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
+                            acc_released = true;
+                        }
                         if constexpr (L::kNoExt) {  // D - pc_j per column
                             const uint4* np = reinterpret_cast<const uint4*>(sNpc + cl / 2);
 #pragma unroll
@@ -1035,7 +1077,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 __syncwarp();
                 if (lane == 0) {
                     if (P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
-                    mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
+                    if (!acc_released) mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
                     if constexpr (L::kNoExt) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
                     else if constexpr (!L::kEarlyB) mbar_arrive_u32(bempty_u32 + 8 * st_idx);
                 }

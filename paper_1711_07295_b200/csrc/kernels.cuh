@@ -1128,6 +1128,156 @@ __global__ void verify_rs(VerifyRsParams P) {
     }
 }
 
+// ================================================ K2/K3 (RS): filtered R x S
+// NAIVE RS-join through the Bitmap Filter (round 2): the reference verifies
+// every (r, s) (src/join.cpp:110-121); here only the pairs that survive a
+// length window (S is size-sorted: per R size an S index range) and the
+// b-bit Xor sketch bound popcount(b_r ^ b_s) <= maxham[|r|+|s|] are merged.
+// Both tests are sound for every similarity function whose required overlap
+// depends on |r|+|s| (Jaccard, Dice, Overlap), so the matches -- and the
+// NAIVE counters, candidates = verified = |R||S| -- are unchanged.
+struct RsFilterParams {
+    const uint64_t* bits_r;    // R sketches, words per row
+    const uint64_t* bits_s;    // S sketches
+    const uint32_t* sizes_r;
+    const uint32_t* sizes_s;
+    const uint32_t* s_lo;      // per R size: first S index of the length window
+    const uint32_t* s_hi;      // per R size: end of the window
+    const int32_t* maxham;     // maxham[|r| + |s|]
+    const uint2* items;        // (R row tile, S column chunk of kColChunk)
+    uint32_t r_begin, r_end, n_s;
+    int words;                 // 1 or 2
+    uint2* surv;               // (s, r)
+    unsigned long long surv_cap, surv_soft;
+    unsigned long long item_begin, item_end;
+    Control* ctl;
+};
+
+constexpr int kRsCols = 1024;  // S columns staged in shared memory per step
+
+__global__ void __launch_bounds__(kRowTile) rs_filter(RsFilterParams P) {
+    __shared__ uint64_t s_bits[kRsCols * 2];
+    __shared__ uint32_t s_size[kRsCols];
+    __shared__ unsigned long long s_item;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = claim_item(P.ctl, P.item_begin, P.item_end, P.surv_soft);
+        __syncthreads();
+        const unsigned long long it = s_item;
+        __syncthreads();
+        if (it >= P.item_end) break;
+        const uint2 w = P.items[it];
+        const uint32_t i = P.r_begin + w.x * kRowTile + threadIdx.x;
+        const bool valid = i < P.r_end;
+        uint32_t si = 0, lo = 0, hi = 0;
+        uint64_t m0 = 0, m1 = 0;
+        if (valid) {
+            si = P.sizes_r[i];
+            lo = P.s_lo[si];
+            hi = P.s_hi[si];
+            m0 = P.bits_r[static_cast<uint64_t>(i) * P.words];
+            if (P.words == 2) m1 = P.bits_r[static_cast<uint64_t>(i) * 2 + 1];
+        }
+        const uint32_t c0 = w.y * kColChunk, c1 = min(c0 + kColChunk, P.n_s);
+        for (uint32_t cb = c0; cb < c1; cb += kRsCols) {
+            const uint32_t ce = min(cb + kRsCols, c1);
+            for (uint32_t k = threadIdx.x; k < ce - cb; k += blockDim.x) {
+                s_size[k] = P.sizes_s[cb + k];
+                s_bits[2 * k] = P.bits_s[static_cast<uint64_t>(cb + k) * P.words];
+                s_bits[2 * k + 1] = P.words == 2 ? P.bits_s[static_cast<uint64_t>(cb + k) * 2 + 1] : 0ull;
+            }
+            __syncthreads();
+            const uint32_t jl = valid ? max(lo, cb) : ce, jh = valid ? min(hi, ce) : ce;
+            uint32_t wl = jl, wh = jh;  // warp-uniform bounds
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wl = min(wl, __shfl_xor_sync(0xFFFFFFFFu, wl, o));
+                wh = max(wh, __shfl_xor_sync(0xFFFFFFFFu, wh, o));
+            }
+            for (uint32_t j = wl; j < wh; ++j) {
+                const uint32_t k = j - cb;
+                const int h = __popcll(m0 ^ s_bits[2 * k]) + __popcll(m1 ^ s_bits[2 * k + 1]);
+                const bool pass = j >= jl && j < jh && h <= __ldg(P.maxham + si + s_size[k]);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pass);
+                if (!bal) continue;
+                unsigned long long base = 0;
+                if (lane == __ffs(bal) - 1) base = atomicAdd(&P.ctl->survivors, static_cast<unsigned long long>(__popc(bal)));
+                base = __shfl_sync(0xFFFFFFFFu, base, __ffs(bal) - 1) + __popc(bal & ((1u << lane) - 1u));
+                if (pass && base < P.surv_cap) P.surv[base] = make_uint2(j, i);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Exact verification of filtered RS survivors (s, r): thread per pair, the
+// merge with early exit of reference src/similarity.cpp:168-185; matches
+// keyed (r << 32) | s.
+struct VerifyRsPairsParams {
+    const uint32_t* ta;
+    const uint64_t* oa;   // R
+    const uint32_t* tb;
+    const uint64_t* ob;   // S
+    SimNeed need;
+    const uint2* surv;
+    const unsigned long long* count_ptr;
+    unsigned long long count_cap;
+    unsigned long long* res_keys;
+    uint32_t* res_ov;
+    unsigned long long res_cap;
+    Control* ctl;
+};
+
+__global__ void verify_rs_pairs(VerifyRsPairsParams P) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long count = min(*P.count_ptr, P.count_cap);
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < count;
+         base += stride) {
+        const unsigned long long k = base + threadIdx.x;
+        bool matched = false;
+        uint32_t r = 0, sidx = 0, ov = 0;
+        unsigned long long vb = 0;
+        if (k < count) {
+            const uint2 pr = P.surv[k];
+            sidx = pr.x;
+            r = pr.y;
+            const uint64_t ab = P.oa[r], ae = P.oa[r + 1];
+            const uint64_t bb = P.ob[sidx], be = P.ob[sidx + 1];
+            const uint32_t na = static_cast<uint32_t>(ae - ab), nb = static_cast<uint32_t>(be - bb);
+            const int32_t need = need_overlap(P.need, na, nb);
+            const uint32_t* A = P.ta + ab;
+            const uint32_t* B = P.tb + bb;
+            uint32_t ia = 0, ib = 0;
+            int32_t o = 0;
+            while (ia < na && ib < nb) {
+                const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
+                if (o + rest < need) break;
+                const uint32_t x = __ldg(A + ia), y = __ldg(B + ib);
+                o += x == y;
+                ia += x <= y;
+                ib += y <= x;
+            }
+            matched = o >= need;
+            ov = static_cast<uint32_t>(o);
+            vb = 4ull * (na + nb) + (matched ? 16 : 0);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
+        if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, matched);
+        if (bal) {
+            unsigned long long slot = 0;
+            if (lane == 0) slot = atomicAdd(&P.ctl->results, static_cast<unsigned long long>(__popc(bal)));
+            slot = __shfl_sync(0xFFFFFFFFu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
+            if (matched && slot < P.res_cap) {
+                P.res_keys[slot] = (static_cast<unsigned long long>(r) << 32) | sidx;
+                P.res_ov[slot] = ov;
+            }
+        }
+    }
+}
+
 // ============================================================ K4: radix sort
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;                       // keys per thread per tile

@@ -69,7 +69,12 @@ def test_rs_join_rejects_non_naive_algorithms(lib):
 
 
 @pytest.mark.gpu
-def test_gpu_naive_joins_match_reference(lib, rs_golden):
+@pytest.mark.parametrize("mode", ["filtered", "brute"])
+def test_gpu_naive_joins_match_reference(lib, rs_golden, mode, monkeypatch):
+    """Every reference NAIVE fixture; RS-joins through the filtered R x S path
+    (length window + Xor sketch bound, forced on) and through the brute-force
+    merge of every pair."""
+    monkeypatch.setenv("SSJB_RS_FILTER", "2" if mode == "filtered" else "0")
     cases, arrs = rs_golden
     colls = {}
 
@@ -91,7 +96,27 @@ def test_gpu_naive_joins_match_reference(lib, rs_golden):
 
 
 @pytest.mark.gpu
-def test_gpu_rs_join_batches_and_result_overflow(lib, oracle, monkeypatch):
+def test_gpu_filtered_rs_join_merges_far_fewer_pairs(lib, monkeypatch):
+    """30,000 x 30,000 Zipf-token records at Jaccard 0.6: the filtered RS path
+    returns the brute-force pair list and NAIVE's counters while merging at
+    least 100x fewer pairs (ssjb_stats.survivors)."""
+    r = S.Collection.generate(lib, 30000, 10, 1000, 41, capi.SSJ_DIST_ZIPF, 1.0)
+    s = S.Collection.generate(lib, 30000, 10, 1000, 42, capi.SSJ_DIST_ZIPF, 1.0)
+    opts = S.default_options(lib, algorithm=capi.SSJ_ALGO_NAIVE, threshold=(3, 5))
+    monkeypatch.setenv("SSJB_RS_FILTER", "0")
+    brute = S.join(r, opts, s)
+    monkeypatch.setenv("SSJB_RS_FILTER", "2")
+    filt = S.join(r, opts, s)
+    assert brute.pairs.tobytes() == filt.pairs.tobytes()
+    assert filt.counters == brute.counters
+    assert filt.counters["candidates"] == 30000 * 30000 == filt.counters["verified"]
+    assert filt.extra["survivors"] * 100 <= 30000 * 30000, filt.extra
+    print(f"filtered RS: {len(filt.pairs)} pairs, {filt.extra['survivors']} merges of {30000 * 30000}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["filtered", "brute"])
+def test_gpu_rs_join_batches_and_result_overflow(lib, oracle, monkeypatch, mode):
     """Small launch ranges and a tiny result buffer force many runs and
     overflow redos; the concatenated runs must still be the canonical list."""
     r = S.Collection.generate(lib, 900, 10, 80, 31)
@@ -104,7 +129,8 @@ def test_gpu_rs_join_batches_and_result_overflow(lib, oracle, monkeypatch):
     assert (base.pairs == want).all() and base.counters["matched"] == cnt["matched"]
     monkeypatch.setenv("SSJB_RS_BATCH", "50000")
     monkeypatch.setenv("SSJB_RESULT_CAP", "1024")
+    monkeypatch.setenv("SSJB_RS_FILTER", "2" if mode == "filtered" else "0")
     rep = S.join(r, opts, s)
     assert len(rep.pairs) == len(want) and (rep.pairs == want).all()
-    assert rep.extra["batches"] > 10
+    assert rep.extra["batches"] >= (1 if mode == "filtered" else 11)
     assert rep.counters["candidates"] == 900 * 700 == rep.counters["verified"]
