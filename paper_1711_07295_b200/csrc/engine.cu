@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -962,6 +963,157 @@ void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
             if (a < b) th.emplace_back([=]() { std::memcpy(out + a, buf + a, b - a); });
         }
         std::memcpy(out, buf, std::min(len, piece));
+        for (auto& x : th) x.join();
+    }
+}
+
+// ------------------------------------------------- result block cache
+}  // namespace
+
+namespace {
+struct ResultBlockCache {
+    std::mutex mu;
+    std::map<void*, size_t> live;                 // block -> capacity
+    std::multimap<size_t, void*> idle;            // capacity -> block
+    std::map<void*, size_t> pinned;               // page-locked blocks (live or idle)
+    size_t idle_bytes = 0;
+};
+ResultBlockCache& result_cache() {
+    static ResultBlockCache* c = new ResultBlockCache();  // leaked: outlives static teardown
+    return *c;
+}
+size_t result_cache_budget() {
+    static const size_t b = static_cast<size_t>(env_u64("SSJB_RESULT_CACHE_MB", 4096)) << 20;
+    return b;
+}
+}  // namespace
+
+void* result_block_alloc(size_t bytes) {
+    ResultBlockCache& C = result_cache();
+    {
+        std::lock_guard<std::mutex> lk(C.mu);
+        auto it = C.idle.lower_bound(bytes);
+        if (it != C.idle.end() && it->first <= 2 * bytes) {
+            void* p = it->second;
+            C.live[p] = it->first;
+            C.idle_bytes -= it->first;
+            C.idle.erase(it);
+            return p;
+        }
+    }
+    const size_t cap = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    void* p = std::aligned_alloc(size_t(2) << 20, cap);
+    if (!p) throw std::bad_alloc();
+    madvise(p, cap, MADV_HUGEPAGE);  // first touch in 2 MB pages
+    std::lock_guard<std::mutex> lk(C.mu);
+    C.live[p] = cap;
+    return p;
+}
+
+void result_block_free(void* p) {
+    if (!p) return;
+    ResultBlockCache& C = result_cache();
+    std::unique_lock<std::mutex> lk(C.mu);
+    auto it = C.live.find(p);
+    if (it == C.live.end()) return;
+    const size_t cap = it->second;
+    C.live.erase(it);
+    if (C.idle_bytes + cap <= result_cache_budget()) {
+        if (!C.pinned.count(p)) {
+            // page-lock once (its pages are faulted in by now); later results
+            // reuse it and the device copies into it directly
+            lk.unlock();
+            const bool ok = cudaHostRegister(p, cap, cudaHostRegisterPortable) == cudaSuccess;
+            if (!ok) cudaGetLastError();
+            lk.lock();
+            if (ok) C.pinned[p] = cap;
+        }
+        C.idle.emplace(cap, p);
+        C.idle_bytes += cap;
+        return;
+    }
+    if (C.pinned.count(p)) {
+        C.pinned.erase(p);
+        lk.unlock();
+        cudaHostUnregister(p);
+    } else {
+        lk.unlock();
+    }
+    std::free(p);
+}
+
+bool result_block_pinned(const void* p, size_t bytes) {
+    ResultBlockCache& C = result_cache();
+    std::lock_guard<std::mutex> lk(C.mu);
+    auto it = C.pinned.upper_bound(const_cast<void*>(p));
+    if (it == C.pinned.begin()) return false;
+    --it;
+    const uint8_t* b = static_cast<const uint8_t*>(it->first);
+    return static_cast<const uint8_t*>(p) >= b && static_cast<const uint8_t*>(p) + bytes <= b + it->second;
+}
+
+namespace {
+
+// Sorted (key, overlap) results straight to ssj_pair records in host memory:
+// the keys (8 B) and overlaps (4 B) travel as they are -- 12 B per pair instead
+// of the 16 B packed record -- through double-buffered pinned staging, and the
+// host threads that copy each chunk out widen it into (id_r, id_s, i64) records.
+void d2h_pairs_staged(PairOut* dst, const unsigned long long* keys, const uint32_t* ov, uint64_t n, cudaStream_t s,
+                      PairOut* dev_scratch = nullptr) {
+    if (dev_scratch && n && result_block_pinned(dst, n * sizeof(PairOut))) {
+        // a cached, page-locked result block: pack on the device, one DMA into it
+        pack_pairs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(keys, ov, dev_scratch, n);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(dst, dev_scratch, n * sizeof(PairOut), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return;
+    }
+    constexpr uint64_t kChunk = uint64_t(4) << 20;  // pairs per staging chunk (48 MB)
+    if (n >= (uint64_t(1) << 20)) {
+        // fresh multi-GB result vectors: transparent huge pages for the first touch
+        const uintptr_t a = (reinterpret_cast<uintptr_t>(dst) + (size_t(2) << 20) - 1) & ~((uintptr_t(2) << 20) - 1);
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(dst) + n * sizeof(PairOut)) & ~((uintptr_t(2) << 20) - 1);
+        if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    }
+    static thread_local uint8_t* stage[2] = {nullptr, nullptr};
+    static thread_local cudaEvent_t ev[2];
+    if (!stage[0]) {
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), kChunk * 12, cudaHostAllocPortable));
+            CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+        }
+    }
+    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+    auto issue = [&](uint64_t k) {
+        const uint64_t off = k * kChunk, len = std::min(kChunk, n - off);
+        uint8_t* st = stage[k & 1];
+        CK(cudaMemcpyAsync(st, keys + off, len * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(st + kChunk * 8, ov + off, len * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[k & 1], s));
+    };
+    static const unsigned max_threads = static_cast<unsigned>(env_u64("SSJB_D2H_THREADS", 32));
+    const unsigned nthreads = std::max(1u, std::min(max_threads, std::thread::hardware_concurrency()));
+    if (nchunks) issue(0);
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        if (k + 1 < nchunks) issue(k + 1);
+        CK(cudaEventSynchronize(ev[k & 1]));
+        const uint64_t off = k * kChunk, len = std::min(kChunk, n - off);
+        const unsigned long long* kk = reinterpret_cast<const unsigned long long*>(stage[k & 1]);
+        const uint32_t* oo = reinterpret_cast<const uint32_t*>(stage[k & 1] + kChunk * 8);
+        PairOut* out = dst + off;
+        auto widen = [=](uint64_t a, uint64_t b) {
+            for (uint64_t x = a; x < b; ++x)
+                out[x] = PairOut{static_cast<uint32_t>(kk[x] >> 32), static_cast<uint32_t>(kk[x] & 0xFFFFFFFFu),
+                                 static_cast<int64_t>(oo[x])};
+        };
+        const unsigned T = len >= (uint64_t(1) << 16) ? nthreads : 1u;
+        const uint64_t piece = (len + T - 1) / T;
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < T; ++t) {
+            const uint64_t a = std::min(len, t * piece), b = std::min(len, a + piece);
+            if (a < b) th.emplace_back(widen, a, b);
+        }
+        widen(0, std::min(len, piece));
         for (auto& x : th) x.join();
     }
 }
@@ -2170,19 +2322,14 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
             return;
         }
-        PairOut* packed = count ? A.alloc<PairOut>(count) : nullptr;
-        if (count) {
-            pack_pairs<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(inb ? SB.kb : SB.ka,
-                                                                              inb ? SB.vb : SB.va, packed, count);
-            ++st.launches;
-            CK(cudaGetLastError());
-        }
         cudaEvent_t b = T.mark();
         PairVec run(count);
-        d2h_staged(run.data(), packed, count * sizeof(PairOut), s);
+        const bool direct = count && result_block_pinned(run.data(), count * sizeof(PairOut));
+        d2h_pairs_staged(run.data(), inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va, count, s,
+                         direct ? A.alloc<PairOut>(count) : nullptr);
         cudaEvent_t d = T.mark();
         CK(cudaStreamSynchronize(s));
-        st.d2h_bytes += count * sizeof(PairOut);
+        st.d2h_bytes += count * (direct ? sizeof(PairOut) : 12);
         st.ms_sort += Timer::ms(a, b);
         st.ms_download += Timer::ms(b, d);
         runs.push_back(std::move(run));

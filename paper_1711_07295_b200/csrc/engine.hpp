@@ -23,6 +23,16 @@ struct PairOut {  // layout of ssj_pair (reference include/ssjoin.h:125-129)
 };
 static_assert(sizeof(PairOut) == 16, "ssj_pair layout");
 
+// Large result blocks (>= 64 MB): a process-wide cache of page-locked host
+// blocks (engine.cu).  A freed block is kept (pinned, pages already faulted
+// in) up to SSJB_RESULT_CACHE_MB (default 4096) and handed to the next large
+// result, so repeated joins neither zero fresh pages nor stage their
+// downloads: the device copies straight into the result.
+void* result_block_alloc(size_t bytes);
+void result_block_free(void* p);
+bool result_block_pinned(const void* p, size_t bytes);  // p..p+bytes inside a pinned cached block
+constexpr size_t kResultBlockMin = size_t(64) << 20;
+
 // Allocator that leaves trivially-constructible elements uninitialised: result
 // vectors of 1e8+ pairs are filled by device copies, not zeroed first.
 template <class T>
@@ -34,6 +44,14 @@ struct DefaultInitAlloc : std::allocator<T> {
     DefaultInitAlloc() = default;
     template <class U>
     DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+    T* allocate(size_t n) {
+        if (n * sizeof(T) >= kResultBlockMin) return static_cast<T*>(result_block_alloc(n * sizeof(T)));
+        return std::allocator<T>::allocate(n);
+    }
+    void deallocate(T* p, size_t n) {
+        if (n * sizeof(T) >= kResultBlockMin) return result_block_free(p);
+        std::allocator<T>::deallocate(p, n);
+    }
     template <class U>
     void construct(U* p) noexcept {
         ::new (static_cast<void*>(p)) U;

@@ -38,6 +38,11 @@ namespace dev {
 #ifndef SSJB_EARLY_ACC
 #define SSJB_EARLY_ACC 1
 #endif
+// pipeline trace probe (SSJB_TC_DEBUG=2) compiled in only with -DSSJB_TRACE=1:
+// its per-tile checks cost the hot loops a handful of instructions each
+#ifndef SSJB_TRACE
+#define SSJB_TRACE 0
+#endif
 constexpr int kTcQueue = 128;      // survivor staging per epilogue warp
 constexpr int kTcLut = 1536;       // shared-memory copy of maxham[] (entries)
 constexpr int kKindI8 = 0;         // tcgen05 kind::i8, s32 accumulators
@@ -556,12 +561,12 @@ struct TcLayout {
     // each for the level-2 GEMM's 128-column tiles (the per-tile fixed cost of a
     // warp -- barrier waits, column sizes, thresholds -- paid by 8 warps, not 16)
     static constexpr int kEpiWarps = NT == 192 ? 12 : 16;
-    // level-2 GEMM kernel: the epilogue is latency-bound per warp, so its 16
-    // warps form two sets that take alternate tiles (the two accumulator
-    // slots) -- each warp has two tile intervals for 64 columns instead of one
-    // for 32 (SSJB_L2_EPI_SETS=1: every warp on every tile)
+    // level-2 GEMM kernel: SSJB_L2_EPI_SETS=2 splits the 16 epilogue warps into
+    // two sets taking alternate tiles (accumulator slots), 64 columns per warp
+    // and two tile intervals each; measured neutral on C4 (162 vs 160 ms), so
+    // the default keeps every warp on every tile
 #ifndef SSJB_L2_EPI_SETS
-#define SSJB_L2_EPI_SETS 2
+#define SSJB_L2_EPI_SETS 1
 #endif
     static constexpr int kSets = (K2 > 0 && NT == 128) ? SSJB_L2_EPI_SETS : 1;
     static constexpr int kSetWarps = kEpiWarps / kSets;      // warps per tile
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     uint8_t* dst = sB + st * L::kB;
                     if constexpr (L::kNoExt) {
@@ -742,9 +747,9 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     const int st = tseq % NS;
                     const int as = aseq % L::kAccSlots;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
                     mbar_spin(&acc_empty[as], ((aseq / L::kAccSlots) & 1) ^ 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
@@ -866,7 +871,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 }
                 mbar_wait_u32(accfull_u32 + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512) P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
+                if (SSJB_TRACE && P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512) P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
                 ++tile_seq;
                 const uint8_t* stage = sB + st * L::kB;
                 const uint32_t* side_sz = reinterpret_cast<const uint32_t*>(sSide + se_idx * L::kSide);
@@ -1000,7 +1005,13 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                             // biased accumulators: SWAR masks in the permuted bit order
                             perm = true;
                             if (!bypass) m = mask16_32_nonneg(d, cim1);
-                            if constexpr (K2 > 0) e2 = mask16_32_nonneg(d2, cim1_2);
+                            if constexpr (K2 > 0) {
+                                // level-2 survivors are rare: the mask only when a lane has one
+                                // (max over the packed accumulators, three-input VIMNMX)
+                                e2 = __any_sync(0xFFFFFFFFu, m != 0 && any_above16_32(d2, max(cim1_2, -32768)))
+                                         ? mask16_32_nonneg(d2, cim1_2)
+                                         : 0u;
+                            }
                         } else if (fast) {
                             if (!bypass) m = mask16_32(d, max(cim1, -32768));
                             if constexpr (K2 > 0) e2 = mask16_32(d2, max(cim1_2, -32768));
@@ -1076,7 +1087,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) {
-                    if (P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
                     if (!acc_released) mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
                     if constexpr (L::kNoExt) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
                     else if constexpr (!L::kEarlyB) mbar_arrive_u32(bempty_u32 + 8 * st_idx);

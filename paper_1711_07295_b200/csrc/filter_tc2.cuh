@@ -225,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     mbar_expect_tx(&b_full[st], L::kB + L::kSz);
                     tma_load_1d(sB + st * L::kB, P.opB + static_cast<uint64_t>(col + rank * kRowTile) * KA, L::kB,
@@ -269,9 +269,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                     const int as = aseq & 1;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
                     mbar_wait_cl(smem_u32(&b_peer[st]), (tseq / NS) & 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
                     mbar_wait_cl(smem_u32(&acc_empty[as]), ((aseq >> 1) & 1) ^ 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
@@ -335,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 mbar_wait_u32(smem_u32(&b_full[0]) + 8 * st_idx, st_phase);
                 mbar_wait_u32(smem_u32(&acc_full[0]) + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                if (P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512)
+                if (SSJB_TRACE && P.trace && blockIdx.x == 0 && lane == 0 && tile_seq < 512)
                     P.trace[2048 + tile_seq * 16 + (warp - 2)] = clock64();
                 const uint32_t* szs = sSz + st_idx * NT;
                 const int cw = part * L::kColsPerWarp;
@@ -399,7 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((Tc2Layout<KA, NS>::
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) {
-                    if (P.trace && blockIdx.x == 0 && tile_seq < 512)
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tile_seq < 512)
                         P.trace[2048 + 8192 + tile_seq * 16 + (warp - 2)] = clock64();
                     if (leader) mbar_arrive(&acc_empty[acc_idx]);
                     else mbar_arrive_cluster_relaxed(L_acc_empty + 8 * acc_idx);

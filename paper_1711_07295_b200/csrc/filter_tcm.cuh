@@ -193,7 +193,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                     const int st = tseq % NS;
                     mbar_spin(&b_empty[st], ((tseq / NS) & 1) ^ 1);
                     const uint32_t col = info.c0 + t * NT;
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     mbar_expect_tx(&b_full[st], L::kB);
                     tma_load_1d(sB + st * L::kB, P.opB + static_cast<uint64_t>(col) * L::kRow, L::kB, &b_full[st]);
                 }
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++useq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
                     const uint32_t b0 = smem_u32(sB + st * L::kB);
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                         umma_commit(&acc_full[r]);
                     }
                     umma_commit(&b_empty[st]);
-                    if (P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
+                    if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                 }
                 umma_commit(&a_empty[aslot]);
                 ++iseq;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                     __syncwarp();
                     if (lane == 0) mbar_arrive_u32(smem_u32(&acc_empty[0]) + 8 * r);
                 }
-                if (P.trace && blockIdx.x == 0 && lane == 0 && useq < 512)
+                if (SSJB_TRACE && P.trace && blockIdx.x == 0 && lane == 0 && useq < 512)
                     P.trace[2048 + 8192 + useq * 16 + ew] = clock64();
                 if (lane == 0) mbar_arrive_u32(smem_u32(&b_empty[0]) + 8 * st_idx);
                 if (++st_idx == NS) {
