@@ -364,6 +364,13 @@ class DeviceWorkers {
 
 int g_shards_per_device = 0;  // 0: env SSJB_SHARDS_PER_DEVICE, else 1
 
+// Relative per-pair cost of the head-overlap region vs the filter's window
+// pairs for row partitioning (C4: K2 ~0.34 ns / window pair, K3a ~2.7 ns / region pair).
+double head_weight() {
+    const char* v = std::getenv("SSJB_HEAD_WEIGHT");
+    return v && *v ? std::atof(v) : 8.0;
+}
+
 int shards_per_device() {
     if (g_shards_per_device > 0) return g_shards_per_device;
     const char* v = std::getenv("SSJB_SHARDS_PER_DEVICE");
@@ -387,23 +394,9 @@ std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, con
     if (shards == 1) {
         ssjb::engine_join(coll, whole, first_device, parts[0]);
     } else {
-        // balanced contiguous row blocks of the range (window-pair prefix sums)
-        std::vector<uint64_t> bounds(static_cast<size_t>(shards) + 1);
-        {
-            std::vector<double> pre(row_end - row_begin + 1, 0.0);
-            for (size_t i = row_begin; i < row_end; ++i) {
-                uint32_t j0 = ssjb::window_start_of(coll, whole, i);
-                pre[i - row_begin + 1] = pre[i - row_begin] + (j0 < i ? double(i - j0) : 0.0) + 1.0;
-            }
-            bounds[0] = row_begin;
-            for (int g = 1; g < shards; ++g) {
-                const double target = pre.back() * g / shards;
-                uint64_t b = row_begin + (std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
-                b = row_begin + ((b - row_begin) & ~uint64_t(127));  // 128-row tile boundaries
-                bounds[g] = std::max(b, bounds[g - 1]);
-            }
-            bounds[shards] = row_end;
-        }
+        // contiguous row blocks of the range balanced on the join's work
+        const std::vector<uint64_t> bounds = ssjb::partition_rows(
+            coll, whole, shards, row_begin, row_end, ssjb::engine_head_start(coll, whole), head_weight());
         std::vector<std::function<void()>> tasks;
         for (int g = 0; g < shards; ++g) {
             tasks.emplace_back([&, g]() {
@@ -896,7 +889,8 @@ SSJB_API ssj_status ssjb_partition_rows(const ssj_collection* coll, const ssj_jo
         ssjb::Options o = to_options(*opts);
         check_supported(o);
         ssjb::JoinPlan plan = ssjb::make_plan(*coll->c, o, 0, coll->c->size());
-        auto b = ssjb::partition_rows(*coll->c, plan, parts);
+        auto b = ssjb::partition_rows(*coll->c, plan, parts, 0, coll->c->size(),
+                                      ssjb::engine_head_start(*coll->c, plan), head_weight());
         std::copy(b.begin(), b.end(), bounds);
         return SSJ_OK;
     });

@@ -1884,6 +1884,14 @@ struct WorkspaceLease {
 };
 }  // namespace
 
+uint32_t engine_head_start(const Collection& c, const JoinPlan& plan) {
+    const int W = plan.bitmap.enabled ? plan.bitmap.width / 64 : 0;
+    const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
+    if (!plan.bitmap.enabled || W < 1 || W > 2 || !set_or_xor || plan.bitmap.width % 64) return UINT32_MAX;
+    const HeadPlan h = make_head_plan(c, plan, level2_words(W));
+    return h.ok ? h.L0 : UINT32_MAX;
+}
+
 // Frees every idle join workspace of `device` (all devices for -1).
 void engine_trim(int device) {
     WorkspacePool& P = workspace_pool();

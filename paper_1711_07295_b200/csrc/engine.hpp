@@ -109,5 +109,8 @@ void engine_pin(const Collection& c, int device);
 void engine_unpin(const Collection& c, int device);
 void engine_release_host(const Collection& c);  // undo host page registration
 void engine_trim(int device);                   // free idle join workspaces (-1: all devices)
+// First record of the head-overlap region (K3a) the join of `plan` over the
+// whole collection would use, or UINT32_MAX (for work-balanced row shards).
+uint32_t engine_head_start(const Collection& c, const JoinPlan& plan);
 
 }  // namespace ssjb

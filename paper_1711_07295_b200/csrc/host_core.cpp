@@ -880,30 +880,39 @@ JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size
     return plan;
 }
 
-std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, int parts) {
+std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, int parts, size_t row_begin,
+                                     size_t row_end, uint32_t head_L0, double head_weight) {
     if (parts < 1) throw std::invalid_argument("parts must be >= 1");
     const size_t n = c.size();
-    std::vector<uint64_t> bounds(static_cast<size_t>(parts) + 1, n);
-    bounds[0] = 0;
-    uint64_t total = 0;
-    for (size_t i = 0; i < n; ++i) {
-        uint32_t j0 = window_start_of(c, plan, i);
-        total += j0 < i ? i - j0 : 0;
-    }
-    // cut where the running window-pair sum crosses g*total/parts (+1 per row
-    // so empty-window rows still spread)
-    const double per = (static_cast<double>(total) + static_cast<double>(n)) / parts;
+    row_end = std::min(row_end, n);
+    row_begin = std::min(row_begin, row_end);
+    std::vector<uint64_t> bounds(static_cast<size_t>(parts) + 1, row_end);
+    bounds[0] = row_begin;
+    // per-row work: its window pairs (+1 so empty-window rows still spread),
+    // plus head_weight x its pairs in the head-overlap region (rows and
+    // columns >= head_L0: K3a's per-pair cost is several times K2's)
+    auto work = [&](size_t i) {
+        const uint32_t j0 = window_start_of(c, plan, i);
+        double w = static_cast<double>(j0 < i ? i - j0 : 0) + 1.0;
+        if (i >= head_L0) {
+            const size_t lo = std::max<size_t>(head_L0, j0);
+            if (i > lo) w += head_weight * static_cast<double>(i - lo);
+        }
+        return w;
+    };
+    double total = 0;
+    for (size_t i = row_begin; i < row_end; ++i) total += work(i);
+    const double per = total / parts;
     double run = 0;
     int g = 1;
-    for (size_t i = 0; i < n && g < parts; ++i) {
-        uint32_t j0 = window_start_of(c, plan, i);
-        run += static_cast<double>(j0 < i ? i - j0 : 0) + 1.0;
+    for (size_t i = row_begin; i < row_end && g < parts; ++i) {
+        run += work(i);
         while (g < parts && run >= per * g) bounds[static_cast<size_t>(g++)] = i + 1;
     }
     // shard starts on 128-row tile boundaries (the filter's row tile and the
     // tensor-core operand layout want 8-aligned row blocks)
     for (int k = 1; k < parts; ++k) {
-        uint64_t b = bounds[static_cast<size_t>(k)] & ~uint64_t(127);
+        uint64_t b = row_begin + ((bounds[static_cast<size_t>(k)] - row_begin) & ~uint64_t(127));
         bounds[static_cast<size_t>(k)] = std::max(b, bounds[static_cast<size_t>(k - 1)]);
     }
     return bounds;

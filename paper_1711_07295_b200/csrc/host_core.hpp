@@ -193,7 +193,11 @@ RsPlan make_rs_plan(const Collection& r, const Collection& s, const Options& o, 
 
 uint32_t window_start_of(const Collection& c, const JoinPlan& plan, size_t row);
 JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size_t row_end);
-// Row boundaries of `parts` shards balancing the window pair count.
-std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, int parts);
+// Row boundaries of `parts` shards of rows [row_begin, row_end) balancing the
+// window pair count (+ head_weight x the pairs of the head-overlap region
+// starting at record head_L0, when the join will run it).
+std::vector<uint64_t> partition_rows(const Collection& c, const JoinPlan& plan, int parts, size_t row_begin = 0,
+                                     size_t row_end = SIZE_MAX, uint32_t head_L0 = UINT32_MAX,
+                                     double head_weight = 0.0);
 
 }  // namespace ssjb
