@@ -317,9 +317,10 @@ def run_ours(args):
         barrier_sync(world)
         t0 = time.perf_counter()
         reps = step(False)
-        if world > 1:
+        if world > 1:  # one node: runs meet in /dev/shm, rank 0 merges them (ssjb_merge_row_shards)
             for r in reps:
-                shard.gather_to_root(r.pairs, r.counters, r.saturated_records, group=gloo)
+                shard.gather_to_root_shm(r.pairs, r.counters, r.saturated_records, lib, group=gloo,
+                                         tag=f"ssjb_{os.environ.get('MASTER_PORT', '0')}")
         t1 = time.perf_counter()
         e2e_times.append((t1 - t0) * 1e3)
         h2d += sum(r.extra["h2d_bytes"] for r in reps)

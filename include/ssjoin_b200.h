@@ -52,6 +52,12 @@ ssj_status ssjb_set_devices(int count);
  * check of reference tests/test_parallel.cpp:37-59 on a one-GPU host. */
 ssj_status ssjb_set_shards_per_device(int count);
 
+/* Canonical merge of row-shard results: runs[k] (counts[k] pairs, each run
+ * sorted by (id_r, id_s)) are the results of ascending, disjoint row blocks of
+ * one self-join (e.g. one per rank of a multi-process join); out receives the
+ * sum of counts pairs in the reference's order.  O(pairs) on all host threads. */
+ssj_status ssjb_merge_row_shards(const ssj_pair* const* runs, const size_t* counts, int nruns, ssj_pair* out);
+
 /* Frees the idle join workspaces (survivor / result buffers a dense join grew
  * and the pool kept) of `device`, or of every device for -1.  Idle bytes kept
  * per device are bounded by env SSJB_WORKSPACE_KEEP_MB (default: 1/4 of HBM). */

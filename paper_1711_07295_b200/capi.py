@@ -132,6 +132,7 @@ _EXT_PROTOS = {
     "ssjb_set_devices": (C.c_int, [C.c_int]),
     "ssjb_set_shards_per_device": (C.c_int, [C.c_int]),
     "ssjb_trim": (C.c_int, [C.c_int]),
+    "ssjb_merge_row_shards": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int, C.c_void_p]),
     "ssjb_report_stats": (C.c_int, [P, C.POINTER(Stats)]),
     "ssjb_build_bitmaps": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
     "ssjb_time_build": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -914,6 +914,21 @@ SSJB_API ssj_status ssjb_set_shards_per_device(int count) {
     });
 }
 
+SSJB_API ssj_status ssjb_merge_row_shards(const ssj_pair* const* runs, const size_t* counts, int nruns,
+                                          ssj_pair* out) {
+    return guarded([&]() {
+        if (nruns < 0 || (nruns > 0 && (runs == nullptr || counts == nullptr)) || out == nullptr) {
+            set_error("null argument");
+            return SSJ_ERROR_INVALID_ARGUMENT;
+        }
+        std::vector<Seq> seqs;
+        for (int k = 0; k < nruns; ++k)
+            if (counts[k]) seqs.emplace_back(reinterpret_cast<const ssjb::PairOut*>(runs[k]), counts[k]);
+        merge_shards(seqs, reinterpret_cast<ssjb::PairOut*>(out));
+        return SSJ_OK;
+    });
+}
+
 SSJB_API ssj_status ssjb_trim(int device) {
     return guarded([&]() {
         ssjb::engine_trim(device);

@@ -42,6 +42,61 @@ def merge_counters(parts):
     return out, sat
 
 
+def merge_row_shards(lib, runs):
+    """Canonical merge of ascending row-block results through the library's
+    O(pairs) multi-threaded merge (ssjb_merge_row_shards)."""
+    import ctypes as C
+    from .ssjoin import PAIR_DTYPE
+    runs = [np.ascontiguousarray(r) for r in runs]
+    total = sum(len(r) for r in runs)
+    out = np.empty(total, dtype=PAIR_DTYPE)
+    if total == 0:
+        return out
+    ptrs = (C.c_void_p * len(runs))(*[r.ctypes.data if len(r) else None for r in runs])
+    counts = (C.c_size_t * len(runs))(*[len(r) for r in runs])
+    if lib.ssjb_merge_row_shards(ptrs, counts, len(runs), out.ctypes.data) != 0:
+        raise RuntimeError("ssjb_merge_row_shards failed")
+    return out
+
+
+def gather_to_root_shm(pairs, counters, saturated, lib, group=None, tag="ssjb"):
+    """Single-node gather through /dev/shm: every rank writes its sorted run to
+    a shared-memory file, rank 0 maps all of them (no copy through a socket)
+    and merges them with the library's row-shard merge.  Counters travel as
+    one int64 all-gather.  Returns (pairs, counters, saturated) on rank 0."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank()
+    world = dist.get_world_size()
+    head = torch.tensor([len(pairs), int(saturated)] + [int(counters.get(k, 0)) for k in COUNTER_KEYS],
+                        dtype=torch.int64)
+    heads = [torch.zeros_like(head) for _ in range(world)]
+    dist.all_gather(heads, head, group=group)
+    path = f"/dev/shm/{tag}_{rank}.bin"
+    if len(pairs):
+        np.ascontiguousarray(pairs).tofile(path)
+    dist.barrier(group=group)
+    out = None
+    if rank == 0:
+        from .ssjoin import PAIR_DTYPE
+        runs = []
+        for r in range(world):
+            c = int(heads[r][0])
+            if r == 0:
+                runs.append(pairs)
+            elif c:
+                runs.append(np.memmap(f"/dev/shm/{tag}_{r}.bin", dtype=PAIR_DTYPE, mode="r", shape=(c,)))
+        merged = merge_row_shards(lib, runs)
+        merged_counters, sat = merge_counters(
+            [({k: int(h[2 + i]) for i, k in enumerate(COUNTER_KEYS)}, int(h[1])) for h in heads])
+        out = (merged, merged_counters, sat)
+    dist.barrier(group=group)
+    if len(pairs):
+        import os
+        os.unlink(path)
+    return out
+
+
 def gather_to_root(pairs, counters, saturated, group=None):
     """Gather every rank's (pairs, counters, saturated) to rank 0 and merge.
     Count-first: the pair counts and counters travel as one small int64

@@ -56,7 +56,10 @@ def _worker(rank, world, port, q):
         counters = {"candidates": cnt["candidates"], "pruned_bitmap": cnt["pruned_bitmap"],
                     "bitmap_tested": cnt["bitmap_tested"], "verified": cnt["verified"], "matched": cnt["matched"]}
         merged = shard.gather_to_root(pairs, counters, cnt["saturated_records"])
+        via_shm = shard.gather_to_root_shm(pairs, counters, cnt["saturated_records"], lib,
+                                           tag=f"ssjb_test_{port}")
         if rank == 0:
+            assert (via_shm[0] == merged[0]).all() and via_shm[1] == merged[1] and via_shm[2] == merged[2]
             want, wcnt = O.par_bitmap_join(t, o, tau[0], tau[1], True, 1, 64, 0, O.INT64_MAX, cap)
             mp_pairs, mcnt, msat = merged
             ok = (len(mp_pairs) == len(want) and bool((mp_pairs == want).all())
@@ -97,3 +100,25 @@ def test_merge_runs_is_a_kway_merge():
         runs.append(np.sort(a, order=["id_r", "id_s"]))
     merged = shard.merge_runs(runs)
     assert [(int(p["id_r"]), int(p["id_s"]), int(p["overlap"])) for p in merged] == shard.heap_merge(runs)
+
+
+def test_library_row_shard_merge_is_the_canonical_order(lib):
+    """ssjb_merge_row_shards (the library's O(pairs) merge, capi.cpp merge_shards)
+    on runs of ascending disjoint row blocks == the (id_r, id_s) sort of their
+    union; large enough to split over several host threads."""
+    from paper_1711_07295_b200 import shard
+    from paper_1711_07295_b200.ssjoin import PAIR_DTYPE
+    rng = np.random.default_rng(5)
+    bounds = [0, 40000, 90000, 90000, 200000]  # one empty block
+    runs = []
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        m = int(rng.integers(0, 300000)) if b > a else 0
+        r = np.zeros(m, dtype=PAIR_DTYPE)
+        r["id_s"] = rng.integers(a, b, m) if m else []
+        r["id_r"] = (rng.random(m) * r["id_s"]).astype(np.uint32) if m else []
+        r["overlap"] = rng.integers(1, 50, m)
+        r = np.unique(r[r["id_r"] < r["id_s"]])
+        runs.append(np.sort(r, order=["id_r", "id_s"]))
+    got = shard.merge_row_shards(lib, runs)
+    want = np.sort(np.concatenate(runs), order=["id_r", "id_s"])
+    assert len(got) == len(want) > 500000 and (got == want).all()
