@@ -394,12 +394,7 @@ def run_ours(args):
             "bytes_formula": "4*T tokens + 8*(n+1) offsets + (b/8)*n sketches (Bitmap-Xor, b as configured)",
             "timing": "ssjb_time_build: mean of 10 launches on the resident replica, L2 flushed before each",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback"},
-        "K3_verify": {
-            "bound": "hbm", "unit": "GB/s", "peak": hbm_peak,
-            "achieved": vb_step / (ver_ms * 1e-3) / 1e9 if ver_ms else None,
-            "frac": vb_step / (ver_ms * 1e-3) / 1e9 / hbm_peak if ver_ms else None,
-            "ms_per_step": ver_ms, "bytes_per_step": vb_step,
-            "bytes_formula": "4*(|r|+|s|) per merged survivor + 16 per match (SURVEY 8d upper bound)"},
+        "K3_verify": k3_roofline(vb_step, ver_ms, hbm_peak),
     }
     if dominant == "filter" and uses_tc:
         roofline.update(filter_traffic(args.workload))
@@ -444,6 +439,24 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def k3_roofline(vb_step, ver_ms, hbm_peak):
+    """K3 against HBM with SURVEY 8d's algorithmic bytes -- an upper bound (the
+    early exit reads less).  On C4 the merged records are L2-resident (ncu:
+    ~0.1 GB of DRAM reads per verify launch), so the formula's rate can exceed
+    the HBM peak; the fraction is reported only where it is a fraction."""
+    if not ver_ms:
+        return None
+    ach = vb_step / (ver_ms * 1e-3) / 1e9
+    out = {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "achieved": ach,
+           "frac": ach / hbm_peak if ach <= hbm_peak else None,
+           "ms_per_step": ver_ms, "bytes_per_step": vb_step,
+           "bytes_formula": "4*(|r|+|s|) per merged survivor + 16 per match (SURVEY 8d upper bound)"}
+    if ach > hbm_peak:
+        out["note"] = ("algorithmic bytes above the HBM peak: the survivors' records are L2-resident and the "
+                       "early exit stops most merges early; ncu of the launches: profiles/r02n_c4_kernels_ncu.md")
+    return out
 
 
 def secondary_workloads(lib, args, device, l2):
