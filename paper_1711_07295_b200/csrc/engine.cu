@@ -1962,6 +1962,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // K3a: exact head-token overlaps for the large-record region of dense joins
     // (head_tc.cuh); active whenever the join runs the level-2 GEMM
     const HeadPlan hplan = use_tc && W <= 2 && W2 == 4 ? make_head_plan(c, plan, W2) : HeadPlan{};
+    // a head region of >= 2^30 window pairs of large records means a dense join:
+    // start on the level-2 GEMM instead of discovering it by a level-1 pass
+    // that overflows (C4: the discarded pass and its operands)
+    if (l2_auto && !l2gemm && hplan.ok && env_u64("SSJB_HEAD_PREDICT", 1) != 0) l2gemm = true;
     bool head_active = l2gemm && hplan.ok;
     const bool head_upfront = head_active;  // batch mode from the start (no single-pass fast path)
     const char* kenv = std::getenv("SSJB_TC_KIND");
@@ -2013,7 +2017,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint16_t* ingest_t16 = nullptr;
     Delta8Dev ingest_d8;
     const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
-    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n && !head_upfront &&
+    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n &&
         n >= env_u64("SSJB_STREAM_MIN_ROWS", 65536) && n > 0 && env_u64("SSJB_STREAM", 1) != 0) {
         static thread_local cudaStream_t copy_streams[16] = {};
         if (!copy_streams[device & 15])
@@ -2439,18 +2443,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
 
     // Fast path: the whole shard as one batch, K2 -> K3 -> K2b -> counters ->
     // K4 chained on the stream with a single host synchronisation.
-    double ms_filter = 0, ms_verify = 0;
-    bool done = false;
-    const auto t_launch = Clock::now();  // host setup ends: the first filter launch
-    auto t_synced = t_launch;
-    if (!head_upfront) {
-        cudaEvent_t a = T.mark();
-        if (streamed) {
+    // Streamed ingest: per row chunk (as its tokens land) decode / widen, build
+    // the sketches and expand the operands; with filter_chunks also launch the
+    // chunk's filter work items.  Returns filter_chunks.
+    auto stream_ingest = [&](bool filter_chunks) {
             const int variant_s = variant;
             // per-chunk filter launches (SSJB_STREAM=2) overlap more of the transfer
             // but pay a launch tail per chunk; by default only the ingest kernels
             // (decode, sketches, operands) are chunked
-            const bool stream_filter = env_u64("SSJB_STREAM", 1) >= 2;
+            const bool stream_filter = filter_chunks;
             for (size_t k = 0; k < ingest.size(); ++k) {
                 const IngestChunk& ch = ingest[k];
                 CK(cudaStreamWaitEvent(s, ch.ev, 0));
@@ -2478,6 +2479,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                     launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
                 }
             }
+        return filter_chunks;
+    };
+    double ms_filter = 0, ms_verify = 0;
+    bool done = false;
+    const auto t_launch = Clock::now();  // host setup ends: the first filter launch
+    auto t_synced = t_launch;
+    if (head_upfront && streamed) stream_ingest(false);  // (batch mode from the start: ingest only)
+    if (!head_upfront) {
+        cudaEvent_t a = T.mark();
+        if (streamed) {
+            const bool stream_filter = stream_ingest(env_u64("SSJB_STREAM", 1) >= 2);
             if (!stream_filter) {
                 FP.surv_soft = TP.surv_soft = std::max<uint64_t>(surv_cap / 2, 1);
                 launch_filter(0, total_items, 0);  // one persistent launch after ingest

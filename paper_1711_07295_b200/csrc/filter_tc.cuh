@@ -866,6 +866,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 bool acc_released = false;
                 uint32_t pre0 = 0, pre1 = 0;
                 if constexpr (L::kEarlyB) {  // issue the size loads before the accumulator wait
+                    // (loading them one tile ahead measured slower: 151.7 vs 147.7 ms on C4)
                     pre0 = __ldg(gsz + part * L::kColsPerWarp);
                     pre1 = __ldg(gsz + part * L::kColsPerWarp + L::kColsPerWarp - 1);
                 }

@@ -91,7 +91,7 @@ def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
 
 
 @pytest.mark.parametrize("mode", ["1", "2"])
-@pytest.mark.parametrize("flavour", ["tc-i8", "tc-i8-pair", "tc-fp4"])
+@pytest.mark.parametrize("flavour", ["tc-i8", "tc-i8-pair", "tc-fp4", "tc-head"])
 def test_streamed_ingest(lib, golden, colls, flavour, mode, monkeypatch):
     """Every fixture with the collection streamed to the device in 3 row chunks
     (decode + sketches + operands of a chunk overlap the next chunk's transfer;

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+P=${TAG:-r02q}
+timeout 300 python tools/heavy_phases.py C4 2>&1 | cut -c1-560 > gpurun_out/${P}_heavy.jsonl
+SSJB_HEAD_PREDICT=0 timeout 300 python tools/heavy_phases.py C4 2>&1 | cut -c1-560 >> gpurun_out/${P}_heavy.jsonl
+timeout 600 python bench.py --steps 5 --warmup 2 --no-cpu-baseline --no-secondary 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('C4 value', d['value'], 'e2e', d['e2e']['value'], 'cold', d['e2e_cold']['value'])" >> gpurun_out/${P}_heavy.jsonl 2>&1
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -k "golden_join or overflow or random or level3 or streamed" > gpurun_out/${P}_tests.log 2>&1; echo rc=$? >> gpurun_out/${P}_tests.log
+timeout 600 python -m pytest tests/test_gpu_heavy.py -x -q -s -k "not sharded" > gpurun_out/${P}_heavy_tests.log 2>&1; echo rc=$? >> gpurun_out/${P}_heavy_tests.log
