@@ -4,6 +4,7 @@
 // or SSJ_ALGO_NAIVE (src/join.cpp:91-126).
 #include <cuda_runtime.h>
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -983,7 +984,14 @@ ResultBlockCache& result_cache() {
     return *c;
 }
 size_t result_cache_budget() {
-    static const size_t b = static_cast<size_t>(env_u64("SSJB_RESULT_CACHE_MB", 4096)) << 20;
+    // SSJB_RESULT_CACHE_MB, default min(8 GB, 1/8 of physical memory)
+    static const size_t b = [] {
+        const uint64_t mb = env_u64("SSJB_RESULT_CACHE_MB", 0);
+        if (mb) return static_cast<size_t>(mb) << 20;
+        const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+        const size_t phys = pages > 0 && psz > 0 ? static_cast<size_t>(pages) * static_cast<size_t>(psz) : 0;
+        return std::min<size_t>(size_t(8) << 30, phys / 8);
+    }();
     return b;
 }
 }  // namespace
@@ -1956,7 +1964,11 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             // median record size (the paper's cutoff analysis), so most window
             // pairs survive level 1 and the level-2 check runs as a GEMM too
             const int64_t cx = cutoff(Method::Xor, width, Rational(plan.p, plan.q), true);
-            l2gemm = static_cast<double>(cx) < 1.25 * static_cast<double>(c.median_size());
+            static const double factor = [] {
+                const char* v = std::getenv("SSJB_L2GEMM_FACTOR");
+                return v && *v ? std::atof(v) : 1.25;
+            }();
+            l2gemm = static_cast<double>(cx) < factor * static_cast<double>(c.median_size());
         }
     }
     // K3a: exact head-token overlaps for the large-record region of dense joins

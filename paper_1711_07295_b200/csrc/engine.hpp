@@ -25,7 +25,7 @@ static_assert(sizeof(PairOut) == 16, "ssj_pair layout");
 
 // Large result blocks (>= 64 MB): a process-wide cache of page-locked host
 // blocks (engine.cu).  A freed block is kept (pinned, pages already faulted
-// in) up to SSJB_RESULT_CACHE_MB (default 4096) and handed to the next large
+// in) up to SSJB_RESULT_CACHE_MB (default min(8 GB, RAM / 8)) and handed to the next large
 // result, so repeated joins neither zero fresh pages nor stage their
 // downloads: the device copies straight into the result.
 void* result_block_alloc(size_t bytes);
