@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <deque>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -977,7 +979,13 @@ struct ResultBlockCache {
     std::map<void*, size_t> live;                 // block -> capacity
     std::multimap<size_t, void*> idle;            // capacity -> block
     std::map<void*, size_t> pinned;               // page-locked blocks (live or idle)
+    std::map<void*, size_t> pinning;              // queued / being page-locked
     size_t idle_bytes = 0;
+    // page-locking runs on a background thread: pinning a multi-GB block costs
+    // ~0.1 s per GB and must not land inside the next join
+    std::condition_variable cv;
+    std::deque<std::pair<void*, size_t>> queue;
+    bool worker = false;
 };
 ResultBlockCache& result_cache() {
     static ResultBlockCache* c = new ResultBlockCache();  // leaked: outlives static teardown
@@ -1027,18 +1035,41 @@ void result_block_free(void* p) {
     const size_t cap = it->second;
     C.live.erase(it);
     if (C.idle_bytes + cap <= result_cache_budget()) {
-        if (!C.pinned.count(p)) {
-            // page-lock once (its pages are faulted in by now); later results
-            // reuse it and the device copies into it directly
-            lk.unlock();
-            const bool ok = cudaHostRegister(p, cap, cudaHostRegisterPortable) == cudaSuccess;
-            if (!ok) cudaGetLastError();
-            lk.lock();
-            if (ok) C.pinned[p] = cap;
+        if (!C.pinned.count(p) && !C.pinning.count(p)) {
+            // page-lock once (its pages are faulted in by now), in the background;
+            // later results reuse it and the device copies into it directly
+            C.pinning[p] = cap;
+            C.queue.emplace_back(p, cap);
+            if (!C.worker) {
+                C.worker = true;
+                std::thread([&C]() {
+                    for (;;) {
+                        std::pair<void*, size_t> job;
+                        {
+                            std::unique_lock<std::mutex> l2(C.mu);
+                            C.cv.wait(l2, [&C]() { return !C.queue.empty(); });
+                            job = C.queue.front();
+                            C.queue.pop_front();
+                        }
+                        const bool ok = cudaHostRegister(job.first, job.second, cudaHostRegisterPortable) == cudaSuccess;
+                        if (!ok) cudaGetLastError();
+                        std::lock_guard<std::mutex> l2(C.mu);
+                        C.pinning.erase(job.first);
+                        if (ok) C.pinned[job.first] = job.second;
+                    }
+                }).detach();
+            }
+            C.cv.notify_one();
         }
         C.idle.emplace(cap, p);
         C.idle_bytes += cap;
         return;
+    }
+    // over budget: release it (after any page-locking in flight)
+    while (C.pinning.count(p)) {
+        lk.unlock();
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        lk.lock();
     }
     if (C.pinned.count(p)) {
         C.pinned.erase(p);

@@ -151,6 +151,16 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
         : "memory");
 }
 
+// Descriptor of the K step s after `d` (K-major, SWIZZLE_NONE): the next two
+// 16-byte K chunks start 256 bytes further, i.e. +16 in the 14-bit start
+// address field (shared-memory addresses < 256 KB never carry out of it).
+// The MMA issuer builds one descriptor per operand and tile and steps it with
+// one add per instruction instead of re-encoding it (a chain of uniform-
+// datapath ops per MMA that paced the single issuing thread).
+__device__ __forceinline__ uint64_t umma_desc_step(uint64_t d, int s) {
+    return d + static_cast<uint64_t>(16 * s);
+}
+
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo) {
     // K-major, SWIZZLE_NONE: LBO = 128 B between the two 16-byte K halves of
     // an instruction, SBO = stride between 8-row core-matrix groups.
@@ -743,20 +753,29 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 const int aslot = iseq % L::kAslots;
                 mbar_spin(&a_full[aslot], (iseq / L::kAslots) & 1);
                 const uint32_t a0 = smem_u32(sA + aslot * L::kA);
+                const uint64_t da0 = umma_desc(a0, L::kSbo);
+                const uint64_t da2 = umma_desc(a0 + KA * 8, L::kSbo);  // level-2 K range of the A rows
+                // the NS stages' B descriptors (a stage's address never changes)
+                uint64_t dbs[NS];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) dbs[k] = umma_desc(smem_u32(sB + k * L::kB), L::kSbo);
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++aseq) {
                     const int st = tseq % NS;
                     const int as = aseq % L::kAccSlots;
+                    uint64_t db0 = dbs[0];
+#pragma unroll
+                    for (int k = 1; k < NS; ++k) db0 = st == k ? dbs[k] : db0;
+                    const uint64_t db2 = umma_desc_step(db0, KA / 32);  // (KA * 8 bytes further = KA/32 K steps)
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
                     mbar_spin(&acc_empty[as], ((aseq / L::kAccSlots) & 1) ^ 1);
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t b0 = smem_u32(sB + st * L::kB);
                     const uint32_t d1 = tmem_base + as * NT;
 #pragma unroll
                     for (int s = 0; s < KA / 32; ++s) {
-                        const uint64_t da = umma_desc(a0 + s * 256, L::kSbo);
-                        const uint64_t db = umma_desc(b0 + s * 256, L::kSbo);
+                        const uint64_t da = umma_desc_step(da0, s);
+                        const uint64_t db = umma_desc_step(db0, s);
                         if constexpr (KIND == kKindI8)
                             umma_i8<NT>(d1, da, db, s > 0);
                         else
@@ -766,8 +785,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         const uint32_t d2 = tmem_base + L::kL2Col + as * NT;
 #pragma unroll
                         for (int s = 0; s < ((P.debug & 4) ? 1 : K2 / 32); ++s)  // (probe bit 4: one L2 MMA)
-                            umma_i8<NT>(d2, umma_desc(a0 + KA * 8 + s * 256, L::kSbo),
-                                        umma_desc(b0 + KA * 8 + s * 256, L::kSbo), s > 0);
+                            umma_i8<NT>(d2, umma_desc_step(da2, s), umma_desc_step(db2, s), s > 0);
                     }
                     umma_commit(&b_empty[st]);
                     umma_commit(&acc_full[as]);

@@ -217,15 +217,15 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                     const int st = tseq % NS;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 1] = clock64();
-                    const uint32_t b0 = smem_u32(sB + st * L::kB);
+                    const uint64_t db0 = umma_desc(smem_u32(sB + st * L::kB), L::kSbo);
 #pragma unroll
                     for (int r = 0; r < 2; ++r) {
                         mbar_spin(&acc_empty[r], (useq & 1) ^ 1);
                         asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint64_t da0 = umma_desc(a0 + r * L::kA, L::kSbo);
 #pragma unroll
                         for (int s = 0; s < KA / 32; ++s)
-                            umma_i8<NT>(tmem_base + r * NT, umma_desc(a0 + r * L::kA + s * 256, L::kSbo),
-                                        umma_desc(b0 + s * 256, L::kSbo), s > 0);
+                            umma_i8<NT>(tmem_base + r * NT, umma_desc_step(da0, s), umma_desc_step(db0, s), s > 0);
                         umma_commit(&acc_full[r]);
                     }
                     umma_commit(&b_empty[st]);

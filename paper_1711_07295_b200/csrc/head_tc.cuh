@@ -268,11 +268,12 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
                         mbar_spin(&s_full[st], (sseq / kHeadStages) & 1);
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         const uint32_t a0 = smem_u32(sStage + st * kHeadStage);
-                        const uint32_t b0 = a0 + kHeadA;
+                        const uint64_t da0 = umma_desc(a0, kHeadGroupBytes);
+                        const uint64_t db0 = umma_desc(a0 + kHeadA, kHeadGroupBytes);
 #pragma unroll
                         for (int k = 0; k < kHeadSliceK / 32; ++k) {
-                            const uint64_t da = umma_desc(a0 + k * 256, kHeadGroupBytes);
-                            const uint64_t db = umma_desc(b0 + k * 256, kHeadGroupBytes);
+                            const uint64_t da = umma_desc_step(da0, k);
+                            const uint64_t db = umma_desc_step(db0, k);
                             if constexpr (KIND == kKindI8)
                                 umma_i8<kHeadNT>(d, da, db, (s | k) != 0);
                             else
