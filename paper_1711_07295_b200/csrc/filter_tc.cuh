@@ -107,6 +107,15 @@ __device__ __forceinline__ uint32_t cols_below(uint32_t end, uint32_t base_col) 
     else return low_mask(x);
 }
 
+// One lane of the (converged) warp: elect.sync
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -742,13 +751,18 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // The whole warp runs the loop (warp-uniform control flow: the tile
+        // bookkeeping and descriptors live in uniform registers); one elected
+        // lane issues each tcgen05 instruction and arrive.
+        const bool leader = elect_one();
+        {
             uint32_t iseq = 0, tseq = 0, aseq = 0;
             for (;;) {
                 const int slot = iseq & 1;
                 mbar_spin(&item_full[slot], (iseq >> 1) & 1);
                 const TcItem info = items[slot];
-                mbar_arrive(&item_empty[slot]);
+                __syncwarp();
+                if (leader) mbar_arrive(&item_empty[slot]);
                 if (info.done) break;
                 const int aslot = iseq % L::kAslots;
                 mbar_spin(&a_full[aslot], (iseq / L::kAslots) & 1);
@@ -772,25 +786,29 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t d1 = tmem_base + as * NT;
+                    if (leader) {
 #pragma unroll
-                    for (int s = 0; s < KA / 32; ++s) {
-                        const uint64_t da = umma_desc_step(da0, s);
-                        const uint64_t db = umma_desc_step(db0, s);
-                        if constexpr (KIND == kKindI8)
-                            umma_i8<NT>(d1, da, db, s > 0);
-                        else
-                            umma_f4<NT>(d1, da, db, s > 0, tmem_base + L::kSfCol, tmem_base + L::kSfCol + 32);
-                    }
-                    if constexpr (K2 > 0) {
-                        const uint32_t d2 = tmem_base + L::kL2Col + as * NT;
+                        for (int s = 0; s < KA / 32; ++s) {
+                            const uint64_t da = umma_desc_step(da0, s);
+                            const uint64_t db = umma_desc_step(db0, s);
+                            if constexpr (KIND == kKindI8)
+                                umma_i8<NT>(d1, da, db, s > 0);
+                            else
+                                umma_f4<NT>(d1, da, db, s > 0, tmem_base + L::kSfCol, tmem_base + L::kSfCol + 32);
+                        }
+                        if constexpr (K2 > 0) {
+                            const uint32_t d2 = tmem_base + L::kL2Col + as * NT;
 #pragma unroll
-                        for (int s = 0; s < ((P.debug & 4) ? 1 : K2 / 32); ++s)  // (probe bit 4: one L2 MMA)
-                            umma_i8<NT>(d2, umma_desc_step(da2, s), umma_desc_step(db2, s), s > 0);
+                            for (int s = 0; s < ((P.debug & 4) ? 1 : K2 / 32); ++s)  // (probe bit 4: one L2 MMA)
+                                umma_i8<NT>(d2, umma_desc_step(da2, s), umma_desc_step(db2, s), s > 0);
+                        }
+                        umma_commit(&b_empty[st]);
+                        umma_commit(&acc_full[as]);
                     }
-                    umma_commit(&b_empty[st]);
-                    umma_commit(&acc_full[as]);
+                    __syncwarp();
                 }
-                umma_commit(&a_empty[aslot]);
+                if (leader) umma_commit(&a_empty[aslot]);
+                __syncwarp();
                 ++iseq;
             }
         }

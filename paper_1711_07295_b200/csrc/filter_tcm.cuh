@@ -202,17 +202,21 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // (warp-uniform loop, one elected lane issues: see filter_tc_kernel)
+        const bool leader = elect_one();
+        {
             uint32_t iseq = 0, tseq = 0, useq = 0;  // useq: uses of each accumulator
             for (;;) {
                 const int slot = iseq & 1;
                 mbar_spin(&item_full[slot], (iseq >> 1) & 1);
                 const TcItem info = items[slot];
-                mbar_arrive(&item_empty[slot]);
+                __syncwarp();
+                if (leader) mbar_arrive(&item_empty[slot]);
                 if (info.done) break;
                 const int aslot = iseq & 1;
                 mbar_spin(&a_full[aslot], (iseq >> 1) & 1);
                 const uint32_t a0 = smem_u32(sA + aslot * 2 * L::kA);
+                const uint64_t da0 = umma_desc(a0, L::kSbo), da1 = umma_desc(a0 + L::kA, L::kSbo);
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++tseq, ++useq) {
                     const int st = tseq % NS;
                     mbar_spin(&b_full[st], (tseq / NS) & 1);
@@ -222,16 +226,21 @@ __global__ void __launch_bounds__((TcmLayout<KA, NS>::kThreads), 1) filter_tcm_k
                     for (int r = 0; r < 2; ++r) {
                         mbar_spin(&acc_empty[r], (useq & 1) ^ 1);
                         asm volatile("tcgen05.fence::after_thread_sync;");
-                        const uint64_t da0 = umma_desc(a0 + r * L::kA, L::kSbo);
+                        if (leader) {
+                            const uint64_t dar = r ? da1 : da0;
 #pragma unroll
-                        for (int s = 0; s < KA / 32; ++s)
-                            umma_i8<NT>(tmem_base + r * NT, umma_desc_step(da0, s), umma_desc_step(db0, s), s > 0);
-                        umma_commit(&acc_full[r]);
+                            for (int s = 0; s < KA / 32; ++s)
+                                umma_i8<NT>(tmem_base + r * NT, umma_desc_step(dar, s), umma_desc_step(db0, s), s > 0);
+                            umma_commit(&acc_full[r]);
+                        }
+                        __syncwarp();
                     }
-                    umma_commit(&b_empty[st]);
+                    if (leader) umma_commit(&b_empty[st]);
+                    __syncwarp();
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 2] = clock64();
                 }
-                umma_commit(&a_empty[aslot]);
+                if (leader) umma_commit(&a_empty[aslot]);
+                __syncwarp();
                 ++iseq;
             }
         }

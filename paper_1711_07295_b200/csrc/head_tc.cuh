@@ -250,13 +250,16 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // (warp-uniform loop, one elected lane issues: see filter_tc_kernel)
+        const bool leader = elect_one();
+        {
             uint32_t iseq = 0, sseq = 0, aseq = 0;
             for (;;) {
                 const int slot = iseq & 1;
                 mbar_spin(&item_full[slot], (iseq >> 1) & 1);
                 const HeadItem info = items[slot];
-                mbar_arrive(&item_empty[slot]);
+                __syncwarp();
+                if (leader) mbar_arrive(&item_empty[slot]);
                 if (info.done) break;
                 for (uint32_t t = 0; t < info.ntiles; ++t, ++aseq) {
                     const int as = aseq & 1;
@@ -267,22 +270,26 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
                         const int st = sseq % kHeadStages;
                         mbar_spin(&s_full[st], (sseq / kHeadStages) & 1);
                         asm volatile("tcgen05.fence::after_thread_sync;");
-                        const uint32_t a0 = smem_u32(sStage + st * kHeadStage);
-                        const uint64_t da0 = umma_desc(a0, kHeadGroupBytes);
-                        const uint64_t db0 = umma_desc(a0 + kHeadA, kHeadGroupBytes);
+                        if (leader) {
+                            const uint32_t a0 = smem_u32(sStage + st * kHeadStage);
+                            const uint64_t da0 = umma_desc(a0, kHeadGroupBytes);
+                            const uint64_t db0 = umma_desc(a0 + kHeadA, kHeadGroupBytes);
 #pragma unroll
-                        for (int k = 0; k < kHeadSliceK / 32; ++k) {
-                            const uint64_t da = umma_desc_step(da0, k);
-                            const uint64_t db = umma_desc_step(db0, k);
-                            if constexpr (KIND == kKindI8)
-                                umma_i8<kHeadNT>(d, da, db, (s | k) != 0);
-                            else
-                                umma_f4<kHeadNT>(d, da, db, (s | k) != 0, tmem_base + L::kSfCol,
-                                                 tmem_base + L::kSfCol + 32);
+                            for (int k = 0; k < kHeadSliceK / 32; ++k) {
+                                const uint64_t da = umma_desc_step(da0, k);
+                                const uint64_t db = umma_desc_step(db0, k);
+                                if constexpr (KIND == kKindI8)
+                                    umma_i8<kHeadNT>(d, da, db, (s | k) != 0);
+                                else
+                                    umma_f4<kHeadNT>(d, da, db, (s | k) != 0, tmem_base + L::kSfCol,
+                                                     tmem_base + L::kSfCol + 32);
+                            }
+                            umma_commit(&s_empty[st]);
                         }
-                        umma_commit(&s_empty[st]);
+                        __syncwarp();
                     }
-                    umma_commit(&acc_full[as]);
+                    if (leader) umma_commit(&acc_full[as]);
+                    __syncwarp();
                 }
                 ++iseq;
             }
