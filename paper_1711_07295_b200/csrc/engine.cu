@@ -2814,7 +2814,12 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                         res_count = 0;
                     }
                     cudaEvent_t c0 = T.mark();
+                    // (one warp per pair, SSJB_HEAD_WARP_VERIFY=1, measured slower on
+                    // C4: 32.9 vs 14.1 ms -- the lanes' binary searches miss L2)
+                    const int wm = VP.warp_mode;
+                    if (env_u64("SSJB_HEAD_WARP_VERIFY", 0) != 0 && wm) VP.warp_mode = 2;
                     launch_verify(&d_hctl->survivors);
+                    VP.warp_mode = wm;
                     cudaEvent_t c1 = T.mark();
                     CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
                     CK(cudaStreamSynchronize(s));

@@ -890,7 +890,7 @@ struct VerifyParams {
     const uint64_t* bits2;    // level-2 Xor sketches (n x w2 words), or null
     const int32_t* maxham;    // maxham[|r|+|s|] (with bits2)
     int w2;
-    int warp_mode;            // 1: warp per pair when the survivors are few
+    int warp_mode;            // 1: warp per pair when the survivors are few; 2: always
     const uint64_t* bits3;    // level-3 512-bit Xor sketches (dense joins), or null
     uint32_t l3_min_sum;      // level 3 is tested when |r| + |s| >= this
 };
@@ -975,7 +975,9 @@ template <int W2>
 __global__ void verify_pairs(VerifyParams P) {
     const int lane = threadIdx.x & 31;
     const unsigned long long count = min(*P.count_ptr, P.count_cap);
-    if (count <= kWarpVerifyMax && P.warp_mode) {
+    // warp_mode 2: every pair one warp (the head-overlap survivors: long records,
+    // where one lane's merge chain of thousands of tokens paces its warp)
+    if ((count <= kWarpVerifyMax && P.warp_mode) || P.warp_mode == 2) {
         verify_warp_mode<W2>(P, count, lane);
         return;
     }
