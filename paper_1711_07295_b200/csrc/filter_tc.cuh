@@ -425,14 +425,21 @@ __device__ __forceinline__ uint32_t survivors_mixed(const uint32_t (&d)[32], int
     return m;
 }
 
-// survivors_mixed with the tile's column sizes read from global memory
-template <int KIND>
+// a column size from the shared side ring (SMEM) or from global memory (read-only path)
+template <bool SMEM>
+__device__ __forceinline__ uint32_t ld_sz(const uint32_t* p) {
+    if constexpr (SMEM) return *p;
+    else return __ldg(p);
+}
+
+// survivors_mixed with the tile's column sizes read from a plain u32 array
+template <int KIND, bool SMEM>
 __device__ __forceinline__ uint32_t survivors_mixed_g(const uint32_t (&d)[32], int base, const int32_t* maxham,
                                                       uint32_t si, const uint32_t* gsz, int cl) {
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k)
-        m |= ((base - maxham[si + __ldg(gsz + cl + k)] - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
+        m |= ((base - maxham[si + ld_sz<SMEM>(gsz + cl + k)] - 1 - acc_int<KIND>(d[k])) < 0 ? 1u : 0u) << k;
     return m;
 }
 
@@ -569,13 +576,31 @@ struct TcLayout {
     // no-extension operands carry no size chunk: the column sizes and -pc pairs of
     // each tile go to a separate, deeper "side" ring, so a B stage is released as
     // soon as its MMAs complete (the epilogue never holds it)
-    static constexpr int kSide = kNoExt ? NT * 4 + NT * 2 : 0;  // sizes u32[NT] | -pc pairs u32[NT/2]
-    static constexpr int NE = kNoExt ? 2 * NS : 1;              // side-ring slots
-    // level-2 GEMM: the epilogue reads column sizes from global memory (L2) so a
-    // B stage is released when its MMAs complete, not when the epilogue is done
-    // with the tile -- with only two 59 KB stages fitting, a stage's lifetime
-    // (copy + MMAs + epilogue) otherwise paces the pipeline
+    // level-2 GEMM: a B stage is released when its MMAs complete, not when the
+    // epilogue is done with the tile -- with only a few 51 KB stages fitting, a
+    // stage's lifetime (copy + MMAs + epilogue) otherwise paces the pipeline.
+    // The epilogue reads the tile's column sizes from global memory (L2);
+    // SSJB_SIZE_RING=1 stages them in a small side ring instead (512 B per
+    // tile, its own bulk copy, released by the epilogue warps) -- measured
+    // slower on C4 (136.5 vs 128.1 ms K2, 4 or 7 slots alike), although the
+    // global loads are the epilogue's largest single stall in ncu.
     static constexpr bool kEarlyB = K2 > 0;
+#ifndef SSJB_L2_EPI_SETS
+#define SSJB_L2_EPI_SETS 1
+#endif
+    static constexpr int kSets = (K2 > 0 && NT == 128) ? SSJB_L2_EPI_SETS : 1;
+#ifndef SSJB_SIZE_RING
+#define SSJB_SIZE_RING 0
+#endif
+    static constexpr bool kSizeRing = kEarlyB && kSets == 1 && SSJB_SIZE_RING;
+    static constexpr int kSide = kNoExt ? NT * 4 + NT * 2 : (kSizeRing ? NT * 4 : 0);  // sizes u32[NT] | -pc pairs
+#ifndef SSJB_SIZE_RING_SLOTS
+#define SSJB_SIZE_RING_SLOTS 7
+#endif
+    // side-ring slots (size ring: enough that the producer's lead over the
+    // epilogue stays that of the B stages plus accumulator slots)
+    static constexpr int NE = kNoExt ? 2 * NS : (kSizeRing ? SSJB_SIZE_RING_SLOTS : 1);
+    static constexpr bool kSideRing = kNoExt || kSizeRing;
     // epilogue warps (4 per column part, one per TMEM lane quarter): 64 columns
     // each for the level-2 GEMM's 128-column tiles (the per-tile fixed cost of a
     // warp -- barrier waits, column sizes, thresholds -- paid by 8 warps, not 16)
@@ -584,10 +609,6 @@ struct TcLayout {
     // two sets taking alternate tiles (accumulator slots), 64 columns per warp
     // and two tile intervals each; measured neutral on C4 (162 vs 160 ms), so
     // the default keeps every warp on every tile
-#ifndef SSJB_L2_EPI_SETS
-#define SSJB_L2_EPI_SETS 1
-#endif
-    static constexpr int kSets = (K2 > 0 && NT == 128) ? SSJB_L2_EPI_SETS : 1;
     static constexpr int kSetWarps = kEpiWarps / kSets;      // warps per tile
     static constexpr int kParts = kSetWarps / 4;             // column parts per tile
     static constexpr int kThreads = 64 + 32 * kEpiWarps;
@@ -599,7 +620,7 @@ struct TcLayout {
     static constexpr int kB = NT * kRow;                       // one B stage: a single bulk copy
     static constexpr int kAslots = K2 ? 1 : 2;
     static constexpr int kQueue = kEpiWarps * kTcQueue * 8;
-    static constexpr int kBytes = kAslots * kA + NS * kB + (kNoExt ? NE * kSide : 0) + kQueue;
+    static constexpr int kBytes = kAslots * kA + NS * kB + (kSideRing ? NE * kSide : 0) + kQueue;
     // accumulator slots in flight: as many NT-column slots (x2 with the level-2
     // GEMM) as TMEM holds next to the fp4 scale factors, at most 4
     static constexpr int kAccSlots = (((KIND == kKindF4 ? 384 : 512) / (NT * (K2 ? 2 : 1))) < 4)
@@ -623,7 +644,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
     uint8_t* sA = smem;                                   // [2][kA]
     uint8_t* sB = smem + L::kAslots * L::kA;              // [NS][kB]
     uint8_t* sSide = sB + NS * L::kB;                     // [NE][kSide] (no-extension operands)
-    uint2* sQ = reinterpret_cast<uint2*>(sSide + (L::kNoExt ? L::NE * L::kSide : 0));  // [8][kTcQueue]
+    uint2* sQ = reinterpret_cast<uint2*>(sSide + (L::kSideRing ? L::NE * L::kSide : 0));  // [8][kTcQueue]
     __shared__ __align__(8) uint64_t item_full[2], item_empty[2], a_full[2], a_empty[2];
     __shared__ __align__(8) uint64_t b_full[NS], b_empty[NS], acc_full[L::kAccSlots], acc_empty[L::kAccSlots];
     __shared__ __align__(8) uint64_t e_full[L::NE], e_empty[L::NE];
@@ -723,13 +744,13 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tseq < 512) P.trace[tseq * 4 + 0] = clock64();
                     const uint32_t col = info.c0 + t * NT;
                     uint8_t* dst = sB + st * L::kB;
-                    if constexpr (L::kNoExt) {
+                    if constexpr (L::kSideRing) {
                         const int se = tseq % L::NE;
                         mbar_spin(&e_empty[se], ((tseq / L::NE) & 1) ^ 1);
                         uint8_t* side = sSide + se * L::kSide;
                         mbar_expect_tx(&e_full[se], L::kSide);
                         tma_load_1d(side, P.sizes + col, NT * 4, &e_full[se]);
-                        tma_load_1d(side + NT * 4, P.npc2 + col / 2, NT * 2, &e_full[se]);
+                        if constexpr (L::kNoExt) tma_load_1d(side + NT * 4, P.npc2 + col / 2, NT * 2, &e_full[se]);
                     }
                     if ((P.debug & 8) && tseq >= NS) {  // (probe bit 8: stale B stages, no copies)
                         mbar_arrive(&b_full[st]);
@@ -890,11 +911,14 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                     }
                 }
                 const int st = static_cast<int>(st_idx), as = static_cast<int>(acc_idx);
-                if constexpr (L::kNoExt) mbar_wait_u32(smem_u32(&e_full[0]) + 8 * se_idx, se_phase);
+                if constexpr (L::kSideRing) mbar_wait_u32(smem_u32(&e_full[0]) + 8 * se_idx, se_phase);
                 else if constexpr (!L::kEarlyB) mbar_wait_u32(bfull_u32 + 8 * st_idx, st_phase);
                 // (early-released stages: the accumulator's completion implies the
                 // operands arrived; sizes come from gsz below)
-                const uint32_t* gsz = P.sizes + info.c0 + t * NT;
+                // tile's column sizes: the side ring (kSizeRing, already waited on
+                // above) or global memory (L2)
+                const uint32_t* gsz = L::kSizeRing ? reinterpret_cast<const uint32_t*>(sSide + se_idx * L::kSide)
+                                                   : P.sizes + info.c0 + t * NT;
                 // level-2 GEMM kernel, one 32-column group per warp: the packed
                 // group loads are the warp's only TMEM reads of the tile, so the slot
                 // is released as soon as they land (SSJB_EARLY_ACC=0: at tile end)
@@ -903,8 +927,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 uint32_t pre0 = 0, pre1 = 0;
                 if constexpr (L::kEarlyB) {  // issue the size loads before the accumulator wait
                     // (loading them one tile ahead measured slower: 151.7 vs 147.7 ms on C4)
-                    pre0 = __ldg(gsz + part * L::kColsPerWarp);
-                    pre1 = __ldg(gsz + part * L::kColsPerWarp + L::kColsPerWarp - 1);
+                    pre0 = ld_sz<L::kSizeRing>(gsz + part * L::kColsPerWarp);
+                    pre1 = ld_sz<L::kSizeRing>(gsz + part * L::kColsPerWarp + L::kColsPerWarp - 1);
                 }
                 mbar_wait_u32(accfull_u32 + 8 * acc_idx, acc_phase);
                 asm volatile("tcgen05.fence::after_thread_sync;");
@@ -938,7 +962,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         int dummy2[32];
                         tmem_ld32(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
                         e = m & (uni ? survivors32<true, KIND>(d2, cim1_2, dummy2, P.neg1)
-                                     : (L::kEarlyB ? survivors_mixed_g<KIND>(d2, pc2, maxham, si, gsz, cl)
+                                     : (L::kEarlyB ? survivors_mixed_g<KIND, L::kSizeRing>(d2, pc2, maxham, si, gsz, cl)
                                                    : survivors_mixed<KIND, L::kKCT>(d2, pc2, maxham, si, stage, cl)));
                     }
                     // (without the level-2 GEMM, level-1 survivors are emitted and
@@ -1001,7 +1025,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         tmem_ld32_pack16_nowait(tmem_base + lane_base + as * NT + cl, d);
                         if constexpr (K2 > 0) tmem_ld32_pack16_nowait(tmem_base + lane_base + L::kL2Col + as * NT + cl, d2);
                         const uint32_t colsz = fast ? 0u
-                                                    : (L::kEarlyB ? __ldg(gsz + cl + lane)
+                                                    : (L::kEarlyB ? ld_sz<L::kSizeRing>(gsz + cl + lane)
                                                                   : tile_col_size<L::kNoExt, L::kKCT>(side_sz, stage, cl + lane));
                         tmem_wait_ld();
                         if constexpr (kEarlyAcc) {
@@ -1097,8 +1121,8 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                         const uint32_t rm = low_mask(kh) & ~low_mask(kl);
                         if (!__any_sync(0xFFFFFFFFu, rm != 0)) continue;
                         tmem_ld32(tmem_base + lane_base + as * NT + cl, d);
-                        const uint32_t sz0 = L::kEarlyB ? __ldg(gsz + cl) : stage_size<L::kKCT>(stage, cl);
-                        uni = sz0 == (L::kEarlyB ? __ldg(gsz + cl + 31) : stage_size<L::kKCT>(stage, cl + 31));
+                        const uint32_t sz0 = L::kEarlyB ? ld_sz<L::kSizeRing>(gsz + cl) : stage_size<L::kKCT>(stage, cl);
+                        uni = sz0 == (L::kEarlyB ? ld_sz<L::kSizeRing>(gsz + cl + 31) : stage_size<L::kKCT>(stage, cl + 31));
                         if (uni) {
                             if (sz0 != last_sz) {
                                 last_sz = sz0;
@@ -1109,7 +1133,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                             }
                             m = survivors32<true, KIND>(d, cim1, dummy, P.neg1);
                         } else {
-                            m = L::kEarlyB ? survivors_mixed_g<KIND>(d, pc, maxham, si, gsz, cl)
+                            m = L::kEarlyB ? survivors_mixed_g<KIND, L::kSizeRing>(d, pc, maxham, si, gsz, cl)
                                            : survivors_mixed<KIND, L::kKCT>(d, pc, maxham, si, stage, cl);
                         }
                         m = bypass ? rm : (m & rm);
@@ -1126,7 +1150,7 @@ __global__ void __launch_bounds__((TcLayout<KIND, KA, K2, W2, NS, NT>::kThreads)
                 if (lane == 0) {
                     if (SSJB_TRACE && P.trace && blockIdx.x == 0 && tile_seq - 1 < 512) P.trace[2048 + 8192 + (tile_seq - 1) * 16 + (warp - 2)] = clock64();
                     if (!acc_released) mbar_arrive_u32(accempty_u32 + 8 * acc_idx);
-                    if constexpr (L::kNoExt) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
+                    if constexpr (L::kSideRing) mbar_arrive_u32(smem_u32(&e_empty[0]) + 8 * se_idx);
                     else if constexpr (!L::kEarlyB) mbar_arrive_u32(bempty_u32 + 8 * st_idx);
                 }
                 if (++st_idx == NS) {
