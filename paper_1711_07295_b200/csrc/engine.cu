@@ -2799,6 +2799,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 CK(cudaMemcpyAsync(&hc, d_hctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 st.ms_head += Timer::ms(a, b);
+#ifdef SSJB_HEAD_PROBE
+                std::fprintf(stderr, "head probe: candidates %llu\n", static_cast<unsigned long long>(hc.verify_bytes));
+#endif
                 const uint64_t S = hc.survivors;
                 const uint64_t processed = std::min<uint64_t>(hc.work_next, he - hb);
                 if (S > surv_cap) {  // overshoot: nothing was counted; redo with a lower cap / fewer items

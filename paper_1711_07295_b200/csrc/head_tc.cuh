@@ -344,6 +344,9 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[as]);  // accumulators are in registers
+#if defined(SSJB_HEAD_PROBE)
+                if (SSJB_HEAD_PROBE == 3) continue;  // (probe: no epilogue math)
+#endif
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
                     const uint32_t gbase = gcol + 32 * g;
@@ -368,6 +371,13 @@ __global__ void __launch_bounds__(HeadLayout<KIND>::kThreads, 1) head_overlap_ke
                         cand &= rm;
                     }
                     uint32_t e = 0;
+#ifdef SSJB_HEAD_PROBE
+                    if (SSJB_HEAD_PROBE == 1) {  // (probe: count candidates)
+                        const int c = __reduce_add_sync(0xFFFFFFFFu, __popc(cand));
+                        if (lane == 0 && c) atomicAdd(&P.ctl->verify_bytes, static_cast<unsigned long long>(c));
+                    }
+                    if (SSJB_HEAD_PROBE >= 1) cand = 0;
+#endif
                     if (cand) {  // rare: exact per-pair test of the pre-test's candidates
 #pragma unroll
                         for (int k = 0; k < 32; ++k) {
