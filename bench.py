@@ -284,6 +284,8 @@ def run_ours(args):
             reps_last = reps
             launches += sum(r.extra["launches"] for r in reps)
             window += sum(r.counters["candidates"] for r in reps)
+            for r in reps:  # (stats only from here on: the result block goes back to the library's cache,
+                r.pairs = None  # as a client's does when it is done with a result)
             kstats.append(reps)
     if pool is not None:
         # per-kernel device times for the roofline come from serial steps (one
@@ -292,7 +294,10 @@ def run_ours(args):
         kstats = []
         for _ in range(min(args.steps, 5)):
             flush_l2(l2)
-            kstats.append([one(o, r0, r1, True) for o, (r0, r1) in zip(opts, rows)])
+            reps = [one(o, r0, r1, True) for o, (r0, r1) in zip(opts, rows)]
+            for r in reps:
+                r.pairs = None
+            kstats.append(reps)
     # K1 alone on the resident replica (its per-join cost is hidden by the
     # replica's sketch cache above): mean of 10 launches, L2 flushed before each
     k1_ms = None
