@@ -384,9 +384,15 @@ int shards_per_device() {
 std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
                                                size_t row_end, int devices, int first_device, int delivery) {
     if (coll.size() >= (size_t(1) << 31)) throw std::invalid_argument("collections above 2^31 records are not supported");
+    const auto h0 = std::chrono::steady_clock::now();
     ssjb::JoinPlan whole = ssjb::make_plan(coll, o, row_begin, row_end);
     whole.delivery = delivery;
+    const auto h1 = std::chrono::steady_clock::now();
     const int avail = ssjb::engine_device_count();
+    if (std::getenv("SSJB_HOST_TIMING") && std::atoi(std::getenv("SSJB_HOST_TIMING")) >= 2)
+        std::fprintf(stderr, "[host] plan %.3f ms, device count %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
     if (avail <= 0) throw ssjb::DeviceError("no CUDA device available for the B200 join");
     devices = std::max(1, std::min(devices, avail - first_device));
     const int shards = devices * shards_per_device();

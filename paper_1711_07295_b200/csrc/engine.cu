@@ -1944,6 +1944,7 @@ void engine_trim(int device) {
 
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out) {
     using Clock = std::chrono::steady_clock;
+    const auto t_enter = Clock::now();
     set_device(device);
     // one non-blocking stream per (host thread, device), reused across joins
     static thread_local cudaStream_t streams[16] = {};
@@ -1952,6 +1953,12 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     EngineStats& st = out.stats;
     st.window_pairs = plan.window_pairs;
     const auto t_start = Clock::now();
+    // SSJB_HOST_TIMING=2: host timestamps of the join's phases (stderr)
+    const bool host_trace = env_u64("SSJB_HOST_TIMING", 0) >= 2;
+    std::vector<std::pair<const char*, Clock::time_point>> hmarks;
+    auto hmark = [&](const char* what) {
+        if (host_trace) hmarks.emplace_back(what, Clock::now());
+    };
     Timer T(s);
     Arena A(s);
 
@@ -2151,6 +2158,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint8_t* d_opA = variant >= 0 ? sk->opA[variant] : nullptr;
     uint8_t* d_opB = variant >= 0 ? sk->opB[variant] : nullptr;
     cudaEvent_t e_build = T.mark();
+    hmark("upload+build enqueued");
 
     // buffers
     // buffer sizing: survivors (8 B) and result sort buffers (24 B); a batch's
@@ -2179,6 +2187,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         std::max<uint64_t>(env_u64("SSJB_SURVIVOR_CAP", uint64_t(1) << (27 + big)), 1u << 20);
     uint64_t res_cap = std::max<uint64_t>(env_u64("SSJB_RESULT_CAP", uint64_t(1) << 26), surv_cap);
     WorkspaceLease lease(device, s);
+    hmark("workspace");
     JoinWorkspace& WS = *lease.ws;
     const bool use_ws = env_u64("SSJB_WORKSPACE", 1) != 0;
     if (use_ws) {
@@ -2378,7 +2387,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             return;
         }
         cudaEvent_t b = T.mark();
+        hmark("flush: sort enqueued");
         PairVec run(count);
+        hmark("flush: result block");
         const bool direct = count && result_block_pinned(run.data(), count * sizeof(PairOut));
         d2h_pairs_staged(run.data(), inb ? SB.kb : SB.ka, inb ? SB.vb : SB.va, count, s,
                          direct ? A.alloc<PairOut>(count) : nullptr);
@@ -2387,6 +2398,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         st.d2h_bytes += count * (direct ? sizeof(PairOut) : 12);
         st.ms_sort += Timer::ms(a, b);
         st.ms_download += Timer::ms(b, d);
+        hmark(direct ? "flush: downloaded (direct)" : "flush: downloaded (staged)");
         runs.push_back(std::move(run));
         CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
     };
@@ -2753,6 +2765,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             // emit them): batches with a soft survivor cap, each verified by K3
             cudaEvent_t h0 = T.mark();
             const HeadDev hd = head_setup(*rep, c, hplan, A, s, sms, st.launches);
+            hmark("head setup");
             dev::Control* d_hctl = A.alloc<dev::Control>(1);
             dev::HeadParams HP{};
             HP.op = hd.op;
@@ -2845,6 +2858,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         flush_results(res_count);
     }
 
+    hmark("results downloaded");
     // merge sorted runs (one run unless the result buffer overflowed)
     if (runs.size() == 1) {
         out.pairs = std::move(runs[0]);
@@ -2893,6 +2907,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         std::fprintf(stderr, "[host] after sync %.3f ms, total %.3f ms\n",
                      std::chrono::duration<double, std::milli>(Clock::now() - t_synced).count(), total * 1e3);
     out.verify_s = std::max(0.0, total - out.index_s - out.candidates_s);
+    if (host_trace) {
+        auto prev = t_start;
+        for (auto& m : hmarks) {
+            std::fprintf(stderr, "[host] %-24s +%8.3f ms (at %8.3f)\n", m.first,
+                         std::chrono::duration<double, std::milli>(m.second - prev).count(),
+                         std::chrono::duration<double, std::milli>(m.second - t_start).count());
+            prev = m.second;
+        }
+        std::fprintf(stderr, "[host] engine total %.3f ms (+ %.3f ms device/stream setup before it)\n", total * 1e3,
+                     std::chrono::duration<double, std::milli>(t_start - t_enter).count());
+    }
 }
 
 // NAIVE RS-join block on one GPU: R rows [r_begin, r_end) x all of S
