@@ -105,6 +105,9 @@ ssjb::Options to_options(const ssj_join_options& in) {
     o.cutoff_value = in.cutoff_value;
     if (in.placement < SSJ_PLACEMENT_DEFAULT || in.placement > SSJ_PLACEMENT_FILTER3)
         throw std::invalid_argument("unknown placement");
+    o.placement = in.placement;
+    o.suffix_depth = in.suffix_depth;
+    o.ell_max = in.ell_max;
     o.workers = in.workers;
     o.buffer_capacity = in.buffer_capacity;
     return o;
@@ -113,26 +116,32 @@ ssjb::Options to_options(const ssj_join_options& in) {
 // Algorithms of the drop-in.  PAR_BITMAP and NAIVE run as themselves (the
 // PAR_BITMAP checks are reference src/parallel_join.cpp:41-44).  The
 // prefix-filter algorithms (ALLPAIRS, PPJOIN, PPJOIN+, GROUPJOIN, ADAPTJOIN)
-// are exact joins whose pair list is the same for every algorithm (reference
-// tests/test_joins.cpp:62-112, tests/test_capi.cpp:64-88), so the B200 build
-// returns that list from its GPU join: the Bitmap-Filter join for Jaccard
-// thresholds (the call's bitmap options, the filter enabled), the NAIVE join
-// for the other similarity functions.  Their counters describe that GPU run,
-// not the reference's prefix-filter internals; candidates == pruned +
-// verified and matched == pair count hold as for every algorithm.
-void check_supported(ssjb::Options& o) {
-    if (o.algorithm == ssjb::Algo::Naive) return;
-    if (o.algorithm != ssjb::Algo::ParBitmap) {
-        if (o.sim == ssjb::Sim::Jaccard) {
-            o.algorithm = ssjb::Algo::ParBitmap;
-            o.bitmap_enabled = true;
-        } else {
-            o.algorithm = ssjb::Algo::Naive;
-        }
-        o.workers = std::max(o.workers, 1);
-        if (o.buffer_capacity < 1) o.buffer_capacity = 2048;
-        return;
+// run on the GPU prefix-filter engine (engine_prefix_join, prefix_join.cuh)
+// with the reference's counters when a whole collection is joined (ssj_join,
+// the delivery entry points).  Row-range entry points (ssjb_join_rows,
+// ssjb_partition_rows) are PAR_BITMAP concepts: there a prefix-filter code is
+// answered by the Bitmap-Filter join of the same threshold (Jaccard) or the
+// NAIVE join (other functions) -- the same pair list, since every exact
+// algorithm returns it (reference tests/test_joins.cpp:62-112).
+bool is_prefix_algo(ssjb::Algo a) {
+    return a == ssjb::Algo::AllPairs || a == ssjb::Algo::PPJoin || a == ssjb::Algo::PPJoinPlus ||
+           a == ssjb::Algo::GroupJoin || a == ssjb::Algo::AdaptJoin;
+}
+
+void to_row_join(ssjb::Options& o) {
+    if (!is_prefix_algo(o.algorithm)) return;
+    if (o.sim == ssjb::Sim::Jaccard) {
+        o.algorithm = ssjb::Algo::ParBitmap;
+        o.bitmap_enabled = true;
+    } else {
+        o.algorithm = ssjb::Algo::Naive;
     }
+    o.workers = std::max(o.workers, 1);
+    if (o.buffer_capacity < 1) o.buffer_capacity = 2048;
+}
+
+void check_supported(ssjb::Options& o) {
+    if (o.algorithm == ssjb::Algo::Naive || is_prefix_algo(o.algorithm)) return;
     if (o.workers < 1) throw std::invalid_argument("workers must be >= 1");
     if (o.buffer_capacity < 1) throw std::invalid_argument("buffer capacity must be >= 1");
     if (o.sim != ssjb::Sim::Jaccard) throw std::invalid_argument("the data-parallel join takes a jaccard threshold");
@@ -254,6 +263,10 @@ void fill_report(ssj_report& rep, std::vector<ssjb::EngineResult>& parts, double
     s.ms_merge = ms_merge;
     for (auto& p : parts) {
         c.candidates += p.candidates;
+        c.pruned_length += p.pruned_length;
+        c.pruned_positional += p.pruned_positional;
+        c.pruned_suffix += p.pruned_suffix;
+        c.filter_evaluations += p.filter_evaluations;
         c.bitmap_tested += p.bitmap_tested;
         c.pruned_bitmap += p.pruned_bitmap;
         c.verified += p.verified;
@@ -384,6 +397,18 @@ int shards_per_device() {
 std::vector<ssjb::EngineResult> run_self_parts(const ssjb::Collection& coll, const ssjb::Options& o, size_t row_begin,
                                                size_t row_end, int devices, int first_device, int delivery) {
     if (coll.size() >= (size_t(1) << 31)) throw std::invalid_argument("collections above 2^31 records are not supported");
+    if (is_prefix_algo(o.algorithm)) {
+        if (row_begin == 0 && row_end == coll.size()) {
+            if (ssjb::engine_device_count() <= first_device)
+                throw ssjb::DeviceError("no CUDA device available for the B200 join");
+            std::vector<ssjb::EngineResult> parts(1);
+            ssjb::engine_prefix_join(coll, o, first_device, parts[0]);
+            return parts;
+        }
+        ssjb::Options ro = o;
+        to_row_join(ro);
+        return run_self_parts(coll, ro, row_begin, row_end, devices, first_device, delivery);
+    }
     const auto h0 = std::chrono::steady_clock::now();
     ssjb::JoinPlan whole = ssjb::make_plan(coll, o, row_begin, row_end);
     whole.delivery = delivery;
@@ -894,6 +919,7 @@ SSJB_API ssj_status ssjb_partition_rows(const ssj_collection* coll, const ssj_jo
         }
         ssjb::Options o = to_options(*opts);
         check_supported(o);
+        to_row_join(o);
         ssjb::JoinPlan plan = ssjb::make_plan(*coll->c, o, 0, coll->c->size());
         auto b = ssjb::partition_rows(*coll->c, plan, parts, 0, coll->c->size(),
                                       ssjb::engine_head_start(*coll->c, plan), head_weight());

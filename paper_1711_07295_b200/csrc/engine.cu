@@ -26,6 +26,7 @@
 #include "filter_tc2.cuh"
 #include "filter_tcm.cuh"
 #include "head_tc.cuh"
+#include "prefix_join.cuh"
 
 namespace ssjb {
 
@@ -3263,6 +3264,347 @@ void engine_join_rs(const Collection& R, const Collection& Sc, const RsPlan& pla
     out.index_s = 0;
     out.candidates_s = 0;
     out.verify_s = std::chrono::duration<double>(Clock::now() - t_start).count();
+}
+
+
+// ---------------------------------------------------------------------------
+// Prefix-filter joins: ALLPAIRS / PPJOIN / PPJOIN+ (reference
+// framework_join, src/join.cpp:132-189), GROUPJOIN (:197-329) and ADAPTJOIN
+// (:331-420) on the GPU with the reference's counters; kernels in
+// prefix_join.cuh.
+namespace {
+
+// In-place exclusive scan of d[0..n) (u64).
+void scan_u64(unsigned long long* d, uint64_t n, Arena& A, cudaStream_t s, uint64_t& launches) {
+    if (n == 0) return;
+    const uint64_t tiles = (n + dev::kScan64Tile - 1) / dev::kScan64Tile;
+    unsigned long long* sums = A.alloc<unsigned long long>(tiles + 1);
+    dev::scan64_tiles<<<static_cast<unsigned>(tiles), dev::kScan64Threads, 0, s>>>(d, n, sums);
+    ++launches;
+    CK(cudaGetLastError());
+    if (tiles > 1) {
+        scan_u64(sums, tiles, A, s, launches);
+        dev::scan64_add<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(d, n, sums);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+}
+
+uint64_t read_u64(const unsigned long long* d, cudaStream_t s) {
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h;
+}
+
+unsigned grid_for(uint64_t work, int sms, unsigned per_sm) {
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, uint64_t(sms) * per_sm)));
+}
+
+}  // namespace
+
+void engine_prefix_join(const Collection& c, const Options& o, int device, EngineResult& out) {
+    using Clock = std::chrono::steady_clock;
+    set_device(device);
+    static thread_local cudaStream_t streams[16] = {};
+    if (!streams[device & 15]) CK(cudaStreamCreateWithFlags(&streams[device & 15], cudaStreamNonBlocking));
+    cudaStream_t s = streams[device & 15];
+    EngineStats& st = out.stats;
+    const auto t_start = Clock::now();
+    const uint64_t n = c.size();
+    if (n < 2) {
+        out.index_s = out.candidates_s = out.verify_s = 0;
+        return;
+    }
+    const bool group = o.algorithm == Algo::GroupJoin;
+    const bool adapt = o.algorithm == Algo::AdaptJoin;
+    const int L = adapt ? std::max(1, o.ell_max) : 1;  // index / tally prefix extension
+    if (L > dev::kAdaptMaxEll)
+        throw std::invalid_argument("ell_max above " + std::to_string(dev::kAdaptMaxEll) + " is not supported");
+    Timer T(s);
+    Arena A(s);
+    cudaEvent_t e0 = T.mark();
+    auto rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
+
+    // host tables over record sizes (exact, reference src/similarity.cpp)
+    const uint32_t ms = c.max_size, ms1 = ms + 1;
+    std::vector<int32_t> plen_ell(static_cast<size_t>(L) * ms1), ellcap(ms1, 1);
+    std::vector<uint32_t> lower(ms1), upper(ms1);
+    for (uint32_t z = 0; z <= ms; ++z) {
+        for (int l = 1; l <= L; ++l)
+            plen_ell[static_cast<size_t>(l - 1) * ms1 + z] = static_cast<int32_t>(prefix_length(o.sim, o.threshold, z, l));
+        const LengthWindow w = length_window(o.sim, o.threshold, z);
+        lower[z] = static_cast<uint32_t>(std::min<int64_t>(w.lower, UINT32_MAX));
+        upper[z] = static_cast<uint32_t>(std::min<int64_t>(w.upper, UINT32_MAX));
+        if (adapt) {
+            const int64_t need = required_overlap(o.sim, o.threshold, z, std::max<int64_t>(w.lower, 0));
+            ellcap[z] = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(L, need)));
+        }
+    }
+    std::vector<int32_t> minov = minov_table(o.sim, o.threshold, 2 * static_cast<size_t>(ms));
+    int32_t *d_plen = nullptr, *d_minov = nullptr, *d_ellcap = nullptr;
+    uint32_t *d_lower = nullptr, *d_upper = nullptr;
+    TableStage stage;
+    stage.add(&d_plen, plen_ell.data(), plen_ell.size() * 4);
+    stage.add(&d_minov, minov.data(), minov.size() * 4);
+    stage.add(&d_lower, lower.data(), lower.size() * 4);
+    stage.add(&d_upper, upper.data(), upper.size() * 4);
+    stage.add(&d_ellcap, ellcap.data(), ellcap.size() * 4);
+    stage.flush(A, s, st.h2d_bytes);
+    // the index holds ell = L prefixes; framework / group probes use ell = 1
+    const int32_t* d_plen_index = d_plen + static_cast<size_t>(L - 1) * ms1;
+
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+
+    // sketches (src/join.cpp:139-140: every record, the resolved config)
+    const ResolvedBitmap rb = resolve_bitmap(c, o);
+    uint64_t* bits = nullptr;
+    const int W = rb.width / 64;
+    if (rb.enabled) {
+        bits = A.alloc<uint64_t>((n + kPadRows) * W);
+        if (!launch_build_sub(*rep, bits, nullptr, rb.method, rb.width, 0, rb.hash, s, st.launches))
+            launch_build(*rep, bits, rb.method, rb.width, rb.hash, s, st.launches);
+    }
+    const bool f2 = !group && !adapt && rb.enabled && o.placement == 1;
+    const bool f3 = !group && !adapt && rb.enabled && !f2;
+
+    // GroupJoin groups: runs of equal (size, full prefix) (src/join.cpp:205-219)
+    uint32_t* grp_begin = nullptr;
+    uint64_t U = n;
+    if (group) {
+        unsigned long long* flag = A.alloc<unsigned long long>(n + 1);
+        CK(cudaMemsetAsync(flag + n, 0, 8, s));
+        dev::group_flags<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(rep->tokens, rep->offsets, rep->sizes,
+                                                                              d_plen, static_cast<uint32_t>(n), flag);
+        ++st.launches;
+        CK(cudaGetLastError());
+        scan_u64(flag, n + 1, A, s, st.launches);
+        U = read_u64(flag + n, s);
+        grp_begin = A.alloc<uint32_t>(U + 1);
+        dev::group_begins<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(flag, static_cast<uint32_t>(n),
+                                                                               grp_begin, rep->sizes, nullptr);
+        ++st.launches;
+        CK(cudaGetLastError());
+    }
+
+    // inverted prefix index: postings (token << 32 | id, pos), sorted
+    unsigned long long* pcnt = A.alloc<unsigned long long>(U + 1);
+    CK(cudaMemsetAsync(pcnt + U, 0, 8, s));
+    dev::prefix_counts<<<static_cast<unsigned>((U + 255) / 256), 256, 0, s>>>(rep->sizes, grp_begin, d_plen_index,
+                                                                            static_cast<uint32_t>(U), pcnt);
+    ++st.launches;
+    CK(cudaGetLastError());
+    scan_u64(pcnt, U + 1, A, s, st.launches);
+    const uint64_t P = read_u64(pcnt + U, s);
+    if (P >= (uint64_t(1) << 32)) throw std::invalid_argument("prefix index above 2^32 postings is not supported");
+    SortBufs IB{};
+    IB.ka = A.alloc<unsigned long long>(P);
+    IB.kb = A.alloc<unsigned long long>(P);
+    IB.va = A.alloc<uint32_t>(P);
+    IB.vb = A.alloc<uint32_t>(P);
+    {
+        const uint64_t ntiles = (P + dev::kSortTile - 1) / dev::kSortTile;
+        IB.hist = A.alloc<uint32_t>(256ull * std::max<uint64_t>(ntiles, 1));
+        IB.sums = A.alloc<uint32_t>((256ull * std::max<uint64_t>(ntiles, 1) + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+    }
+    IB.count_store = pcnt + U;
+    IB.count = pcnt + U;
+    dev::prefix_emit<<<static_cast<unsigned>((U * 32 + 255) / 256), 256, 0, s>>>(
+        rep->tokens, rep->offsets, rep->sizes, grp_begin, d_plen_index, static_cast<uint32_t>(U), pcnt, IB.ka, IB.va);
+    ++st.launches;
+    CK(cudaGetLastError());
+    int idbits = 1;
+    while ((uint64_t(1) << idbits) < std::max<uint64_t>(c.universe, U) + 1) ++idbits;
+    const bool inb = sort_results(IB, P, idbits, s, st.launches);
+    const unsigned long long* pkey = inb ? IB.kb : IB.ka;
+    const uint32_t* ppos = inb ? IB.vb : IB.va;
+    unsigned long long* eoff = A.alloc<unsigned long long>(P + 1);
+    CK(cudaMemsetAsync(eoff + P, 0, 8, s));
+    if (P)
+        dev::prefix_encounter_counts<<<static_cast<unsigned>((P + 255) / 256), 256, 0, s>>>(pkey, P, eoff);
+    ++st.launches;
+    CK(cudaGetLastError());
+    scan_u64(eoff, P + 1, A, s, st.launches);
+    const uint64_t E = read_u64(eoff + P, s);
+    cudaEvent_t e_index = T.mark();
+    st.window_pairs = E;  // encounters (pair x common prefix token)
+
+    unsigned long long* ctr = A.alloc<unsigned long long>(dev::kPcSlots);
+    dev::PrefixParams PP{};
+    PP.tokens = rep->tokens;
+    PP.offsets = rep->offsets;
+    PP.sizes = rep->sizes;
+    PP.rec = grp_begin;  // group g's representative = its first record
+    PP.pkey = pkey;
+    PP.ppos = ppos;
+    PP.eoff = eoff;
+    PP.P = P;
+    PP.E = E;
+    PP.plen = d_plen_index;
+    PP.lower = d_lower;
+    PP.upper = d_upper;
+    PP.need.minov = d_minov;
+    PP.need.cosine = o.sim == Sim::Cosine ? 1 : 0;
+    PP.need.cp = o.threshold.num;
+    PP.need.cq = o.threshold.den;
+    PP.positional = o.algorithm == Algo::PPJoin || o.algorithm == Algo::PPJoinPlus || group;
+    PP.suffix = o.algorithm == Algo::PPJoinPlus;
+    PP.suffix_depth = o.suffix_depth;
+    PP.f2 = f2;
+    PP.f3 = f3;
+    PP.bits = rb.enabled ? bits : nullptr;
+    PP.words = W;
+    PP.cutoff = rb.cutoff;
+    PP.ctr = ctr;
+    PP.group_mode = group;
+    PP.grp_begin = grp_begin;
+    PP.ell_max = L;
+    PP.plen_ell = d_plen;
+    PP.max_size = ms;
+    PP.n_rows = static_cast<uint32_t>(n);
+
+    uint64_t res_cap = std::min<uint64_t>(std::max<uint64_t>(E, 1024), env_u64("SSJB_PREFIX_RESULT_CAP", uint64_t(1) << 26));
+    uint64_t item_cap = group ? std::min<uint64_t>(std::max<uint64_t>(E + U, 1024), uint64_t(1) << 26) : 0;
+    unsigned long long h[dev::kPcSlots];
+    double ms_filter = 0, ms_verify = 0;
+    uint64_t R = 0;
+    SortBufs RB{};
+    for (;;) {  // re-run with larger buffers if the results / items overflowed
+        CK(cudaMemsetAsync(ctr, 0, dev::kPcSlots * 8, s));
+        RB = SortBufs{};
+        RB.ka = A.alloc<unsigned long long>(res_cap);
+        RB.va = A.alloc<uint32_t>(res_cap);
+        PP.res_keys = RB.ka;
+        PP.res_ov = RB.va;
+        PP.res_cap = res_cap;
+        PP.items = group ? A.alloc<uint2>(item_cap) : nullptr;
+        PP.item_cap = item_cap;
+        cudaEvent_t f0 = T.mark();
+        if (adapt) {
+            const uint64_t nL = n * static_cast<uint64_t>(L);
+            uint32_t* tallies = A.alloc<uint32_t>(4 * nL + n);
+            CK(cudaMemsetAsync(tallies, 0, (4 * nL + n) * 4, s));
+            PP.a_touch = tallies;
+            PP.a_alive = tallies + nL;
+            PP.a_len = tallies + 2 * nL;
+            PP.a_bmp = tallies + 3 * nL;
+            PP.a_bt = tallies + 4 * nL;
+            uint8_t* ell = A.alloc<uint8_t>(n);
+            PP.adapt = 1;
+            if (E) dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            ++st.launches;
+            CK(cudaGetLastError());
+            dev::AdaptRowParams AR{};
+            AR.tokens = rep->tokens;
+            AR.offsets = rep->offsets;
+            AR.sizes = rep->sizes;
+            AR.pkey = pkey;
+            AR.P = P;
+            AR.plen_ell = d_plen;
+            AR.ellcap = d_ellcap;
+            AR.max_size = ms;
+            AR.ell_max = L;
+            AR.avg = c.mean_size();
+            AR.n = static_cast<uint32_t>(n);
+            AR.touch = PP.a_touch;
+            AR.alive = PP.a_alive;
+            AR.len = PP.a_len;
+            AR.bmp = PP.a_bmp;
+            AR.bt = PP.a_bt;
+            AR.ell_out = ell;
+            AR.ctr = ctr;
+            dev::adapt_rows<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(AR);
+            ++st.launches;
+            CK(cudaGetLastError());
+            PP.adapt = 2;
+            PP.a_ell = ell;
+            if (E) dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            ++st.launches;
+            CK(cudaGetLastError());
+        } else if (E) {
+            dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            ++st.launches;
+            CK(cudaGetLastError());
+        }
+        cudaEvent_t f1 = T.mark();
+        if (group) {
+            dev::group_intra<<<static_cast<unsigned>((U + 255) / 256), 256, 0, s>>>(grp_begin, static_cast<uint32_t>(U),
+                                                                                  PP.items, item_cap, ctr);
+            ++st.launches;
+            CK(cudaGetLastError());
+            const uint64_t m = read_u64(ctr + dev::kPcItems, s);
+            if (m > item_cap) {
+                item_cap = m;
+                continue;
+            }
+            if (m) {
+                unsigned long long* foff = A.alloc<unsigned long long>(m + 1);
+                CK(cudaMemsetAsync(foff + m, 0, 8, s));
+                dev::group_item_sizes<<<static_cast<unsigned>((m + 255) / 256), 256, 0, s>>>(PP.items, m, grp_begin, foff);
+                ++st.launches;
+                CK(cudaGetLastError());
+                scan_u64(foff, m + 1, A, s, st.launches);
+                const uint64_t total = read_u64(foff + m, s);
+                if (total) dev::group_expand<<<grid_for(total, sms, 8), 256, 0, s>>>(PP, PP.items, m, foff, total);
+                ++st.launches;
+                CK(cudaGetLastError());
+            }
+        }
+        cudaEvent_t f2e = T.mark();
+        CK(cudaMemcpyAsync(h, ctr, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ms_filter = Timer::ms(f0, f1);
+        ms_verify = Timer::ms(f1, f2e);
+        R = h[dev::kPcResults];
+        if (R > res_cap) {
+            res_cap = R;
+            continue;
+        }
+        break;
+    }
+    out.candidates = h[dev::kPcCandidates];
+    out.pruned_length = h[dev::kPcPrunedLength];
+    out.pruned_positional = h[dev::kPcPrunedPositional];
+    out.pruned_suffix = h[dev::kPcPrunedSuffix];
+    out.pruned_bitmap = h[dev::kPcPrunedBitmap];
+    out.bitmap_tested = h[dev::kPcBitmapTested];
+    out.filter_evaluations = h[dev::kPcFilterEvals];
+    out.verified = h[dev::kPcVerified];
+    out.matched = h[dev::kPcMatched];
+    st.survivors = out.verified;
+
+    // canonical order (src/join.cpp:30-32), one packed download
+    cudaEvent_t s0 = T.mark();
+    if (R) {
+        RB.kb = A.alloc<unsigned long long>(R);
+        RB.vb = A.alloc<uint32_t>(R);
+        const uint64_t ntiles = (R + dev::kSortTile - 1) / dev::kSortTile;
+        RB.hist = A.alloc<uint32_t>(256ull * ntiles);
+        RB.sums = A.alloc<uint32_t>((256ull * ntiles + dev::kScanBlock - 1) / dev::kScanBlock + 1);
+        RB.count = ctr + dev::kPcResults;
+        int rbits = 1;
+        while ((uint64_t(1) << rbits) < n + 1) ++rbits;
+        const bool rin = sort_results(RB, R, rbits, s, st.launches);
+        PairOut* packed = A.alloc<PairOut>(R);
+        pack_pairs<<<static_cast<unsigned>((R + 255) / 256), 256, 0, s>>>(rin ? RB.kb : RB.ka, rin ? RB.vb : RB.va,
+                                                                          packed, R);
+        ++st.launches;
+        CK(cudaGetLastError());
+        out.pairs.resize(R);
+        d2h_staged(out.pairs.data(), packed, R * sizeof(PairOut), s);
+        st.d2h_bytes += R * sizeof(PairOut);
+    }
+    cudaEvent_t s1 = T.mark();
+    CK(cudaStreamSynchronize(s));
+    st.ms_upload = Timer::ms(e0, e_index);
+    st.ms_filter = ms_filter;
+    st.ms_verify = ms_verify;
+    st.ms_sort = Timer::ms(s0, s1);
+    st.batches = 1;
+    out.index_s = Timer::ms(e0, e_index) / 1e3;
+    out.candidates_s = ms_filter / 1e3;
+    out.verify_s = std::chrono::duration<double>(Clock::now() - t_start).count() - out.index_s - out.candidates_s;
 }
 
 }  // namespace ssjb

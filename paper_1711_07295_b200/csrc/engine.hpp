@@ -83,6 +83,8 @@ struct EngineResult {
     PairVec pairs;  // sorted by (id_r, id_s)
     std::shared_ptr<DeviceRuns> runs;  // delivery 2: further sorted runs in HBM (null if none)
     uint64_t candidates = 0, bitmap_tested = 0, pruned_bitmap = 0, verified = 0, matched = 0;
+    // prefix-filter joins only (engine_prefix_join)
+    uint64_t pruned_length = 0, pruned_positional = 0, pruned_suffix = 0, filter_evaluations = 0;
     uint64_t saturated = 0;
     double index_s = 0, candidates_s = 0, verify_s = 0;
     EngineStats stats;
@@ -91,6 +93,9 @@ struct EngineResult {
 int engine_device_count();
 // One shard (plan.row_begin..row_end) of a self-join on `device`.
 void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineResult& out);
+// ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN / ADAPTJOIN self-join of the whole
+// collection on `device` (reference src/join.cpp:132-420), reference counters.
+void engine_prefix_join(const Collection& c, const Options& o, int device, EngineResult& out);
 // NAIVE RS-join block (plan.r_begin..r_end of R) x S on `device`; pairs are
 // (R id, S id), sorted.
 void engine_join_rs(const Collection& r, const Collection& s, const RsPlan& plan, int device, EngineResult& out);

@@ -813,6 +813,47 @@ int64_t required_overlap(Sim f, const Rational& t, int64_t size_r, int64_t size_
     return std::max<int64_t>(1, v);
 }
 
+LengthWindow length_window(Sim f, const Rational& t, int64_t size_r) {
+    // reference src/similarity.cpp:117-142 (sizes and thresholds are non-negative)
+    const __int128 p = t.num, q = t.den, n = size_r;
+    const int64_t unbounded = std::numeric_limits<int64_t>::max();
+    LengthWindow w;
+    switch (f) {
+        case Sim::Overlap:
+            w.lower = t.num;
+            w.upper = unbounded;
+            break;
+        case Sim::Jaccard:
+            w.lower = ceil_div(n * p, q);
+            w.upper = p == 0 ? unbounded : static_cast<int64_t>(n * q / p);
+            break;
+        case Sim::Cosine:
+            w.lower = ceil_div(n * p * p, q * q);
+            w.upper = static_cast<int64_t>(n * q * q / (p * p));
+            break;
+        case Sim::Dice:
+            w.lower = ceil_div(n * p, 2 * q - p);
+            w.upper = static_cast<int64_t>(n * (2 * q - p) / p);
+            break;
+    }
+    if (w.lower < 0) w.lower = 0;
+    return w;
+}
+
+int64_t prefix_length(Sim f, const Rational& t, int64_t size_r, int ell) {
+    // reference src/similarity.cpp:144-166
+    const __int128 p = t.num, q = t.den, n = size_r;
+    int64_t base = 0;
+    switch (f) {
+        case Sim::Overlap: base = size_r - t.num + 1; break;
+        case Sim::Jaccard: base = static_cast<int64_t>(n * (q - p) / q) + 1; break;
+        case Sim::Cosine: base = static_cast<int64_t>(n * (q * q - p * p) / (q * q)) + 1; break;
+        case Sim::Dice: base = static_cast<int64_t>(n * (2 * q - 2 * p) / (2 * q - p)) + 1; break;
+    }
+    const int64_t len = base + (ell - 1);
+    return std::min<int64_t>(std::max<int64_t>(len, 0), size_r);
+}
+
 std::vector<int32_t> minov_table(Sim f, const Rational& t, size_t smax) {
     std::vector<int32_t> m(smax + 1, 1);
     if (f == Sim::Cosine) return m;  // depends on |r|*|s|: computed per pair

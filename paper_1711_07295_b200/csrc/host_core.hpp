@@ -143,6 +143,9 @@ struct Options {
     int64_t cutoff_value = 0;
     int workers = 1;
     int buffer_capacity = 2048;
+    int placement = 0;     // 0 default (filter3), 1 filter2, 2 filter3 (reference src/join.hpp:13)
+    int suffix_depth = 2;  // PPJoin+ partition rounds
+    int ell_max = 3;       // AdaptJoin prefix extension cap
 };
 
 struct ResolvedBitmap {
@@ -190,6 +193,16 @@ struct RsPlan {
     int delivery = 0;            // as JoinPlan::delivery
 };
 RsPlan make_rs_plan(const Collection& r, const Collection& s, const Options& o, size_t r_begin, size_t r_end);
+
+// Prefix-filter bounds (reference src/similarity.cpp:117-166): the length
+// window of a probe of size `size_r` (upper clamped to UINT32_MAX) and the
+// prefix length at `ell`.
+struct LengthWindow {
+    int64_t lower = 0;
+    int64_t upper = 0;
+};
+LengthWindow length_window(Sim f, const Rational& t, int64_t size_r);
+int64_t prefix_length(Sim f, const Rational& t, int64_t size_r, int ell);
 
 uint32_t window_start_of(const Collection& c, const JoinPlan& plan, size_t row);
 JoinPlan make_plan(const Collection& c, const Options& o, size_t row_begin, size_t row_end);

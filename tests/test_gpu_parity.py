@@ -291,10 +291,11 @@ def test_concurrent_joins_from_threads(lib, golden, colls):
 @pytest.mark.parametrize("sim", [capi.SSJ_SIM_JACCARD, capi.SSJ_SIM_COSINE, capi.SSJ_SIM_DICE,
                                  capi.SSJ_SIM_OVERLAP])
 def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim):
-    """ssj_join with ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN / ADAPTJOIN returns
-    the reference's pair list for that algorithm (run live from oracle/_ref on
-    the same collection and options) for every similarity function; the
-    counters satisfy the reference's invariants."""
+    """ssj_join with ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN / ADAPTJOIN (the
+    GPU prefix-filter engine) returns the reference's pair list AND all nine
+    counters for that algorithm (run live from oracle/_ref on the same
+    collection and options) for every similarity function, bitmap off / on
+    (filter3) / filter2."""
     rng = np.random.default_rng(77 + sim)
     for trial in range(6):
         n = int(rng.integers(100, 900))
@@ -304,7 +305,8 @@ def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim)
         theirs = S.Collection.generate(ref, **gen)
         thr = (int(rng.integers(2, 8)), 1) if sim == capi.SSJ_SIM_OVERLAP else (int(rng.integers(4, 10)), 10)
         for algo in (1, 2, 3, 4, 5):
-            kw = dict(algorithm=algo, similarity=sim, threshold=thr, bitmap_enabled=int(trial % 2),
+            kw = dict(algorithm=algo, similarity=sim, threshold=thr, bitmap_enabled=int(trial % 3 != 0),
+                      placement=capi.SSJ_PLACEMENT_FILTER2 if trial % 3 == 2 else capi.SSJ_PLACEMENT_DEFAULT,
                       workers=2)
             want = S.join(theirs, S.default_options(ref, **kw))
             got = S.join(mine, S.default_options(lib, **kw))
@@ -313,3 +315,4 @@ def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim)
             assert c["candidates"] == (c["pruned_length"] + c["pruned_positional"] + c["pruned_suffix"]
                                        + c["pruned_bitmap"] + c["verified"])
             assert c["matched"] == len(got.pairs)
+            assert c == want.counters, (sim, algo, trial)

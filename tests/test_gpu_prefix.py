@@ -1,0 +1,76 @@
+"""GPU prefix-filter joins against the reference's own runs.
+
+ssj_join with ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN / ADAPTJOIN runs the
+GPU prefix-filter engine (csrc/prefix_join.cuh): every case of
+tests/golden/golden_prefix.json (made by make_golden_prefix.py from the
+unmodified reference, src/join.cpp:132-420) must give the same sorted pair
+list and the same nine counters -- the algorithm-specific ones included
+(filter_evaluations, pruned_length / positional / suffix, bitmap_tested)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR
+from paper_1711_07295_b200 import capi
+from paper_1711_07295_b200 import ssjoin as S
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def gp():
+    with open(os.path.join(GOLDEN_DIR, "golden_prefix.json")) as f:
+        cases = json.load(f)["cases"]
+    return cases, np.load(os.path.join(GOLDEN_DIR, "golden_prefix.npz"))
+
+
+def options_of(lib, case):
+    o = S.default_options(lib)
+    for k, v in case["options"].items():
+        setattr(o, k, v)
+    return o
+
+
+def test_prefix_fixtures_are_consistent(gp):
+    """CPU: the committed fixtures hold the reference's counter invariants
+    (tests/test_joins.cpp:14-19) and their stored pair arrays match the shas."""
+    cases, arr = gp
+    algos = set()
+    for c in cases:
+        k = c["counters"]
+        assert k["candidates"] == (k["pruned_length"] + k["pruned_positional"] + k["pruned_suffix"] +
+                                   k["pruned_bitmap"] + k["verified"]), c["id"]
+        assert k["matched"] == c["pair_count"]
+        if f"pairs/{c['id']}" in arr:
+            assert sha(arr[f"pairs/{c['id']}"]) == c["pairs_sha256"]
+        algos.add(c["options"]["algorithm"])
+    assert algos == {1, 2, 3, 4, 5}
+    assert any(c["counters"]["pruned_suffix"] for c in cases)
+    assert any(c["counters"]["pruned_positional"] for c in cases)
+    assert any(c["counters"]["pruned_bitmap"] and c["options"]["placement"] == 1 for c in cases)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", [1, 2, 3, 4, 5])
+def test_prefix_joins_match_reference_fixtures(lib, gp, algo):
+    cases, arr = gp
+    colls = {}
+    n = 0
+    for c in cases:
+        if c["options"]["algorithm"] != algo:
+            continue
+        name = c["collection"]
+        if name not in colls:
+            colls[name] = S.Collection.from_csr(lib, arr[f"coll/{name}/tokens"], arr[f"coll/{name}/offsets"])
+        rep = S.join(colls[name], options_of(lib, c))
+        where = (c["id"], c["label"], c["collection"])
+        assert rep.counters == c["counters"], (where, rep.counters, c["counters"])
+        assert len(rep.pairs) == c["pair_count"], where
+        assert sha(rep.pairs) == c["pairs_sha256"], where
+        n += 1
+    assert n > 200
