@@ -474,7 +474,7 @@ def k3_roofline(vb_step, ver_ms, hbm_peak):
            "bytes_formula": "4*(|r|+|s|) per merged survivor + 16 per match (SURVEY 8d upper bound)"}
     if ach > hbm_peak:
         out["note"] = ("algorithmic bytes above the HBM peak: the survivors' records are L2-resident and the "
-                       "early exit stops most merges early; ncu of the launches: profiles/r02n_c4_kernels_ncu.md")
+                       "early exit stops most merges early; ncu of the launches: profiles/r02ao_c4_kernels_ncu.md")
     return out
 
 

@@ -3464,7 +3464,14 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
     PP.max_size = ms;
     PP.n_rows = static_cast<uint32_t>(n);
 
-    uint64_t res_cap = std::min<uint64_t>(std::max<uint64_t>(E, 1024), env_u64("SSJB_PREFIX_RESULT_CAP", uint64_t(1) << 26));
+    // result buffer: matches <= first encounters <= E; sized from free HBM
+    // (40 B per result: keys / overlaps, sort buffers, packed pairs) so a
+    // re-run after an overflow is the exception
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t res_cap = std::min<uint64_t>(std::max<uint64_t>(E, 1024),
+                                          std::max<uint64_t>(free_b / 2 / 40, uint64_t(1) << 20));
+    res_cap = std::min<uint64_t>(res_cap, env_u64("SSJB_PREFIX_RESULT_CAP", ~uint64_t(0)));
     uint64_t item_cap = group ? std::min<uint64_t>(std::max<uint64_t>(E + U, 1024), uint64_t(1) << 26) : 0;
     unsigned long long h[dev::kPcSlots];
     double ms_filter = 0, ms_verify = 0;
@@ -3492,7 +3499,7 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
             PP.a_bt = tallies + 4 * nL;
             uint8_t* ell = A.alloc<uint8_t>(n);
             PP.adapt = 1;
-            if (E) dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            if (E) dev::adapt_tally<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
             ++st.launches;
             CK(cudaGetLastError());
             dev::AdaptRowParams AR{};

@@ -793,7 +793,9 @@ int64_t required_overlap(Sim f, const Rational& t, int64_t size_r, int64_t size_
             unsigned __int128 target = static_cast<unsigned __int128>(p) * static_cast<unsigned __int128>(p);
             target *= static_cast<unsigned __int128>(size_r) * static_cast<unsigned __int128>(size_s);
             uint64_t root = 0;
-            if (target != 0) {  // isqrt_ceil (src/rational.cpp:51-71)
+            if (target == 1) {
+                root = 1;  // isqrt_floor(0) = 0 (src/rational.cpp:51-52)
+            } else if (target != 0) {  // isqrt_ceil (src/rational.cpp:51-71)
                 const unsigned __int128 m = target - 1;
                 unsigned __int128 x = static_cast<unsigned __int128>(std::sqrt(static_cast<long double>(m)));
                 if (x == 0) x = 1;

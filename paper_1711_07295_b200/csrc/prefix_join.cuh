@@ -174,8 +174,20 @@ __device__ __forceinline__ void pfx_count(unsigned long long* acc, int slot, uns
     acc[slot] += v;
 }
 
+// One slot of a global counter per calling lane, one atomic per warp: the
+// lanes active at the call (coalesced group) share the leader's claim.
+__device__ __forceinline__ unsigned long long warp_claim(unsigned long long* counter) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(m, base, leader);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ void pfx_emit(const PrefixParams& P, uint32_t lo, uint32_t hi, uint32_t overlap) {
-    const unsigned long long slot = atomicAdd(P.ctr + kPcResults, 1ull);
+    const unsigned long long slot = warp_claim(P.ctr + kPcResults);
     if (slot < P.res_cap) {
         P.res_keys[slot] = (static_cast<unsigned long long>(lo) << 32) | hi;
         P.res_ov[slot] = overlap;
@@ -210,6 +222,37 @@ __device__ __forceinline__ uint64_t pfx_find_posting(const PrefixParams& P, unsi
     return lo;
 }
 
+// AdaptJoin (src/join.cpp:330-420) per pair: the walks use prefixes of
+// ell = 1..ell_max and the index holds ell_max prefixes, so the first common
+// token is taken over those.  cnt[l]: common tokens inside both records'
+// (l + 1)-prefixes = the pair's match count in the walk at ell = l + 1
+// (touched iff > 0).  Causes: length (every walk), bitmap (pruned by the
+// first walk's in-loop test, then killed on first touch by later walks).
+__device__ __forceinline__ void adapt_pair(const PrefixParams& P, uint32_t rr, uint32_t ss, uint32_t nr, uint32_t ns,
+                                           const uint32_t* Tr, const uint32_t* Ts, uint32_t i, uint32_t pos,
+                                           uint32_t (&cnt)[kAdaptMaxEll], bool& inwin, bool& bskip,
+                                           long long& minov) {
+    const uint32_t ms1 = P.max_size + 1;
+    const int L = P.ell_max;
+    inwin = ns >= P.lower[nr] && ns <= P.upper[nr];
+    minov = need_overlap(P.need, nr, ns);
+    bskip = inwin && P.bits && pfx_bitmap_skip(P, rr, ss, nr, ns, minov);
+#pragma unroll
+    for (int l = 0; l < kAdaptMaxEll; ++l) cnt[l] = 0;
+    uint32_t ii = i, pp = pos;
+    const uint32_t plr = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + nr]);
+    const uint32_t pls = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + ns]);
+    do {
+#pragma unroll
+        for (int l = 0; l < kAdaptMaxEll; ++l)
+            if (l < L && ii < static_cast<uint32_t>(P.plen_ell[l * ms1 + nr]) &&
+                pp < static_cast<uint32_t>(P.plen_ell[l * ms1 + ns]))
+                ++cnt[l];
+        ++ii;
+        ++pp;
+    } while (next_common(Tr, plr, Ts, pls, ii, pp));
+}
+
 // One thread per encounter; the thread holding a pair's first common prefix
 // token replays the pair's probe walk (src/prefix_index.cpp:70-133) and the
 // join's candidate loop (src/join.cpp:160-181 / :300-326).
@@ -239,42 +282,11 @@ __global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
             // inside both records' (l + 1)-prefixes = the pair's match count
             // in the walk at ell = l + 1 (touched iff > 0).
             if (spans_intersect(Tr, i, Ts, pos)) continue;
-            const uint32_t ms1 = P.max_size + 1;
-            const int L = P.ell_max;
-            const bool inwin = ns >= P.lower[nr] && ns <= P.upper[nr];
-            const long long minov = need_overlap(P.need, nr, ns);
-            const bool bskip = inwin && P.bits && pfx_bitmap_skip(P, rr, ss, nr, ns, minov);
             uint32_t cnt[kAdaptMaxEll];
-#pragma unroll
-            for (int l = 0; l < kAdaptMaxEll; ++l) cnt[l] = 0;
-            uint32_t ii = i, pp = pos;
-            const uint32_t plr = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + nr]);
-            const uint32_t pls = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + ns]);
-            do {
-#pragma unroll
-                for (int l = 0; l < kAdaptMaxEll; ++l)
-                    if (l < L && ii < static_cast<uint32_t>(P.plen_ell[l * ms1 + nr]) &&
-                        pp < static_cast<uint32_t>(P.plen_ell[l * ms1 + ns]))
-                        ++cnt[l];
-                ++ii;
-                ++pp;
-            } while (next_common(Tr, plr, Ts, pls, ii, pp));
-            // cause: length (any walk), bitmap (pruned by the first walk's
-            // in-loop test, then killed on first touch by later walks)
+            bool inwin, bskip;
+            long long minov;
+            adapt_pair(P, rr, ss, nr, ns, Tr, Ts, i, pos, cnt, inwin, bskip, minov);
             const bool bpruned = bskip && cnt[0] > 0;
-            if (P.adapt == 1) {
-                if (cnt[0] && inwin && P.bits) atomicAdd(P.a_bt + r, bskip ? 1u : cnt[0]);
-#pragma unroll
-                for (int l = 0; l < kAdaptMaxEll; ++l) {
-                    if (l >= L || !cnt[l]) continue;
-                    const uint64_t at = static_cast<uint64_t>(l) * P.n_rows + r;
-                    atomicAdd(P.a_touch + at, 1u);
-                    if (!inwin) atomicAdd(P.a_len + at, 1u);
-                    else if (bpruned) atomicAdd(P.a_bmp + at, 1u);
-                    else if (cnt[l] >= static_cast<uint32_t>(l + 1)) atomicAdd(P.a_alive + at, 1u);
-                }
-                continue;
-            }
             const int ell = P.a_ell[r];  // verify pass: the row's final walk
             if (!inwin || bpruned || cnt[ell - 1] < static_cast<uint32_t>(ell)) continue;
             // (verified is counted per row by adapt_rows)
@@ -341,7 +353,7 @@ __global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
             continue;
         }
         if (P.group_mode) {  // expanded to record pairs by group_expand
-            const unsigned long long slot = atomicAdd(P.ctr + kPcItems, 1ull);
+            const unsigned long long slot = warp_claim(P.ctr + kPcItems);
             if (slot < P.item_cap) P.items[slot] = make_uint2(r, s);
             continue;
         }
@@ -360,6 +372,66 @@ __global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
         }
     }
     pfx_flush(P, acc);
+}
+
+// AdaptJoin tally pass: per (probe row, ell) counts of touched, length-pruned,
+// bitmap-pruned and surviving (count >= ell) pairs, and the first walk's
+// bitmap evaluations.  Consecutive encounters mostly share the probe row, so
+// lanes with the same row (__match_any_sync) reduce first and one lane adds.
+__global__ void __launch_bounds__(256) adapt_tally(PrefixParams P) {
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned long long start = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const unsigned long long Eround = (P.E + 31) / 32 * 32;
+    const int L = P.ell_max;
+    for (unsigned long long e = start; e < Eround; e += stride) {
+        uint32_t key = 0xFFFFFFFFu, tmask = 0, amask = 0, btv = 0;
+        bool lenp = false, bmpp = false;
+        if (e < P.E) {
+            const uint64_t g = pfx_find_posting(P, e);
+            const uint64_t k = P.eoff[g + 1] - P.eoff[g];
+            const uint64_t a = g - k + (e - P.eoff[g]);
+            const uint32_t r = static_cast<uint32_t>(P.pkey[g]), s = static_cast<uint32_t>(P.pkey[a]);
+            const uint32_t i = P.ppos[g], pos = P.ppos[a];
+            const uint32_t nr = P.sizes[r], ns = P.sizes[s];
+            const uint32_t* Tr = P.tokens + P.offsets[r];
+            const uint32_t* Ts = P.tokens + P.offsets[s];
+            if (!spans_intersect(Tr, i, Ts, pos)) {
+                uint32_t cnt[kAdaptMaxEll];
+                bool inwin, bskip;
+                long long minov;
+                adapt_pair(P, r, s, nr, ns, Tr, Ts, i, pos, cnt, inwin, bskip, minov);
+                key = r;
+                lenp = !inwin;
+                bmpp = inwin && bskip && cnt[0] > 0;
+                if (cnt[0] && inwin && P.bits) btv = bskip ? 1u : cnt[0];
+#pragma unroll
+                for (int l = 0; l < kAdaptMaxEll; ++l) {
+                    if (l < L && cnt[l]) tmask |= 1u << l;
+                    if (l < L && cnt[l] >= static_cast<uint32_t>(l + 1)) amask |= 1u << l;
+                }
+            }
+        }
+        const unsigned grp = __match_any_sync(0xFFFFFFFFu, key);
+        if (key == 0xFFFFFFFFu) continue;
+        const bool lead = (threadIdx.x & 31) == __ffs(grp) - 1;
+        const uint32_t bt = __reduce_add_sync(grp, btv);
+        if (lead && bt) atomicAdd(P.a_bt + key, bt);
+        for (int l = 0; l < L; ++l) {
+            const uint32_t t = (tmask >> l) & 1u;
+            const uint32_t nt = __reduce_add_sync(grp, t);
+            if (!nt) continue;  // uniform over the group
+            const uint32_t nl = __reduce_add_sync(grp, t & (lenp ? 1u : 0u));
+            const uint32_t nb = __reduce_add_sync(grp, t & (bmpp ? 1u : 0u));
+            const uint32_t na = __reduce_add_sync(grp, t & (!lenp && !bmpp ? (amask >> l) & 1u : 0u));
+            if (lead) {
+                const uint64_t at = static_cast<uint64_t>(l) * P.n_rows + key;
+                atomicAdd(P.a_touch + at, nt);
+                if (nl) atomicAdd(P.a_len + at, nl);
+                if (nb) atomicAdd(P.a_bmp + at, nb);
+                if (na) atomicAdd(P.a_alive + at, na);
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------- index build

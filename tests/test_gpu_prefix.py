@@ -74,3 +74,23 @@ def test_prefix_joins_match_reference_fixtures(lib, gp, algo):
         assert sha(rep.pairs) == c["pairs_sha256"], where
         n += 1
     assert n > 200
+
+
+@pytest.mark.gpu
+def test_prefix_joins_survive_result_overflow(lib, gp, monkeypatch):
+    """A result buffer smaller than the output (SSJB_PREFIX_RESULT_CAP) makes
+    the engine re-run with the exact size: same pairs and counters."""
+    cases, arr = gp
+    monkeypatch.setenv("SSJB_PREFIX_RESULT_CAP", "1000")
+    done = set()
+    for c in cases:
+        algo = c["options"]["algorithm"]
+        if algo in done or not 5000 < c["pair_count"] < 200000:
+            continue
+        name = c["collection"]
+        coll = S.Collection.from_csr(lib, arr[f"coll/{name}/tokens"], arr[f"coll/{name}/offsets"])
+        rep = S.join(coll, options_of(lib, c))
+        assert rep.counters == c["counters"], c["id"]
+        assert sha(rep.pairs) == c["pairs_sha256"], c["id"]
+        done.add(algo)
+    assert done == {1, 2, 3, 4, 5}
