@@ -277,6 +277,7 @@ struct DeviceReplica {
     size_t n = 0;
     uint64_t tokens_total = 0;
     uint64_t bytes = 0;
+    const Collection* src = nullptr;  // host collection (sizes: first_ge) for launch shapes
     cudaStream_t stream = nullptr;  // set for per-join replicas: stream-ordered alloc/free
     std::shared_ptr<SketchSet> sketches;  // resident replicas only
     ~DeviceReplica() {
@@ -467,6 +468,7 @@ std::shared_ptr<DeviceReplica> upload(const Collection& c, int device, cudaStrea
     }
     rep->device = device;
     rep->n = n;
+    rep->src = &c;
     rep->tokens_total = c.tokens.size();
     uint64_t tok_h2d = 0;
     CK(cudaMemcpyAsync(rep->offsets, c.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
@@ -539,6 +541,7 @@ std::shared_ptr<DeviceReplica> upload_streamed(const Collection& c, int device, 
     const size_t T = c.tokens.size();
     const size_t tok_bytes = std::max<size_t>(T, 4) * sizeof(uint32_t) + 16;
     rep->stream = stream;
+    rep->src = &c;
     CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->tokens), tok_bytes, stream));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->offsets), (n + 1) * sizeof(uint64_t), stream));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&rep->sizes), (n + kPadRows + 8) * sizeof(uint32_t), stream));
@@ -834,13 +837,16 @@ using BuildFn2 = void (*)(dev::BuildParams2);
 
 // Set/Xor sketches (and the level-2 Xor sketch in the same token pass) with
 // several lanes per record; null when the shape has no instantiation.
-BuildFn2 build_sub_fn(int words, int words2, bool x) {
+BuildFn2 build_sub_fn(int words, int words2, bool x, bool big = false) {
 #define SSJB_SUB(W)                                      \
     case W:                                              \
         switch (words2) {                                \
-            case 0: return x ? dev::build_sketches_sub<W, 0, true> : dev::build_sketches_sub<W, 0, false>; \
-            case 4: return x ? dev::build_sketches_sub<W, 4, true> : dev::build_sketches_sub<W, 4, false>; \
-            case 8: return x ? dev::build_sketches_sub<W, 8, true> : dev::build_sketches_sub<W, 8, false>; \
+            case 0: return big ? (x ? dev::build_sketches_big<W, 0, true> : dev::build_sketches_big<W, 0, false>) \
+                               : (x ? dev::build_sketches_sub<W, 0, true> : dev::build_sketches_sub<W, 0, false>); \
+            case 4: return big ? (x ? dev::build_sketches_big<W, 4, true> : dev::build_sketches_big<W, 4, false>) \
+                               : (x ? dev::build_sketches_sub<W, 4, true> : dev::build_sketches_sub<W, 4, false>); \
+            case 8: return big ? (x ? dev::build_sketches_big<W, 8, true> : dev::build_sketches_big<W, 8, false>) \
+                               : (x ? dev::build_sketches_sub<W, 8, true> : dev::build_sketches_sub<W, 8, false>); \
         }                                                \
         break;
     switch (words) {
@@ -887,11 +893,29 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
     while (lg < 5 && (1 << lg) * 4.0 < mean / 4.0 + 1.0) ++lg;
     P.lpr_log2 = lg;
     P.total_tokens = rep.tokens_total;
-    const uint64_t threads = static_cast<uint64_t>(row1 - row0) << lg;
-    const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-    fn<<<grid, 256, 0, s>>>(P);
-    ++launches;
-    CK(cudaGetLastError());
+    // rows longer than ~4 rounds of their lane group (sizes ascend with the
+    // row) go to the CTA-per-record kernel
+    uint32_t big0 = row1;
+    if (rep.src && !rep.src->first_ge.empty() && !env_u64("SSJB_BUILD_NO_BIG", 0)) {
+        const uint64_t s_big = static_cast<uint64_t>(16) << lg << 2;  // 4 x 16 tokens per lane
+        if (s_big <= rep.src->max_size)
+            big0 = std::max<uint32_t>(row0, std::min<uint32_t>(row1, rep.src->first_ge[s_big + 1]));
+    }
+    if (big0 > row0) {
+        P.n = big0;
+        const uint64_t threads = static_cast<uint64_t>(big0 - row0) << lg;
+        const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+        fn<<<grid, 256, 0, s>>>(P);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+    if (big0 < row1) {
+        P.row0 = big0;
+        P.n = row1;
+        build_sub_fn(width / 64, bits2 ? width2 / 64 : 0, method == Method::Xor, true)<<<row1 - big0, 256, 0, s>>>(P);
+        ++launches;
+        CK(cudaGetLastError());
+    }
     return true;
 }
 
@@ -3498,7 +3522,6 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
             PP.a_bmp = tallies + 3 * nL;
             PP.a_bt = tallies + 4 * nL;
             uint8_t* ell = A.alloc<uint8_t>(n);
-            PP.adapt = 1;
             if (E) dev::adapt_tally<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
             ++st.launches;
             CK(cudaGetLastError());
@@ -3524,13 +3547,12 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
             dev::adapt_rows<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(AR);
             ++st.launches;
             CK(cudaGetLastError());
-            PP.adapt = 2;
             PP.a_ell = ell;
-            if (E) dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            if (E) dev::adapt_verify<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
             ++st.launches;
             CK(cudaGetLastError());
         } else if (E) {
-            dev::prefix_encounters<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            dev::prefix_encounters<<<grid_for(E, sms, 16), 256, 0, s>>>(PP);
             ++st.launches;
             CK(cudaGetLastError());
         }

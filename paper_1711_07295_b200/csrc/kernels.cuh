@@ -295,6 +295,106 @@ __global__ void __launch_bounds__(256) build_sketches_sub(BuildParams2 P) {
     }
 }
 
+// Records too long for a lane group (sizes are sorted, so they are the tail
+// rows of the build): one CTA per record, every thread folds 16-byte chunks
+// (four in flight), then warp shuffles and a shared-memory combine.  Without
+// this the last blocks of a heavy-tailed collection (C4: up to 40,425 tokens
+// per record on 8 lanes) run alone long after the rest of the grid.
+template <int W, int W2, bool XOR>
+__global__ void __launch_bounds__(256) build_sketches_big(BuildParams2 P) {
+    __shared__ uint64_t part[8][W + (W2 > 0 ? W2 : 0)];
+    const uint32_t r = P.row0 + blockIdx.x;
+    if (r >= P.n) return;
+    uint64_t row[W], row2[W2 > 0 ? W2 : 1];
+#pragma unroll
+    for (int w = 0; w < W; ++w) row[w] = 0;
+#pragma unroll
+    for (int w = 0; w < (W2 > 0 ? W2 : 1); ++w) row2[w] = 0;
+    auto fold = [&](uint32_t t) {
+        const uint32_t hm = P.hash_mult ? static_cast<uint32_t>((static_cast<uint64_t>(t) * 0x9E3779B97F4A7C15ull) >> 33)
+                                        : t;
+        const uint32_t h = hm % (64u * W);
+        const uint64_t bit = 1ull << (h & 63);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint64_t m = (W == 1 || (h >> 6) == uint32_t(w)) ? bit : 0ull;
+            row[w] = XOR ? (row[w] ^ m) : (row[w] | m);
+        }
+        if constexpr (W2 > 0) {
+            const uint32_t h2 = hm % (64u * W2);
+            const uint64_t bit2 = 1ull << (h2 & 63);
+#pragma unroll
+            for (int w = 0; w < W2; ++w) row2[w] ^= (h2 >> 6) == uint32_t(w) ? bit2 : 0ull;
+        }
+    };
+    const uint64_t b = P.offsets[r], e = P.offsets[r + 1];
+    const uint64_t a0 = b & ~uint64_t(3);
+    const uint32_t lo = static_cast<uint32_t>(b - a0), hi = static_cast<uint32_t>(e - a0);
+    const uint64_t rem = P.total_tokens - a0;
+    const uint32_t lim = rem > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(rem);
+    const uint32_t* base = P.tokens + a0;
+    constexpr uint32_t T = 256;
+    for (uint32_t c = 4u * threadIdx.x; c < hi; c += 16u * T) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t cc = c + 4u * T * u;
+            if (cc + 4 <= lim) {
+                v[u] = cc < hi ? __ldg(reinterpret_cast<const uint4*>(base + cc)) : make_uint4(0, 0, 0, 0);
+            } else {
+                v[u].x = cc < hi ? base[cc] : 0u;
+                v[u].y = cc + 1 < hi ? base[cc + 1] : 0u;
+                v[u].z = cc + 2 < hi ? base[cc + 2] : 0u;
+                v[u].w = 0u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t cc = c + 4u * T * u;
+            if (cc >= lo && cc + 4 <= hi) {
+                fold(v[u].x);
+                fold(v[u].y);
+                fold(v[u].z);
+                fold(v[u].w);
+            } else if (cc < hi) {
+                const uint32_t t4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (cc + q >= lo && cc + q < hi) fold(t4[q]);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, row[w], o);
+            row[w] = XOR ? (row[w] ^ v) : (row[w] | v);
+        }
+        if constexpr (W2 > 0) {
+#pragma unroll
+            for (int w = 0; w < W2; ++w) row2[w] ^= __shfl_xor_sync(0xFFFFFFFFu, row2[w], o);
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[warp][w] = row[w];
+        if constexpr (W2 > 0) {
+#pragma unroll
+            for (int w = 0; w < W2; ++w) part[warp][W + w] = row2[w];
+        }
+    }
+    __syncthreads();
+    constexpr int kAll = W + (W2 > 0 ? W2 : 0);
+    if (threadIdx.x < kAll) {
+        const int w = threadIdx.x;
+        uint64_t acc = part[0][w];
+        for (int k = 1; k < 8; ++k) acc = (XOR || w >= W) ? (acc ^ part[k][w]) : (acc | part[k][w]);
+        if (w < W) P.bits[static_cast<uint64_t>(r) * W + w] = acc;
+        else P.bits2[static_cast<uint64_t>(r) * W2 + (w - W)] = acc;
+    }
+}
+
 // ================================================================ K2: filter
 struct FilterParams {
     const uint64_t* bits;        // sketches, n * W words (padded by kColSub rows)

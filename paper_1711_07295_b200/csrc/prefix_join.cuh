@@ -72,7 +72,6 @@ struct PrefixParams {
     uint2* items;
     unsigned long long item_cap;
     // AdaptJoin (mode 2): per-(row, ell) tallies, ell_max prefixes per size
-    int adapt;                        // 1: tally pass, 2: verify pass
     int ell_max;
     const int32_t* plen_ell;          // plen_ell[(ell - 1) * (max_size + 1) + size]
     uint32_t max_size;
@@ -208,8 +207,8 @@ __device__ __forceinline__ void pfx_flush(const PrefixParams& P, unsigned long l
 
 // Posting g of the sorted index -> (token, index id, pos); eoff[g]..eoff[g+1]
 // are its encounters with the earlier postings of its list.
-__device__ __forceinline__ uint64_t pfx_find_posting(const PrefixParams& P, unsigned long long e) {
-    uint64_t lo = 0, len = P.P;  // last g with eoff[g] <= e
+__device__ __forceinline__ uint64_t pfx_find_posting_from(const PrefixParams& P, unsigned long long e, uint64_t lo) {
+    uint64_t len = P.P - lo;  // last g >= lo with eoff[g] <= e
     while (len > 0) {
         const uint64_t half = len >> 1;
         if (P.eoff[lo + half + 1] <= e) {
@@ -220,6 +219,23 @@ __device__ __forceinline__ uint64_t pfx_find_posting(const PrefixParams& P, unsi
         }
     }
     return lo;
+}
+
+// Called by all 32 lanes with consecutive encounters (e < E or not): lane 0
+// binary-searches the warp's first encounter, the others step forward from
+// it (a posting usually holds many encounters) and fall back to a search.
+__device__ __forceinline__ uint64_t pfx_find_posting(const PrefixParams& P, unsigned long long e) {
+    const unsigned long long e0 = __shfl_sync(0xFFFFFFFFu, e, 0);
+    uint64_t g0 = 0;
+    if ((threadIdx.x & 31) == 0) g0 = pfx_find_posting_from(P, min(e0, P.E - 1), 0);
+    g0 = __shfl_sync(0xFFFFFFFFu, g0, 0);
+    if (e >= P.E) return g0;
+    uint64_t g = g0;
+    for (int step = 0; step < 8; ++step) {
+        if (P.eoff[g + 1] > e) return g;
+        ++g;
+    }
+    return pfx_find_posting_from(P, e, g);
 }
 
 // AdaptJoin (src/join.cpp:330-420) per pair: the walks use prefixes of
@@ -256,7 +272,7 @@ __device__ __forceinline__ void adapt_pair(const PrefixParams& P, uint32_t rr, u
 // One thread per encounter; the thread holding a pair's first common prefix
 // token replays the pair's probe walk (src/prefix_index.cpp:70-133) and the
 // join's candidate loop (src/join.cpp:160-181 / :300-326).
-__global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
+__global__ void __launch_bounds__(256, 4) prefix_encounters(PrefixParams P) {
     unsigned long long acc[kPcResults];
 #pragma unroll
     for (int k = 0; k < kPcResults; ++k) acc[k] = 0;
@@ -264,8 +280,8 @@ __global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
     const unsigned long long start = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const unsigned long long Eround = (P.E + 31) / 32 * 32;  // whole warps for the flush
     for (unsigned long long e = start; e < Eround; e += stride) {
-        if (e >= P.E) continue;
         const uint64_t g = pfx_find_posting(P, e);
+        if (e >= P.E) continue;
         const uint64_t k = P.eoff[g + 1] - P.eoff[g];
         const uint64_t a = g - k + (e - P.eoff[g]);
         const unsigned long long kg = P.pkey[g], ka = P.pkey[a];
@@ -275,28 +291,6 @@ __global__ void __launch_bounds__(256) prefix_encounters(PrefixParams P) {
         const uint32_t nr = P.sizes[rr], ns = P.sizes[ss];
         const uint32_t* Tr = P.tokens + P.offsets[rr];
         const uint32_t* Ts = P.tokens + P.offsets[ss];
-        if (P.adapt) {
-            // AdaptJoin (src/join.cpp:330-420): the walks use prefixes of
-            // ell = 1..ell_max and the index holds ell_max prefixes, so the
-            // first common token is taken over those.  cnt[l]: common tokens
-            // inside both records' (l + 1)-prefixes = the pair's match count
-            // in the walk at ell = l + 1 (touched iff > 0).
-            if (spans_intersect(Tr, i, Ts, pos)) continue;
-            uint32_t cnt[kAdaptMaxEll];
-            bool inwin, bskip;
-            long long minov;
-            adapt_pair(P, rr, ss, nr, ns, Tr, Ts, i, pos, cnt, inwin, bskip, minov);
-            const bool bpruned = bskip && cnt[0] > 0;
-            const int ell = P.a_ell[r];  // verify pass: the row's final walk
-            if (!inwin || bpruned || cnt[ell - 1] < static_cast<uint32_t>(ell)) continue;
-            // (verified is counted per row by adapt_rows)
-            uint32_t ov = 0;
-            if (pfx_verify(Ts, ns, Tr, nr, minov, ov)) {
-                pfx_count(acc, kPcMatched, 1);
-                pfx_emit(P, s, r, ov);
-            }
-            continue;
-        }
         // first common prefix token of the pair?  (tokens before i / pos are smaller)
         if (spans_intersect(Tr, i, Ts, pos)) continue;
         const unsigned long long factor =
@@ -386,8 +380,8 @@ __global__ void __launch_bounds__(256) adapt_tally(PrefixParams P) {
     for (unsigned long long e = start; e < Eround; e += stride) {
         uint32_t key = 0xFFFFFFFFu, tmask = 0, amask = 0, btv = 0;
         bool lenp = false, bmpp = false;
+        const uint64_t g = pfx_find_posting(P, e);
         if (e < P.E) {
-            const uint64_t g = pfx_find_posting(P, e);
             const uint64_t k = P.eoff[g + 1] - P.eoff[g];
             const uint64_t a = g - k + (e - P.eoff[g]);
             const uint32_t r = static_cast<uint32_t>(P.pkey[g]), s = static_cast<uint32_t>(P.pkey[a]);
@@ -432,6 +426,42 @@ __global__ void __launch_bounds__(256) adapt_tally(PrefixParams P) {
             }
         }
     }
+}
+
+// AdaptJoin verify pass: the candidates of each probe row's final walk.
+__global__ void __launch_bounds__(256) adapt_verify(PrefixParams P) {
+    unsigned long long acc[kPcResults];
+#pragma unroll
+    for (int k = 0; k < kPcResults; ++k) acc[k] = 0;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned long long start = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const unsigned long long Eround = (P.E + 31) / 32 * 32;
+    for (unsigned long long e = start; e < Eround; e += stride) {
+        const uint64_t g = pfx_find_posting(P, e);
+        if (e >= P.E) continue;
+        const uint64_t k = P.eoff[g + 1] - P.eoff[g];
+        const uint64_t a = g - k + (e - P.eoff[g]);
+        const uint32_t r = static_cast<uint32_t>(P.pkey[g]), s = static_cast<uint32_t>(P.pkey[a]);
+        const uint32_t i = P.ppos[g], pos = P.ppos[a];
+        const uint32_t nr = P.sizes[r], ns = P.sizes[s];
+        const uint32_t* Tr = P.tokens + P.offsets[r];
+        const uint32_t* Ts = P.tokens + P.offsets[s];
+        if (spans_intersect(Tr, i, Ts, pos)) continue;
+        uint32_t cnt[kAdaptMaxEll];
+        bool inwin, bskip;
+        long long minov;
+        adapt_pair(P, r, s, nr, ns, Tr, Ts, i, pos, cnt, inwin, bskip, minov);
+        const bool bpruned = bskip && cnt[0] > 0;
+        const int ell = P.a_ell[r];  // the row's final walk
+        if (!inwin || bpruned || cnt[ell - 1] < static_cast<uint32_t>(ell)) continue;
+        // (verified is counted per row by adapt_rows)
+        uint32_t ov = 0;
+        if (pfx_verify(Ts, ns, Tr, nr, minov, ov)) {
+            pfx_count(acc, kPcMatched, 1);
+            pfx_emit(P, s, r, ov);
+        }
+    }
+    pfx_flush(P, acc);
 }
 
 // ------------------------------------------------------------- index build

@@ -316,3 +316,23 @@ def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim)
                                        + c["pruned_bitmap"] + c["verified"])
             assert c["matched"] == len(got.pairs)
             assert c == want.counters, (sim, algo, trial)
+
+
+@pytest.mark.parametrize("mean", [3.0, 40.0, 400.0])
+def test_sketch_build_heavy_tail(lib, oracle, mean):
+    """Heavy-tailed sizes: the tail rows go to the CTA-per-record build kernel
+    (build_sketches_big); every Set / Xor store (with and without the
+    multiplicative hash, 64..512 bits) equals the oracle's
+    (reference src/bitmap.cpp:66-88,145-158)."""
+    rng = np.random.default_rng(int(mean))
+    n = 3000
+    sizes = np.minimum(np.maximum(1, rng.lognormal(np.log(mean), 1.2, n).astype(np.int64)), 20000)
+    sizes[-5:] = [5000, 9000, 12000, 17000, 20000]
+    recs = [np.unique(rng.integers(0, 200000, int(z))).tolist() for z in sizes]
+    coll = S.Collection.from_records(lib, recs)
+    t, o = coll.csr()
+    for method in (capi.SSJ_BITMAP_SET, capi.SSJ_BITMAP_XOR):
+        for bits, h in ((64, 0), (128, 1), (256, 0), (512, 1)):
+            got = S.build_bitmaps(coll, method, bits, h)
+            want = oracle.build_bitmaps(t, o, method, bits, h)
+            assert (got == want).all(), (mean, method, bits, h)
