@@ -894,21 +894,30 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
     P.lpr_log2 = lg;
     P.total_tokens = rep.tokens_total;
     // rows longer than ~4 rounds of their lane group (sizes ascend with the
-    // row) go to the CTA-per-record kernel
-    uint32_t big0 = row1;
+    // row) go to a warp per record, rows above 4096 tokens to the
+    // CTA-per-record kernel
+    uint32_t mid0 = row1, big0 = row1;
     if (rep.src && !rep.src->first_ge.empty() && !env_u64("SSJB_BUILD_NO_BIG", 0)) {
-        const uint64_t s_big = static_cast<uint64_t>(16) << lg << 2;  // 4 x 16 tokens per lane
-        if (s_big <= rep.src->max_size)
-            big0 = std::max<uint32_t>(row0, std::min<uint32_t>(row1, rep.src->first_ge[s_big + 1]));
+        auto first_above = [&](uint64_t z) {
+            return z >= rep.src->max_size ? row1
+                                          : std::max<uint32_t>(row0, std::min<uint32_t>(row1, rep.src->first_ge[z + 1]));
+        };
+        const uint64_t s_mid = static_cast<uint64_t>(16) << lg << 2;  // 4 x 16 tokens per lane
+        big0 = first_above(std::max<uint64_t>(s_mid, 4096));
+        mid0 = lg < 5 ? std::min(first_above(s_mid), big0) : big0;
     }
-    if (big0 > row0) {
-        P.n = big0;
-        const uint64_t threads = static_cast<uint64_t>(big0 - row0) << lg;
-        const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-        fn<<<grid, 256, 0, s>>>(P);
+    auto launch_sub = [&](uint32_t a, uint32_t b, int lgr) {
+        if (b <= a) return;
+        P.row0 = a;
+        P.n = b;
+        P.lpr_log2 = lgr;
+        const uint64_t threads = static_cast<uint64_t>(b - a) << lgr;
+        fn<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(P);
         ++launches;
         CK(cudaGetLastError());
-    }
+    };
+    launch_sub(row0, mid0, lg);
+    launch_sub(mid0, big0, 5);
     if (big0 < row1) {
         P.row0 = big0;
         P.n = row1;

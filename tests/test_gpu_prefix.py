@@ -94,3 +94,27 @@ def test_prefix_joins_survive_result_overflow(lib, gp, monkeypatch):
         assert sha(rep.pairs) == c["pairs_sha256"], c["id"]
         done.add(algo)
     assert done == {1, 2, 3, 4, 5}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_prefix_joins_full_size(lib, name):
+    """Full-size BASELINE-shaped collections (C1 tau 0.9, C2 tau 0.8, C3 tau
+    0.5 with 203.6M pairs): pairs sha256 and all nine counters equal the
+    reference's own single-threaded runs (tests/golden/prefix_large.jsonl,
+    make_golden_prefix_large.py)."""
+    from paper_1711_07295_b200 import datasets as D
+    with open(os.path.join(GOLDEN_DIR, "prefix_large.jsonl")) as f:
+        cases = [json.loads(l) for l in f if l.strip()]
+    cases = [c for c in cases if c["config"] == name]
+    assert cases
+    coll = getattr(D, name)(lib)
+    t, o = coll.csr()
+    assert hashlib.sha256(np.ascontiguousarray(t).tobytes() + np.ascontiguousarray(o).tobytes()).hexdigest() == \
+        cases[0]["collection_sha256"]
+    for c in cases:
+        rep = S.join(coll, options_of(lib, c))
+        where = (name, c["algo"], c["bitmap"])
+        assert rep.counters == c["counters"], (where, rep.counters, c["counters"])
+        assert len(rep.pairs) == c["pair_count"] and sha(rep.pairs) == c["pairs_sha256"], where
+        del rep
