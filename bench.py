@@ -484,7 +484,7 @@ def secondary_workloads(lib, args, device, l2):
     through ssj_join.  Reported beside the headline, not part of it."""
     import torch
 
-    from paper_1711_07295_b200 import datasets as D
+    from paper_1711_07295_b200 import capi, datasets as D
     from paper_1711_07295_b200 import ssjoin as S
     from concurrent.futures import ThreadPoolExecutor
     out = {}
@@ -525,6 +525,27 @@ def secondary_workloads(lib, args, device, l2):
                      "matches": r3.counters["matched"], "verify_ms": r3.extra["ms_verify"],
                      "verify_bytes": r3.extra["verify_bytes"],
                      "workload": "C3 KOSARAK-shaped (606,770 sets, tau 1/2, Bitmap-Next b=64), ssj_join, warm"}
+    # the Bitmap Filter inside the prefix-filter algorithms (GPU
+    # prefix-filter engine), PPJOIN with the bitmap as filter3 on C3; the
+    # reference's own single-threaded run of the same join is in
+    # tests/golden/prefix_large.jsonl (counters and pair sha checked here too)
+    ref = None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "prefix_large.jsonl")) as f:
+            ref = next(d for d in map(json.loads, f) if d["config"] == "c3" and d["algo"] == 2 and d["bitmap"] == "f3")
+    except (OSError, StopIteration):
+        pass
+    po = S.default_options(lib, algorithm=capi.SSJ_ALGO_PPJOIN, threshold=(1, 2), bitmap_enabled=1)
+    S.join(c3, po)
+    t0 = time.perf_counter()
+    rp = S.join(c3, po)
+    dt = time.perf_counter() - t0
+    out["C3_ppjoin_bitmap_e2e"] = {
+        "join_s": dt, "encounters": rp.extra.get("window_pairs"), "matches": rp.counters["matched"],
+        "workload": "C3, ssj_join(PPJOIN, tau 1/2, bitmap filter3): GPU prefix-filter engine",
+        "reference_join_s": ref and ref["join_s"],
+        "reference_note": "unmodified reference, 1 thread, build container (tests/golden/prefix_large.jsonl)",
+        "same_counters_as_reference": bool(ref) and rp.counters == ref["counters"]}
     return out
 
 

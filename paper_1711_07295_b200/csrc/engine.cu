@@ -893,38 +893,45 @@ bool launch_build_sub(const DeviceReplica& rep, uint64_t* bits, uint64_t* bits2,
     while (lg < 5 && (1 << lg) * 4.0 < mean / 4.0 + 1.0) ++lg;
     P.lpr_log2 = lg;
     P.total_tokens = rep.tokens_total;
-    // rows longer than ~4 rounds of their lane group (sizes ascend with the
-    // row) go to a warp per record, rows above 4096 tokens to the
-    // CTA-per-record kernel
-    uint32_t mid0 = row1, big0 = row1;
-    if (rep.src && !rep.src->first_ge.empty() && !env_u64("SSJB_BUILD_NO_BIG", 0)) {
+    // Size tiers (sizes ascend with the row, so each tier is a row range):
+    // 2^k lanes for records of (8 << k, 16 << k] tokens -- about four 16-byte
+    // chunks per lane, four loads in flight -- a warp up to 4096 tokens, one
+    // CTA per record above.  Without sizes (no host collection) one launch
+    // with lanes from the mean size.
+    if (rep.src && !rep.src->first_ge.empty() && !env_u64("SSJB_BUILD_ONE_TIER", 0)) {
         auto first_above = [&](uint64_t z) {
             return z >= rep.src->max_size ? row1
                                           : std::max<uint32_t>(row0, std::min<uint32_t>(row1, rep.src->first_ge[z + 1]));
         };
-        const uint64_t s_mid = static_cast<uint64_t>(16) << lg << 2;  // 4 x 16 tokens per lane
-        big0 = first_above(std::max<uint64_t>(s_mid, 4096));
-        mid0 = lg < 5 ? std::min(first_above(s_mid), big0) : big0;
+        auto launch_tier = [&](uint32_t a, uint32_t b, int lgr) {
+            if (b <= a) return;
+            P.row0 = a;
+            P.n = b;
+            P.lpr_log2 = lgr;
+            const uint64_t threads = static_cast<uint64_t>(b - a) << lgr;
+            fn<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(P);
+            ++launches;
+            CK(cudaGetLastError());
+        };
+        uint32_t at = row0;
+        for (int k = 0; k <= 5 && at < row1; ++k) {
+            const uint32_t e = first_above(k < 5 ? (uint64_t(16) << k) : 4096);
+            launch_tier(at, e, k);
+            at = std::max(at, e);
+        }
+        if (at < row1) {
+            P.row0 = at;
+            P.n = row1;
+            build_sub_fn(width / 64, bits2 ? width2 / 64 : 0, method == Method::Xor, true)<<<row1 - at, 256, 0, s>>>(P);
+            ++launches;
+            CK(cudaGetLastError());
+        }
+        return true;
     }
-    auto launch_sub = [&](uint32_t a, uint32_t b, int lgr) {
-        if (b <= a) return;
-        P.row0 = a;
-        P.n = b;
-        P.lpr_log2 = lgr;
-        const uint64_t threads = static_cast<uint64_t>(b - a) << lgr;
-        fn<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(P);
-        ++launches;
-        CK(cudaGetLastError());
-    };
-    launch_sub(row0, mid0, lg);
-    launch_sub(mid0, big0, 5);
-    if (big0 < row1) {
-        P.row0 = big0;
-        P.n = row1;
-        build_sub_fn(width / 64, bits2 ? width2 / 64 : 0, method == Method::Xor, true)<<<row1 - big0, 256, 0, s>>>(P);
-        ++launches;
-        CK(cudaGetLastError());
-    }
+    const uint64_t threads = static_cast<uint64_t>(row1 - row0) << lg;
+    fn<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(P);
+    ++launches;
+    CK(cudaGetLastError());
     return true;
 }
 

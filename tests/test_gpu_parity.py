@@ -318,12 +318,15 @@ def test_prefix_filter_algorithm_codes_return_the_reference_pairs(lib, ref, sim)
             assert c == want.counters, (sim, algo, trial)
 
 
+@pytest.mark.parametrize("tiers", ["1", "0"])
 @pytest.mark.parametrize("mean", [3.0, 40.0, 400.0])
-def test_sketch_build_heavy_tail(lib, oracle, mean):
-    """Heavy-tailed sizes: the tail rows go to the CTA-per-record build kernel
-    (build_sketches_big); every Set / Xor store (with and without the
-    multiplicative hash, 64..512 bits) equals the oracle's
+def test_sketch_build_heavy_tail(lib, oracle, mean, tiers, monkeypatch):
+    """Heavy-tailed sizes: the build runs in size tiers (2^k lanes per record,
+    a warp, one CTA per record for the tail rows: build_sketches_big), or as
+    one launch (SSJB_BUILD_ONE_TIER=1); every Set / Xor store (with and without
+    the multiplicative hash, 64..512 bits) equals the oracle's
     (reference src/bitmap.cpp:66-88,145-158)."""
+    monkeypatch.setenv("SSJB_BUILD_ONE_TIER", "0" if tiers == "1" else "1")
     rng = np.random.default_rng(int(mean))
     n = 3000
     sizes = np.minimum(np.maximum(1, rng.lognormal(np.log(mean), 1.2, n).astype(np.int64)), 20000)

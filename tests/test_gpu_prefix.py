@@ -118,3 +118,26 @@ def test_prefix_joins_full_size(lib, name):
         assert rep.counters == c["counters"], (where, rep.counters, c["counters"])
         assert len(rep.pairs) == c["pair_count"] and sha(rep.pairs) == c["pairs_sha256"], where
         del rep
+
+
+@pytest.mark.gpu
+def test_prefix_joins_delivery_entry_points(lib, gp):
+    """ssjb_join_count and ssjb_join_stream take the prefix-filter codes too:
+    the same counters, and the streamed chunks concatenate to the pair list."""
+    cases, arr = gp
+    seen = set()
+    for c in cases:
+        algo = c["options"]["algorithm"]
+        if algo in seen or c["pair_count"] < 50:
+            continue
+        seen.add(algo)
+        name = c["collection"]
+        coll = S.Collection.from_csr(lib, arr[f"coll/{name}/tokens"], arr[f"coll/{name}/offsets"])
+        o = options_of(lib, c)
+        assert S.join_count(coll, o).counters == c["counters"], c["id"]
+        chunks = []
+        rep = S.join_stream(coll, o, lambda a: chunks.append(a.copy()), chunk_pairs=17)
+        assert rep.counters == c["counters"], c["id"]
+        got = np.concatenate(chunks) if chunks else np.zeros(0, dtype=S.PAIR_DTYPE)
+        assert len(got) == c["pair_count"] and sha(got) == c["pairs_sha256"], c["id"]
+    assert seen == {1, 2, 3, 4, 5}
