@@ -1405,6 +1405,40 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
     return t;
 }
 
+// The tiling of the collection's last join with the same rows, window and
+// tile shape (host cache on the Collection: repeated joins skip rebuilding
+// and re-ordering millions of work items).
+struct TilingCacheEntry {
+    size_t row_begin = 0, row_end = 0;
+    int64_t p = 0, q = 0;
+    uint32_t tile_rows = 0;
+    bool ordered = false;
+    Tiling tl;
+};
+
+std::shared_ptr<const Tiling> cached_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows,
+                                            bool ordered) {
+    {
+        std::lock_guard<std::mutex> lk(c.plan_cache_mu);
+        auto e = std::static_pointer_cast<TilingCacheEntry>(c.plan_cache);
+        if (e && e->row_begin == plan.row_begin && e->row_end == plan.row_end && e->p == plan.p && e->q == plan.q &&
+            e->tile_rows == tile_rows && e->ordered == ordered && !plan.naive)
+            return std::shared_ptr<const Tiling>(e, &e->tl);
+    }
+    auto e = std::make_shared<TilingCacheEntry>();
+    e->tl = make_tiling(c, plan, tile_rows, ordered);
+    if (plan.naive) return std::shared_ptr<const Tiling>(e, &e->tl);
+    e->row_begin = plan.row_begin;
+    e->row_end = plan.row_end;
+    e->p = plan.p;
+    e->q = plan.q;
+    e->tile_rows = tile_rows;
+    e->ordered = ordered;
+    std::lock_guard<std::mutex> lk(c.plan_cache_mu);
+    c.plan_cache = e;
+    return std::shared_ptr<const Tiling>(e, &e->tl);
+}
+
 // Zeroes the per-(item, row) survivor counts of the items at claim positions
 // [k0, k1) of a column-chunk-major order (the items a batch has not processed).
 __global__ void zero_item_counts(const uint32_t* order, uint64_t k0, uint64_t k1, uint32_t* counts,
@@ -2052,7 +2086,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     }
     // K3a: exact head-token overlaps for the large-record region of dense joins
     // (head_tc.cuh); active whenever the join runs the level-2 GEMM
+    hmark("plan tables");
     const HeadPlan hplan = use_tc && W <= 2 && W2 == 4 ? make_head_plan(c, plan, W2) : HeadPlan{};
+    hmark("head plan");
     // a head region of >= 2^30 window pairs of large records means a dense join:
     // start on the level-2 GEMM instead of discovering it by a level-1 pass
     // that overflows (C4: the discarded pass and its operands)
@@ -2077,7 +2113,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     const bool use_tcm = use_tc && !l2gemm && !fp4 && !use_tc2 && !noext && W <= 2 && env_u64("SSJB_TCM", 1) != 0;
 
     // work items: (row tile, 4096-column chunk); the pair kernel takes 256-row tiles
-    Tiling tl;
+    std::shared_ptr<const Tiling> tlp = std::make_shared<Tiling>();
     uint64_t* d_item_base = nullptr;
     uint32_t* d_col_lo = nullptr;
     uint32_t* d_item_tile = nullptr;
@@ -2087,14 +2123,15 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     const bool item_ordered = use_tc && !use_tc2 && n >= env_u64("SSJB_ORDER_MIN_ROWS", 262144) &&
                               env_u64("SSJB_STREAM", 1) < 2 && env_u64("SSJB_ITEM_ORDER", 1) != 0;
     auto set_tiling = [&](uint32_t tile_rows) {
-        tl = make_tiling(c, plan, tile_rows, item_ordered);
-        stage.add(&d_item_base, tl.item_base.data(), tl.item_base.size() * 8);
-        stage.add(&d_col_lo, tl.col_lo.data(), tl.col_lo.size() * 4);
-        stage.add(&d_item_tile, tl.item_tile.data(), tl.item_tile.size() * 4);
-        if (!tl.order.empty()) stage.add(&d_item_order, tl.order.data(), tl.order.size() * 4);
+        tlp = cached_tiling(c, plan, tile_rows, item_ordered);
+        stage.add(&d_item_base, tlp->item_base.data(), tlp->item_base.size() * 8);
+        stage.add(&d_col_lo, tlp->col_lo.data(), tlp->col_lo.size() * 4);
+        stage.add(&d_item_tile, tlp->item_tile.data(), tlp->item_tile.size() * 4);
+        if (!tlp->order.empty()) stage.add(&d_item_order, tlp->order.data(), tlp->order.size() * 4);
         stage.flush(A, s, st.h2d_bytes);
     };
     set_tiling(use_tc2 || use_tcm ? 2 * dev::kRowTile : dev::kRowTile);
+    hmark("tiling staged");
 
     // the collection on the device: a pinned replica, or uploaded for this join --
     // streamed in row chunks (overlapping the first chunks' sketches and filter
@@ -2113,7 +2150,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         static thread_local cudaStream_t copy_streams[16] = {};
         if (!copy_streams[device & 15])
             CK(cudaStreamCreateWithFlags(&copy_streams[device & 15], cudaStreamNonBlocking));
-        rep = upload_streamed(c, device, s, copy_streams[device & 15], tl.tile_rows,
+        rep = upload_streamed(c, device, s, copy_streams[device & 15], tlp->tile_rows,
                               static_cast<int>(env_u64("SSJB_STREAM_CHUNKS", 2)), st.h2d_bytes, st.launches, ingest,
                               ingest_t16, ingest_d8);
     } else if (!rep) {
@@ -2241,12 +2278,12 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     uint32_t* d_jstar = A.alloc<uint32_t>(rows + 1);
     uint32_t* d_satlist = A.alloc<uint32_t>(rows + 1);
     // per-(item,row) survivor counts let the saturation rescan touch one chunk per row
-    uint64_t n_items = tl.item_base.back();
-    const uint64_t ic_bytes = n_items * tl.tile_rows * 4;
+    uint64_t n_items = tlp->item_base.back();
+    const uint64_t ic_bytes = n_items * tlp->tile_rows * 4;
     const bool keep_item_counts =
         !naive && (ic_bytes <= (uint64_t(1) << 30) ||
                    (ic_bytes <= (uint64_t(16) << 30) && static_cast<double>(ic_bytes) <= 0.3 * double(live_free())));
-    uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * tl.tile_rows) : nullptr;
+    uint32_t* d_item_counts = keep_item_counts ? A.alloc<uint32_t>(n_items * tlp->tile_rows) : nullptr;
     // second level: per (item, filter tile, column part, row) counts written by the
     // tcgen05 epilogue (plain u16 stores, no memset: every slot of a processed
     // tile is written), so a saturated row's rescan covers one filter tile
@@ -2255,7 +2292,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     const uint64_t tc_bytes = n_items * kTilesPerItem * 4 * dev::kRowTile * 2;
     // (kept for the dense regime only -- the level-2 GEMM joins, where most rows
     // saturate; elsewhere the stores cost the filter more than the rescan saves)
-    uint16_t* d_tile_counts = keep_item_counts && use_tc && l2gemm && !use_tc2 && tl.tile_rows == dev::kRowTile &&
+    uint16_t* d_tile_counts = keep_item_counts && use_tc && l2gemm && !use_tc2 && tlp->tile_rows == dev::kRowTile &&
                                       tc_bytes <= std::min<uint64_t>(uint64_t(2) << 30, live_free() / 5)
                                   ? A.alloc<uint16_t>(n_items * kTilesPerItem * 4 * dev::kRowTile)
                                   : nullptr;
@@ -2307,7 +2344,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     FP.item_counts = d_item_counts;
     FP.ctl = d_ctl;
     FP.surv_cap = surv_cap;
-    FP.ntiles = tl.ntiles;
+    FP.ntiles = tlp->ntiles;
     FP.row_begin = static_cast<uint32_t>(plan.row_begin);
     FP.row_end = static_cast<uint32_t>(plan.row_end);
     FP.cutoff = enabled ? plan.bitmap.cutoff : kUnlimited;
@@ -2341,7 +2378,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         TP.tiles_per_item = kTilesPerItem;
         TP.ctl = d_ctl;
         TP.surv_cap = surv_cap;
-        TP.ntiles = tl.ntiles;
+        TP.ntiles = tlp->ntiles;
         TP.row_begin = static_cast<uint32_t>(plan.row_begin);
         TP.row_end = static_cast<uint32_t>(plan.row_end);
         TP.cutoff = FP.cutoff;
@@ -2444,13 +2481,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         CK(cudaMemsetAsync(&d_ctl->results, 0, 8, s));
     };
 
-    uint64_t total_items = tl.item_base.back();
+    uint64_t total_items = tlp->item_base.back();
     auto launch_filter = [&](uint64_t ib, uint64_t ie, uint32_t tb, bool keep_survivors = false,
                              bool zero_counts = true) {
         if (!keep_survivors) CK(cudaMemsetAsync(&d_ctl->survivors, 0, 8, s));
         CK(cudaMemsetAsync(&d_ctl->work_next, 0, 8, s));
         if (d_item_counts && ie > ib && zero_counts)
-            CK(cudaMemsetAsync(d_item_counts + ib * tl.tile_rows, 0, (ie - ib) * tl.tile_rows * 4, s));
+            CK(cudaMemsetAsync(d_item_counts + ib * tlp->tile_rows, 0, (ie - ib) * tlp->tile_rows * 4, s));
         if (ie <= ib) return;
         FP.item_begin = ib;
         FP.item_end = ie;
@@ -2497,7 +2534,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.wstart = d_wstart;
             RP.rowcnt = d_rowcnt;
             RP.item_counts = d_item_counts;
-            RP.tile_rows = tl.tile_rows;
+            RP.tile_rows = tlp->tile_rows;
             RP.tile_counts = use_tc ? TP.tile_counts : nullptr;
             RP.tiles_per_item = kTilesPerItem;
             RP.tile_cols = static_cast<uint32_t>(tck.nt);
@@ -2570,9 +2607,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 if (variant_s == 4)
                     launch_column_info(sk->bits, W, ch.r0, last ? n_pad : ch.r1, sk->npc2, s, st.launches);
                 if (stream_filter) {  // filter work items of this chunk's row tiles
-                    const uint32_t ta = ch.r0 / tl.tile_rows;
-                    const uint32_t tb2 = last ? tl.ntiles : ch.r1 / tl.tile_rows;
-                    launch_filter(tl.item_base[ta], tl.item_base[tb2], ta, k > 0);
+                    const uint32_t ta = ch.r0 / tlp->tile_rows;
+                    const uint32_t tb2 = last ? tlp->ntiles : ch.r1 / tlp->tile_rows;
+                    launch_filter(tlp->item_base[ta], tlp->item_base[tb2], ta, k > 0);
                 }
             }
         return filter_chunks;
@@ -2665,17 +2702,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
                 uint8_t* b1 = A.alloc<uint8_t>(static_cast<size_t>(n_pad) * rowb);
                 launch_expand(sk->bits, W, sk->bits2, W2, rep->sizes, a1, b1, n_pad, 1, s, st.launches);
                 l2gemm = true;
-                if (tl.tile_rows != dev::kRowTile) {
+                if (tlp->tile_rows != dev::kRowTile) {
                     // the level-2 GEMM kernel takes 128-row work items
                     tc2_active = false;
                     set_tiling(dev::kRowTile);
-                    total_items = n_items = tl.item_base.back();
+                    total_items = n_items = tlp->item_base.back();
                     TP.item_base = d_item_base;
                     TP.item_tile = d_item_tile;
                     TP.item_order = item_ordered ? d_item_order : nullptr;
                     TP.tile_col_lo = d_col_lo;
-                    TP.ntiles = tl.ntiles;
-                    if (d_item_counts && n_items * tl.tile_rows * 4 <= ic_bytes) {
+                    TP.ntiles = tlp->ntiles;
+                    if (d_item_counts && n_items * tlp->tile_rows * 4 <= ic_bytes) {
                         TP.item_counts = d_item_counts;  // same buffer, fewer/equal bytes
                     } else {
                         d_item_counts = nullptr;
@@ -2747,20 +2784,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         auto zero_unprocessed = [&](uint64_t k0) {
             if (!d_item_counts || total_items <= k0) return;
             if (ordered) {
-                const uint64_t cnt = (total_items - k0) * tl.tile_rows;
+                const uint64_t cnt = (total_items - k0) * tlp->tile_rows;
                 zero_item_counts<<<static_cast<unsigned>(std::min<uint64_t>((cnt + 255) / 256, uint64_t(sms) * 16)), 256,
-                                   0, s>>>(TP.item_order, k0, total_items, d_item_counts, tl.tile_rows);
+                                   0, s>>>(TP.item_order, k0, total_items, d_item_counts, tlp->tile_rows);
                 ++st.launches;
                 CK(cudaGetLastError());
             } else {
-                CK(cudaMemsetAsync(d_item_counts + k0 * tl.tile_rows, 0, (total_items - k0) * tl.tile_rows * 4, s));
+                CK(cudaMemsetAsync(d_item_counts + k0 * tlp->tile_rows, 0, (total_items - k0) * tlp->tile_rows * 4, s));
             }
         };
         zero_unprocessed(ib);
         while (ib < total_items) {
-            const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tl.item_base.begin(), tl.item_base.end(), ib) -
-                                                      tl.item_base.begin() - 1);
-            const uint32_t rb = ordered ? 0u : tb * tl.tile_rows;  // rows this launch may touch: [rb, rows)
+            const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tlp->item_base.begin(), tlp->item_base.end(), ib) -
+                                                      tlp->item_base.begin() - 1);
+            const uint32_t rb = ordered ? 0u : tb * tlp->tile_rows;  // rows this launch may touch: [rb, rows)
             CK(cudaMemcpyAsync(d_rowsnap + rb, d_rowcnt + rb, (rows - rb) * 4ull, cudaMemcpyDeviceToDevice, s));
             FP.surv_soft = soft;
             TP.surv_soft = soft;
@@ -3538,6 +3575,16 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
             PP.a_bmp = tallies + 3 * nL;
             PP.a_bt = tallies + 4 * nL;
             uint8_t* ell = A.alloc<uint8_t>(n);
+            // candidate list of the tally pass (10 B per pair), bounded by free HBM;
+            // if it overflows the verify pass re-enumerates the encounters instead
+            {
+                size_t fb = 0, tb = 0;
+                CK(cudaMemGetInfo(&fb, &tb));
+                PP.a_cand_cap = std::min<uint64_t>(std::max<uint64_t>(E, 1), fb / 4 / 10);
+                PP.a_cand_cap = std::min<uint64_t>(PP.a_cand_cap, env_u64("SSJB_ADAPT_LIST_CAP", ~uint64_t(0)));
+                PP.a_cand = A.alloc<uint2>(PP.a_cand_cap);
+                PP.a_cmask = A.alloc<uint16_t>(PP.a_cand_cap);
+            }
             if (E) dev::adapt_tally<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
             ++st.launches;
             CK(cudaGetLastError());
@@ -3564,7 +3611,12 @@ void engine_prefix_join(const Collection& c, const Options& o, int device, Engin
             ++st.launches;
             CK(cudaGetLastError());
             PP.a_ell = ell;
-            if (E) dev::adapt_verify<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            const uint64_t ncand = read_u64(ctr + dev::kPcCand, s);
+            if (ncand <= PP.a_cand_cap) {
+                if (ncand) dev::adapt_verify_list<<<grid_for(ncand, sms, 8), 256, 0, s>>>(PP, ncand);
+            } else if (E) {
+                dev::adapt_verify<<<grid_for(E, sms, 8), 256, 0, s>>>(PP);
+            }
             ++st.launches;
             CK(cudaGetLastError());
         } else if (E) {

@@ -105,6 +105,10 @@ struct Collection {
     mutable std::vector<uint32_t> exc_start;
     mutable std::vector<uint16_t> exc_val;
     mutable bool use_delta8 = false;
+    // engine-owned host cache of the last join's work-item tiling (keyed by
+    // the plan; repeated joins with the same options skip rebuilding it)
+    mutable std::mutex plan_cache_mu;
+    mutable std::shared_ptr<void> plan_cache;
     ~Collection();
 };
 

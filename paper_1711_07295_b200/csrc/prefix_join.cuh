@@ -38,6 +38,7 @@ enum PfxCounter {
     kPcMatched,
     kPcResults,   // result slots claimed (may exceed the buffer: overflow)
     kPcItems,     // group-pair expansion items claimed
+    kPcCand,      // AdaptJoin candidate-list entries claimed
     kPcSlots
 };
 
@@ -82,6 +83,9 @@ struct PrefixParams {
     uint32_t* a_bmp;                  // [ell_max][n] bitmap-pruned (touched)
     uint32_t* a_bt;                   // [n] bitmap predicate evaluations of the first walk
     const uint8_t* a_ell;             // [n] final ell per probe row (verify pass)
+    uint2* a_cand;                    // tally pass: pairs (s, r) that survive some walk
+    uint16_t* a_cmask;                // bit l: the pair is a candidate of the walk at ell = l + 1
+    unsigned long long a_cand_cap;
 };
 
 __device__ __forceinline__ uint32_t pfx_rec(const PrefixParams& P, uint32_t id) {
@@ -403,6 +407,13 @@ __global__ void __launch_bounds__(256) adapt_tally(PrefixParams P) {
                     if (l < L && cnt[l]) tmask |= 1u << l;
                     if (l < L && cnt[l] >= static_cast<uint32_t>(l + 1)) amask |= 1u << l;
                 }
+                if (P.a_cand && !lenp && !bmpp && amask) {  // verified iff its row ends on such a walk
+                    const unsigned long long slot = warp_claim(P.ctr + kPcCand);
+                    if (slot < P.a_cand_cap) {
+                        P.a_cand[slot] = make_uint2(s, r);
+                        P.a_cmask[slot] = static_cast<uint16_t>(amask);
+                    }
+                }
             }
         }
         const unsigned grp = __match_any_sync(0xFFFFFFFFu, key);
@@ -457,6 +468,32 @@ __global__ void __launch_bounds__(256) adapt_verify(PrefixParams P) {
         // (verified is counted per row by adapt_rows)
         uint32_t ov = 0;
         if (pfx_verify(Ts, ns, Tr, nr, minov, ov)) {
+            pfx_count(acc, kPcMatched, 1);
+            pfx_emit(P, s, r, ov);
+        }
+    }
+    pfx_flush(P, acc);
+}
+
+// AdaptJoin verify over the tally pass's candidate list (when it fit): the
+// pairs whose probe row's final walk (a_ell) keeps them.
+__global__ void __launch_bounds__(256) adapt_verify_list(PrefixParams P, unsigned long long count) {
+    unsigned long long acc[kPcResults];
+#pragma unroll
+    for (int k = 0; k < kPcResults; ++k) acc[k] = 0;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned long long cround = (count + 31) / 32 * 32;
+    for (unsigned long long k = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < cround;
+         k += stride) {
+        if (k >= count) continue;
+        const uint2 pr = P.a_cand[k];
+        const uint32_t s = pr.x, r = pr.y;
+        const int ell = P.a_ell[r];
+        if (!((P.a_cmask[k] >> (ell - 1)) & 1u)) continue;
+        const uint32_t nr = P.sizes[r], ns = P.sizes[s];
+        const long long minov = need_overlap(P.need, nr, ns);
+        uint32_t ov = 0;
+        if (pfx_verify(P.tokens + P.offsets[s], ns, P.tokens + P.offsets[r], nr, minov, ov)) {
             pfx_count(acc, kPcMatched, 1);
             pfx_emit(P, s, r, ov);
         }

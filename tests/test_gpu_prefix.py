@@ -79,9 +79,12 @@ def test_prefix_joins_match_reference_fixtures(lib, gp, algo):
 @pytest.mark.gpu
 def test_prefix_joins_survive_result_overflow(lib, gp, monkeypatch):
     """A result buffer smaller than the output (SSJB_PREFIX_RESULT_CAP) makes
-    the engine re-run with the exact size: same pairs and counters."""
+    the engine re-run with the exact size, and an AdaptJoin candidate list that
+    does not fit (SSJB_ADAPT_LIST_CAP) falls back to re-enumerating the
+    encounters: same pairs and counters."""
     cases, arr = gp
     monkeypatch.setenv("SSJB_PREFIX_RESULT_CAP", "1000")
+    monkeypatch.setenv("SSJB_ADAPT_LIST_CAP", "3")  # AdaptJoin: verify by re-enumeration
     done = set()
     for c in cases:
         algo = c["options"]["algorithm"]
