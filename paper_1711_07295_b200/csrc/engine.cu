@@ -1524,6 +1524,51 @@ HeadPlan make_head_plan(const Collection& c, const JoinPlan& plan, int W2) {
     return h;
 }
 
+// make_head_plan of the collection's last join with the same rows, threshold,
+// level-2 width and SSJB_HEAD* settings (host cache on the Collection, next to
+// the tiling: the region's sampled token counts and work items are a few ms).
+struct HeadPlanCacheEntry {
+    size_t row_begin = 0, row_end = 0;
+    std::vector<int32_t> minov;
+    int W2 = 0;
+    std::string env;
+    std::shared_ptr<const HeadPlan> hp;
+};
+
+std::string head_env_key() {
+    std::string k;
+    for (const char* v : {"SSJB_HEAD", "SSJB_HEAD_KIND", "SSJB_HEAD_K", "SSJB_HEAD_MIN_SIZE"}) {
+        const char* x = std::getenv(v);
+        k += x ? x : "-";
+        k += '|';
+    }
+    return k;
+}
+
+std::shared_ptr<const HeadPlan> cached_head_plan(const Collection& c, const JoinPlan& plan, int W2) {
+    const std::string env = head_env_key();
+    const bool cacheable = !plan.naive && !plan.cosine && plan.bitmap.enabled;
+    {
+        std::lock_guard<std::mutex> lk(c.plan_cache_mu);
+        auto e = std::static_pointer_cast<HeadPlanCacheEntry>(c.head_cache);
+        if (cacheable && e && e->row_begin == plan.row_begin && e->row_end == plan.row_end && e->W2 == W2 &&
+            e->env == env && e->minov == plan.minov)
+            return e->hp;
+    }
+    auto hp = std::make_shared<const HeadPlan>(make_head_plan(c, plan, W2));
+    if (!cacheable) return hp;
+    auto e = std::make_shared<HeadPlanCacheEntry>();
+    e->row_begin = plan.row_begin;
+    e->row_end = plan.row_end;
+    e->minov = plan.minov;
+    e->W2 = W2;
+    e->env = env;
+    e->hp = hp;
+    std::lock_guard<std::mutex> lk(c.plan_cache_mu);
+    c.head_cache = e;
+    return hp;
+}
+
 // Device side of the head plan: head selection (token counts over the region,
 // count threshold for the K most frequent, dense indices), the head operand
 // and the per-row (size, tail) info.  Everything lives in the join's arena.
@@ -2087,7 +2132,9 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // K3a: exact head-token overlaps for the large-record region of dense joins
     // (head_tc.cuh); active whenever the join runs the level-2 GEMM
     hmark("plan tables");
-    const HeadPlan hplan = use_tc && W <= 2 && W2 == 4 ? make_head_plan(c, plan, W2) : HeadPlan{};
+    std::shared_ptr<const HeadPlan> hplan_p =
+        use_tc && W <= 2 && W2 == 4 ? cached_head_plan(c, plan, W2) : std::make_shared<const HeadPlan>();
+    const HeadPlan& hplan = *hplan_p;
     hmark("head plan");
     // a head region of >= 2^30 window pairs of large records means a dense join:
     // start on the level-2 GEMM instead of discovering it by a level-1 pass

@@ -109,6 +109,7 @@ struct Collection {
     // the plan; repeated joins with the same options skip rebuilding it)
     mutable std::mutex plan_cache_mu;
     mutable std::shared_ptr<void> plan_cache;
+    mutable std::shared_ptr<void> head_cache;
     ~Collection();
 };
 
