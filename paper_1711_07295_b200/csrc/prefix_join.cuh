@@ -257,25 +257,20 @@ __device__ __forceinline__ void adapt_pair(const PrefixParams& P, uint32_t rr, u
     inwin = ns >= P.lower[nr] && ns <= P.upper[nr];
     minov = need_overlap(P.need, nr, ns);
     bskip = inwin && P.bits && pfx_bitmap_skip(P, rr, ss, nr, ns, minov);
-    // a common token at (ii, pp) counts for walk l iff it lies in both
-    // (l + 1)-prefixes: ii < plen_l(|r|) and pp < plen_l(|s|); the prefix
-    // lengths are loaded once per pair
-    uint32_t lr[kAdaptMaxEll], ls[kAdaptMaxEll];
 #pragma unroll
-    for (int l = 0; l < kAdaptMaxEll; ++l) {
-        cnt[l] = 0;
-        lr[l] = l < L ? static_cast<uint32_t>(P.plen_ell[l * ms1 + nr]) : 0u;
-        ls[l] = l < L ? static_cast<uint32_t>(P.plen_ell[l * ms1 + ns]) : 0u;
-    }
+    for (int l = 0; l < kAdaptMaxEll; ++l) cnt[l] = 0;
     uint32_t ii = i, pp = pos;
-    const uint32_t plr_max = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + nr]);
-    const uint32_t pls_max = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + ns]);
+    const uint32_t plr = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + nr]);
+    const uint32_t pls = static_cast<uint32_t>(P.plen_ell[(L - 1) * ms1 + ns]);
     do {
 #pragma unroll
-        for (int l = 0; l < kAdaptMaxEll; ++l) cnt[l] += (ii < lr[l]) & (pp < ls[l]);
+        for (int l = 0; l < kAdaptMaxEll; ++l)
+            if (l < L && ii < static_cast<uint32_t>(P.plen_ell[l * ms1 + nr]) &&
+                pp < static_cast<uint32_t>(P.plen_ell[l * ms1 + ns]))
+                ++cnt[l];
         ++ii;
         ++pp;
-    } while (next_common(Tr, plr_max, Ts, pls_max, ii, pp));
+    } while (next_common(Tr, plr, Ts, pls, ii, pp));
 }
 
 // One thread per encounter; the thread holding a pair's first common prefix
