@@ -1364,7 +1364,8 @@ struct Tiling {
     std::vector<uint32_t> order;      // claim order -> item id (column-chunk-major), empty: identity
 };
 
-Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows, bool ordered = false) {
+Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows, bool ordered = false,
+                   uint32_t split_tile = 0) {
     Tiling t;
     t.tile_rows = tile_rows;
     const size_t rows = plan.row_end - plan.row_begin;
@@ -1389,10 +1390,16 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
         // claim order: items by the 4096-column bucket of their first column
         // (counting sort, stable in tile order), so the CTAs working at once
         // stream the same column operands from L2
-        const size_t nb = c.size() / dev::kColChunk + 2;
+        // (split_tile > 0: the items of tiles [0, split_tile) come first, each
+        // group column-chunk-major -- a streamed join filters them while the
+        // rest of the collection is still in flight)
+        const size_t nb1 = c.size() / dev::kColChunk + 2;
+        const size_t nb = split_tile ? 2 * nb1 : nb1;
         std::vector<uint64_t> at(nb + 1, 0);
         auto bucket = [&](uint32_t k, uint64_t item) {
-            return std::min<size_t>(nb - 1, (t.col_lo[k] + (item - t.item_base[k]) * dev::kColChunk) / dev::kColChunk);
+            const size_t b = std::min<size_t>(nb1 - 1, (t.col_lo[k] + (item - t.item_base[k]) * dev::kColChunk) /
+                                                           dev::kColChunk);
+            return split_tile && k >= split_tile ? nb1 + b : b;
         };
         for (uint32_t k = 0; k < t.ntiles; ++k)
             for (uint64_t it = t.item_base[k]; it < t.item_base[k + 1]; ++it) ++at[bucket(k, it) + 1];
@@ -1411,28 +1418,29 @@ Tiling make_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows
 struct TilingCacheEntry {
     size_t row_begin = 0, row_end = 0;
     int64_t p = 0, q = 0;
-    uint32_t tile_rows = 0;
+    uint32_t tile_rows = 0, split_tile = 0;
     bool ordered = false;
     Tiling tl;
 };
 
 std::shared_ptr<const Tiling> cached_tiling(const Collection& c, const JoinPlan& plan, uint32_t tile_rows,
-                                            bool ordered) {
+                                            bool ordered, uint32_t split_tile = 0) {
     {
         std::lock_guard<std::mutex> lk(c.plan_cache_mu);
         auto e = std::static_pointer_cast<TilingCacheEntry>(c.plan_cache);
         if (e && e->row_begin == plan.row_begin && e->row_end == plan.row_end && e->p == plan.p && e->q == plan.q &&
-            e->tile_rows == tile_rows && e->ordered == ordered && !plan.naive)
+            e->tile_rows == tile_rows && e->split_tile == split_tile && e->ordered == ordered && !plan.naive)
             return std::shared_ptr<const Tiling>(e, &e->tl);
     }
     auto e = std::make_shared<TilingCacheEntry>();
-    e->tl = make_tiling(c, plan, tile_rows, ordered);
+    e->tl = make_tiling(c, plan, tile_rows, ordered, split_tile);
     if (plan.naive) return std::shared_ptr<const Tiling>(e, &e->tl);
     e->row_begin = plan.row_begin;
     e->row_end = plan.row_end;
     e->p = plan.p;
     e->q = plan.q;
     e->tile_rows = tile_rows;
+    e->split_tile = split_tile;
     e->ordered = ordered;
     std::lock_guard<std::mutex> lk(c.plan_cache_mu);
     c.plan_cache = e;
@@ -2169,8 +2177,34 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // (tcgen05 single-CTA kernels; per-chunk streamed filter launches keep item order)
     const bool item_ordered = use_tc && !use_tc2 && n >= env_u64("SSJB_ORDER_MIN_ROWS", 262144) &&
                               env_u64("SSJB_STREAM", 1) < 2 && env_u64("SSJB_ITEM_ORDER", 1) != 0;
+    // The collection on the device: a pinned replica, or uploaded for this join --
+    // streamed in row chunks when the whole self-join runs here.  A dense join
+    // (batch mode from the start) streams a small first chunk (1/16 of the
+    // tokens, SSJB_STREAM_CHUNKS_BATCH) whose rows' work items (C4: ~57% of the
+    // filter work) are claimed first and filtered while the rest is in flight.
+    std::shared_ptr<DeviceReplica> rep;
+    {
+        std::lock_guard<std::mutex> lk(c.dev_mu);
+        if (c.pinned[device & 15] && c.pinned[device & 15]->device == device) rep = c.pinned[device & 15];
+    }
+    const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
+    const bool will_stream = !rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n &&
+                             n >= env_u64("SSJB_STREAM_MIN_ROWS", 65536) && n > 0 && env_u64("SSJB_STREAM", 1) != 0;
+    const bool two_phase = will_stream && head_upfront && env_u64("SSJB_STREAM", 1) < 2 &&
+                           env_u64("SSJB_STREAM_PHASES", 1) != 0;
+    const int stream_chunks = static_cast<int>(two_phase ? std::max<uint64_t>(2, env_u64("SSJB_STREAM_CHUNKS_BATCH", 16))
+                                                         : env_u64("SSJB_STREAM_CHUNKS", 2));
+    const uint32_t phase_tile_rows = use_tc2 || use_tcm ? 2 * dev::kRowTile : dev::kRowTile;
+    uint32_t split_row = 0;  // first row of the second streaming phase (upload_streamed's first chunk end)
+    if (two_phase) {
+        const uint64_t target = c.tokens.size() / static_cast<uint64_t>(stream_chunks);
+        const size_t r = std::lower_bound(c.offsets.begin(), c.offsets.end(), target) - c.offsets.begin();
+        split_row = static_cast<uint32_t>(std::min<size_t>(n, (r + phase_tile_rows - 1) / phase_tile_rows * phase_tile_rows));
+        if (split_row >= n) split_row = 0;
+    }
     auto set_tiling = [&](uint32_t tile_rows) {
-        tlp = cached_tiling(c, plan, tile_rows, item_ordered);
+        tlp = cached_tiling(c, plan, tile_rows, item_ordered,
+                            split_row && tile_rows == phase_tile_rows ? split_row / tile_rows : 0);
         stage.add(&d_item_base, tlp->item_base.data(), tlp->item_base.size() * 8);
         stage.add(&d_col_lo, tlp->col_lo.data(), tlp->col_lo.size() * 4);
         stage.add(&d_item_tile, tlp->item_tile.data(), tlp->item_tile.size() * 4);
@@ -2180,30 +2214,22 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     set_tiling(use_tc2 || use_tcm ? 2 * dev::kRowTile : dev::kRowTile);
     hmark("tiling staged");
 
-    // the collection on the device: a pinned replica, or uploaded for this join --
-    // streamed in row chunks (overlapping the first chunks' sketches and filter
-    // work with the rest of the transfer) when the whole self-join runs here
-    std::shared_ptr<DeviceReplica> rep;
-    {
-        std::lock_guard<std::mutex> lk(c.dev_mu);
-        if (c.pinned[device & 15] && c.pinned[device & 15]->device == device) rep = c.pinned[device & 15];
-    }
     std::vector<IngestChunk> ingest;
     uint16_t* ingest_t16 = nullptr;
     Delta8Dev ingest_d8;
-    const bool set_or_xor = plan.bitmap.method == Method::Set || plan.bitmap.method == Method::Xor;
-    if (!rep && use_tc && set_or_xor && W <= 8 && plan.row_begin == 0 && plan.row_end == n &&
-        n >= env_u64("SSJB_STREAM_MIN_ROWS", 65536) && n > 0 && env_u64("SSJB_STREAM", 1) != 0) {
+    if (will_stream) {
         static thread_local cudaStream_t copy_streams[16] = {};
         if (!copy_streams[device & 15])
             CK(cudaStreamCreateWithFlags(&copy_streams[device & 15], cudaStreamNonBlocking));
-        rep = upload_streamed(c, device, s, copy_streams[device & 15], tlp->tile_rows,
-                              static_cast<int>(env_u64("SSJB_STREAM_CHUNKS", 2)), st.h2d_bytes, st.launches, ingest,
-                              ingest_t16, ingest_d8);
+        rep = upload_streamed(c, device, s, copy_streams[device & 15], tlp->tile_rows, stream_chunks, st.h2d_bytes,
+                              st.launches, ingest, ingest_t16, ingest_d8);
     } else if (!rep) {
         rep = replica_for(c, device, s, st.h2d_bytes, st.launches);
     }
     const bool streamed = !ingest.empty();
+    size_t ingest_pending = 0;  // first chunk whose ingest kernels are not enqueued yet (two-phase streaming)
+    uint64_t phase_items = 0;   // claim positions [0, phase_items) read only the first chunk's rows
+    uint64_t* l3_bits = nullptr;
     cudaEvent_t e_up = T.mark();
     const uint32_t n_pad = static_cast<uint32_t>(((n + kPadRows) + 7) & ~size_t(7));
     const bool resident = rep->stream == nullptr;
@@ -2466,7 +2492,10 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     auto enable_level3 = [&]() {
         if (VP.bits3 || W2 != 4 || naive || env_u64("SSJB_L3", 1) == 0) return;
         uint64_t* b3 = A.alloc<uint64_t>((n + kPadRows + 8) * 8);
-        launch_build_sub(*rep, b3, nullptr, Method::Xor, 512, 0, plan.bitmap.hash, s, st.launches);
+        // (two-phase streaming: the rows still in flight are built by finish_ingest)
+        launch_build_sub(*rep, b3, nullptr, Method::Xor, 512, 0, plan.bitmap.hash, s, st.launches, 0,
+                         ingest_pending ? split_row : static_cast<uint32_t>(n));
+        l3_bits = b3;
         VP.bits3 = b3;
         VP.maxham = d_maxham;
         VP.l3_min_sum = static_cast<uint32_t>(env_u64("SSJB_L3_MIN", 128));
@@ -2626,13 +2655,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     // Streamed ingest: per row chunk (as its tokens land) decode / widen, build
     // the sketches and expand the operands; with filter_chunks also launch the
     // chunk's filter work items.  Returns filter_chunks.
-    auto stream_ingest = [&](bool filter_chunks) {
+    auto stream_ingest = [&](bool filter_chunks, size_t k_begin = 0, size_t k_end = SIZE_MAX) {
             const int variant_s = variant;
             // per-chunk filter launches (SSJB_STREAM=2) overlap more of the transfer
             // but pay a launch tail per chunk; by default only the ingest kernels
             // (decode, sketches, operands) are chunked
             const bool stream_filter = filter_chunks;
-            for (size_t k = 0; k < ingest.size(); ++k) {
+            for (size_t k = k_begin; k < std::min(k_end, ingest.size()); ++k) {
                 const IngestChunk& ch = ingest[k];
                 CK(cudaStreamWaitEvent(s, ch.ev, 0));
                 if (ingest_d8.bytes)
@@ -2665,7 +2694,17 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
     bool done = false;
     const auto t_launch = Clock::now();  // host setup ends: the first filter launch
     auto t_synced = t_launch;
-    if (head_upfront && streamed) stream_ingest(false);  // (batch mode from the start: ingest only)
+    // batch mode from the start: ingest only -- in two phases, the first chunk
+    // now and the rest once the batches reach items outside it
+    if (head_upfront && streamed) {
+        if (two_phase && ingest.size() > 1 && ingest[0].r1 == split_row) {
+            stream_ingest(false, 0, 1);
+            ingest_pending = 1;
+            phase_items = tlp->item_base[split_row / tlp->tile_rows];
+        } else {
+            stream_ingest(false);
+        }
+    }
     if (!head_upfront) {
         cudaEvent_t a = T.mark();
         if (streamed) {
@@ -2780,9 +2819,20 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         }
     }
 
-    for (auto& ch : ingest) CK(cudaEventDestroy(ch.ev));
-    if (ingest_t16) CK(cudaFreeAsync(ingest_t16, s));
-    free_delta8(ingest_d8, s);
+    auto finish_ingest = [&]() {
+        if (ingest_pending) {
+            stream_ingest(false, ingest_pending);
+            if (l3_bits) launch_build_sub(*rep, l3_bits, nullptr, Method::Xor, 512, 0, plan.bitmap.hash, s, st.launches,
+                                           split_row, static_cast<uint32_t>(n));
+            ingest_pending = 0;
+        }
+        for (auto& ch : ingest) CK(cudaEventDestroy(ch.ev));
+        ingest.clear();
+        if (ingest_t16) CK(cudaFreeAsync(ingest_t16, s));
+        ingest_t16 = nullptr;
+        free_delta8(ingest_d8, s);
+    };
+    if (!ingest_pending) finish_ingest();
 
     if (!done) {
         // Survivor batches.  Grow the survivor / result buffers toward the first
@@ -2842,6 +2892,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         };
         zero_unprocessed(ib);
         while (ib < total_items) {
+            if (ingest_pending && ib >= phase_items) finish_ingest();
             const uint32_t tb = static_cast<uint32_t>(std::upper_bound(tlp->item_base.begin(), tlp->item_base.end(), ib) -
                                                       tlp->item_base.begin() - 1);
             const uint32_t rb = ordered ? 0u : tb * tlp->tile_rows;  // rows this launch may touch: [rb, rows)
@@ -2849,7 +2900,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             FP.surv_soft = soft;
             TP.surv_soft = soft;
             cudaEvent_t a = T.mark();
-            const uint64_t ie = std::min(total_items, ib + span);
+            const uint64_t ie = std::min(ingest_pending ? phase_items : total_items, ib + span);
             launch_filter(ib, ie, tb, false, false);
             cudaEvent_t b = T.mark();
             CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
@@ -2883,6 +2934,7 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             }
             ib += processed;
         }
+        finish_ingest();  // (no-op unless every item fit the first phase)
         FP.surv_soft = 0;
         TP.surv_soft = 0;
         if (head_active) {
