@@ -90,6 +90,22 @@ def test_every_golden_join(lib, golden, colls, flavour, monkeypatch):
         assert_same(rep, e, flavour)
 
 
+@pytest.mark.parametrize("chunks", ["2", "5"])
+def test_two_phase_streamed_ingest(lib, golden, colls, chunks, monkeypatch):
+    """Dense joins stream in two phases: the first chunk's work items are
+    filtered (and verified) while the rest of the collection is in flight;
+    every fixture with the head kernel forced, first chunks of 1/2 and 1/5 of
+    the tokens, and the saturated-row rescan on its side stream and inline."""
+    set_filter(monkeypatch, "tc-head")
+    monkeypatch.setenv("SSJB_STREAM", "1")
+    monkeypatch.setenv("SSJB_STREAM_MIN_ROWS", "1")
+    monkeypatch.setenv("SSJB_STREAM_CHUNKS_BATCH", chunks)
+    monkeypatch.setenv("SSJB_RESCAN_SIDE", "1" if chunks == "2" else "0")
+    for e in golden["joins"]:
+        rep = S.join(colls(e["collection"]), options_of(lib, e))
+        assert_same(rep, e, "two-phase " + chunks)
+
+
 @pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("flavour", ["tc-i8", "tc-i8-pair", "tc-fp4", "tc-head"])
 def test_streamed_ingest(lib, golden, colls, flavour, mode, monkeypatch):
