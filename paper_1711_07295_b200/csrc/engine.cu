@@ -2599,9 +2599,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         ++st.launches;
         CK(cudaGetLastError());
     };
-    auto launch_counters = [&]() {
+    // K2b: the saturated-row rescan (on `rs`, default the join stream) and the
+    // counter reduction (on the join stream; with reduce = false the caller
+    // launches it later)
+    auto launch_counters = [&](cudaStream_t rs = nullptr, bool rescan = true, bool reduce = true) {
         if (!rows) return;
-        if (!naive) {
+        if (!rs) rs = s;
+        if (!naive && rescan) {
             dev::RescanParams RP{};
             RP.bits = d_bits;
             RP.sizes = rep->sizes;
@@ -2627,12 +2631,13 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             RP.sat_list = d_satlist;
             RP.sat_count = &d_ctl->sat_rows;
             const unsigned gf = static_cast<unsigned>(std::min<uint64_t>((rows + 255) / 256, uint64_t(sms) * 8));
-            dev::find_saturated<<<gf, 256, 0, s>>>(d_rowcnt, rows, plan.capacity, d_satlist, d_ctl);
+            dev::find_saturated<<<gf, 256, 0, rs>>>(d_rowcnt, rows, plan.capacity, d_satlist, d_ctl);
             const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, uint64_t(sms) * 8));
-            dev::rescan_saturated<<<g, 256, 0, s>>>(RP);
+            dev::rescan_saturated<<<g, 256, 0, rs>>>(RP);
             st.launches += 2;
             CK(cudaGetLastError());
         }
+        if (!reduce) return;
         dev::CountParams CP{};
         CP.sizes = rep->sizes;
         CP.wstart = d_wstart;
@@ -2937,6 +2942,23 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
         finish_ingest();  // (no-op unless every item fit the first phase)
         FP.surv_soft = 0;
         TP.surv_soft = 0;
+        // with K3a to run, the saturated-row rescan (it reads only the filter's
+        // row / item counts and the level-1 sketches) runs on a side stream
+        // next to the head kernel; the counter reduction waits for it
+        cudaStream_t side = nullptr;
+        cudaEvent_t ev_side0 = nullptr, ev_side1 = nullptr;
+        if (head_active && !naive && rows && env_u64("SSJB_RESCAN_SIDE", 1) != 0) {
+            static thread_local cudaStream_t side_streams[16] = {};
+            if (!side_streams[device & 15])
+                CK(cudaStreamCreateWithFlags(&side_streams[device & 15], cudaStreamNonBlocking));
+            side = side_streams[device & 15];
+            CK(cudaEventCreate(&ev_side0));
+            CK(cudaEventCreate(&ev_side1));
+            CK(cudaEventRecord(ev_side0, s));
+            CK(cudaStreamWaitEvent(side, ev_side0, 0));
+            launch_counters(side, true, false);
+            CK(cudaEventRecord(ev_side1, side));
+        }
         if (head_active) {
             // K3a over the large-record region (K2 counted those pairs but did not
             // emit them): batches with a soft survivor cap, each verified by K3
@@ -3027,11 +3049,23 @@ void engine_join(const Collection& c, const JoinPlan& plan, int device, EngineRe
             st.head_k = hplan.K;
         }
         cudaEvent_t r0 = T.mark();
-        launch_counters();
+        if (side) {
+            CK(cudaStreamWaitEvent(s, ev_side1, 0));
+            launch_counters(s, false, true);
+        } else {
+            launch_counters();
+        }
         cudaEvent_t r1 = T.mark();
         CK(cudaMemcpyAsync(&h_ctl, d_ctl, sizeof(h_ctl), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         st.ms_rescan = Timer::ms(r0, r1);
+        if (side) {
+            float side_ms = 0;
+            CK(cudaEventElapsedTime(&side_ms, ev_side0, ev_side1));
+            st.ms_rescan += side_ms;  // (overlapped with K3a)
+            CK(cudaEventDestroy(ev_side0));
+            CK(cudaEventDestroy(ev_side1));
+        }
         flush_results(res_count);
     }
 
