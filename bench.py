@@ -87,10 +87,12 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("SSJB_BENCH_NO_CLOCKS"):  # (diagnostics only: a line without clocks is not a bench value)
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -281,6 +283,8 @@ def run_ours(args):
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+            if debug:
+                print(f"[bench] resident step {len(times)}: {times[-1]:.2f} ms", file=sys.stderr)
             reps_last = reps
             launches += sum(r.extra["launches"] for r in reps)
             window += sum(r.counters["candidates"] for r in reps)
