@@ -20,7 +20,7 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "prefix_large.jsonl")
-TAU = {"c1": (9, 10), "c2": (4, 5), "c3": (1, 2)}
+TAU = {"c1": (9, 10), "c2": (4, 5), "c3": (1, 2), "c4": (7, 10)}
 JOBS = ([("c1", a, "f3") for a in (1, 2, 3, 4, 5)] + [("c1", a, "f2") for a in (1, 2, 3)] +
         [("c2", a, "f3") for a in (1, 2, 3, 4, 5)] + [("c2", 1, "f2"), ("c2", 3, "f2")] +
         [("c3", a, "f3") for a in (1, 2, 3, 4)] + [("c3", 2, "f2")])
