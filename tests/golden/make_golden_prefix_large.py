@@ -2,7 +2,8 @@
 """Full-size prefix-filter joins from the UNMODIFIED reference
 (oracle/_ref/libssjoin_ref.so): ALLPAIRS / PPJOIN / PPJOIN+ / GROUPJOIN /
 ADAPTJOIN with the Bitmap Filter (filter3, and filter2 for some) on the
-BASELINE-shaped C1 (tau 0.9), C2 (tau 0.8) and C3 (tau 0.5) collections
+BASELINE-shaped C1 (tau 0.9), C2 (tau 0.8), C3 (tau 0.5) and C4 (tau 0.7,
+ALLPAIRS, PPJOIN and GROUPJOIN: ~9-10 min each) collections
 (paper_1711_07295_b200.datasets).  One process per join (single-threaded, as
 the reference runs these algorithms), several in parallel; each records the
 collection sha256, the options, the full pair list's count and sha256, the
@@ -23,7 +24,8 @@ OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "prefix_large.jso
 TAU = {"c1": (9, 10), "c2": (4, 5), "c3": (1, 2), "c4": (7, 10)}
 JOBS = ([("c1", a, "f3") for a in (1, 2, 3, 4, 5)] + [("c1", a, "f2") for a in (1, 2, 3)] +
         [("c2", a, "f3") for a in (1, 2, 3, 4, 5)] + [("c2", 1, "f2"), ("c2", 3, "f2")] +
-        [("c3", a, "f3") for a in (1, 2, 3, 4)] + [("c3", 2, "f2")])
+        [("c3", a, "f3") for a in (1, 2, 3, 4)] + [("c3", 2, "f2")] +
+        [("c4", a, "f3") for a in (1, 2, 4)])
 
 
 def one(name, algo, bl):

@@ -100,12 +100,12 @@ def test_prefix_joins_survive_result_overflow(lib, gp, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_prefix_joins_full_size(lib, name):
     """Full-size BASELINE-shaped collections (C1 tau 0.9, C2 tau 0.8, C3 tau
-    0.5 with 203.6M pairs): pairs sha256 and all nine counters equal the
-    reference's own single-threaded runs (tests/golden/prefix_large.jsonl,
-    make_golden_prefix_large.py)."""
+    0.5 with 203.6M pairs, C4 tau 0.7 with 42.4M pairs): pairs sha256 and all
+    nine counters equal the reference's own single-threaded runs
+    (tests/golden/prefix_large.jsonl, make_golden_prefix_large.py)."""
     from paper_1711_07295_b200 import datasets as D
     with open(os.path.join(GOLDEN_DIR, "prefix_large.jsonl")) as f:
         cases = [json.loads(l) for l in f if l.strip()]
